@@ -205,8 +205,8 @@ int orc_bicg_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double
  *     den = <rh,v>                         breakdown if scalar_breaks
  *     alpha = rho/den
  *     s_i = r_i - alpha*v_i;  z_i = dinv_i*s_i;  x_i = x_i + alpha*y_i
- *     t = A z;  tt = <t,t>;  ts = <t,s>    breakdown if scalar_breaks(tt)
- *     omega = ts/tt
+ *     t = A z;  tt = <t,t>;  ts = <t,s>    breakdown if tt != 0 && scalar_breaks(tt)
+ *     omega = tt == 0 ? 0 : ts/tt          (t = 0: s vanished, finish below)
  *     x_i = x_i + omega*z_i;  r_i = s_i - omega*t_i
  *     rho_prev = rho; iterations = iter
  *     sigma = <r,r>                        breakdown if !isfinite
@@ -272,8 +272,10 @@ int orc_bicgstab_solve(int64_t n, const int64_t* rp, const int64_t* ci, const do
         orc_spmv(n, rp, ci, va, z, t);
         const double tt = reduce_prod(&pc, n, t, t);
         const double ts = reduce_prod(&pc, n, t, s);
-        if (scalar_breaks(tt)) { out->breakdown = 1; break; }
-        omega = ts / tt;
+        /* tt == 0 exactly: t = 0, i.e. s already vanished; omega = 0 lets the
+         * convergence test below finish the solve (x = x + alpha*y). */
+        if (tt != 0.0 && scalar_breaks(tt)) { out->breakdown = 1; break; }
+        omega = tt == 0.0 ? 0.0 : ts / tt;
         for (int64_t i = 0; i < n; ++i) {
             x[i] = x[i] + omega * z[i];
             r[i] = s[i] - omega * t[i];

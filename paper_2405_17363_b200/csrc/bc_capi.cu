@@ -1,0 +1,670 @@
+// bc_capi.cu -- C ABI (include/blockcells_b200.h): validation mirroring the
+// reference's exceptions, group planning (plan_kernel / solve_block_cells),
+// device memory, kernel launches, the LU fallback and merge_groups.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "bc_block.cuh"
+#include "bc_lu.cuh"
+#include "bc_newton.cuh"
+#include "bc_plan.hpp"
+#include "blockcells_b200.h"
+
+namespace {
+
+constexpr int kMaxDynSmem = 227 * 1024;
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(bytes, 256);
+        const cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct Status : std::runtime_error {
+    int code;
+    Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw Status(BC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+using BlockFn = void (*)(bc::BlockParams);
+
+struct KernelCfg {
+    int W, R, RV;
+    BlockFn fn[2];
+};
+
+#define BC_CFG(W, R, RV) \
+    {W, R, RV, {&bc::block_cells_kernel<bc::kBiCG, W, R, RV>, &bc::block_cells_kernel<bc::kBiCGStab, W, R, RV>}}
+
+const KernelCfg kConfigs[] = {
+    BC_CFG(1, 1, 1), BC_CFG(1, 2, 2), BC_CFG(1, 4, 4), BC_CFG(1, 8, 5), BC_CFG(1, 8, 8),
+    BC_CFG(2, 8, 5), BC_CFG(2, 8, 8), BC_CFG(4, 8, 5), BC_CFG(4, 8, 8), BC_CFG(8, 8, 5),
+    BC_CFG(8, 8, 8),
+};
+
+const KernelCfg* pick_config(const bc::Geometry& g) {
+    const KernelCfg* best = nullptr;
+    for (const KernelCfg& k : kConfigs)
+        if (k.W == g.W && k.R == g.R && k.RV >= g.RV && (!best || k.RV < best->RV)) best = &k;
+    return best;
+}
+
+}  // namespace
+
+struct bc_ctx {
+    int device = 0;
+    int sms = 0;
+    std::string err;
+    bool has_pattern = false;
+    bc::Pattern pat;
+    DevBuf d_rp, d_ci;
+    std::map<std::pair<int, int>, bc::GroupPlan> plans;  // (k, with_transpose)
+    std::vector<DevBuf> plan_bufs;
+    DevBuf values, rhs, x, giters, grms, gflags, counters, lu_scratch, lu_entries, lu_status,
+        f_scratch;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    int64_t launches = 0;
+    std::map<BlockFn, bool> smem_set;
+};
+
+namespace {
+
+thread_local std::string g_last_error;  // errors of context-free calls
+
+void set_err(bc_ctx* ctx, const std::string& m) {
+    g_last_error = m;
+    if (ctx) ctx->err = m;
+}
+
+template <class F>
+int guarded(bc_ctx* ctx, F&& f) {
+    try {
+        if (ctx) {
+            ctx->err.clear();
+            check_cuda(cudaSetDevice(ctx->device), "cudaSetDevice");
+        }
+        return f();
+    } catch (const Status& s) {
+        set_err(ctx, s.what());
+        return s.code;
+    } catch (const std::bad_alloc&) {
+        set_err(ctx, "out of host memory");
+        return BC_ERR_NO_MEMORY;
+    } catch (const std::exception& e) {
+        set_err(ctx, e.what());
+        return BC_ERR_INVALID_ARGUMENT;
+    }
+}
+
+void fail(int code, const std::string& m) { throw Status(code, m); }
+
+bc::Pattern make_pattern(int32_t species, const int32_t* row_ptr, const int32_t* col_idx) {
+    if (species < 1) fail(BC_ERR_INVALID_ARGUMENT, "batched system: no species");
+    if (!row_ptr || !col_idx) fail(BC_ERR_INVALID_ARGUMENT, "pattern: null pointer");
+    bc::Pattern p;
+    p.species = species;
+    p.row_ptr.assign(row_ptr, row_ptr + species + 1);
+    if (p.row_ptr[0] != 0) fail(BC_ERR_INVALID_ARGUMENT, "csr: row_ptr[0] != 0");
+    for (int i = 0; i < species; ++i)
+        if (p.row_ptr[i] > p.row_ptr[i + 1]) fail(BC_ERR_INVALID_ARGUMENT, "csr: row_ptr decreasing");
+    p.nnz = p.row_ptr[species];
+    p.col_idx.assign(col_idx, col_idx + p.nnz);
+    p.diag.assign(species, -1);
+    for (int i = 0; i < species; ++i)
+        for (int e = p.row_ptr[i]; e < p.row_ptr[i + 1]; ++e) {
+            if (p.col_idx[e] < 0 || p.col_idx[e] >= species)
+                fail(BC_ERR_INVALID_ARGUMENT, "csr: column index out of range");
+            if (e > p.row_ptr[i] && p.col_idx[e - 1] >= p.col_idx[e])
+                fail(BC_ERR_INVALID_ARGUMENT, "csr: columns not strictly increasing within a row");
+            if (p.col_idx[e] == i) p.diag[i] = e;
+        }
+    return p;
+}
+
+template <class T>
+T* upload(bc_ctx* ctx, const std::vector<T>& v) {
+    ctx->plan_bufs.emplace_back();
+    DevBuf& b = ctx->plan_bufs.back();
+    check_cuda(b.ensure(sizeof(T) * std::max<size_t>(v.size(), 1)), "cudaMalloc(plan)");
+    if (!v.empty())
+        check_cuda(cudaMemcpy(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice),
+                   "cudaMemcpy(plan)");
+    return b.as<T>();
+}
+
+bc::GroupPlan& get_plan(bc_ctx* ctx, const bc::Pattern& pat, int k, bool with_t,
+                        std::map<std::pair<int, int>, bc::GroupPlan>* cache) {
+    const auto key = std::make_pair(k, with_t ? 1 : 0);
+    auto it = cache->find(key);
+    if (it != cache->end()) return it->second;
+    bc::GroupPlan gp = bc::build_group_plan(pat, k, with_t);
+    gp.d_words = upload(ctx, gp.a.words);
+    gp.d_vpos = upload(ctx, gp.a.vpos);
+    gp.d_dpos = upload(ctx, gp.dpos);
+    if (with_t) {
+        gp.d_twords = upload(ctx, gp.at.words);
+        gp.d_tvpos = upload(ctx, gp.at.vpos);
+    }
+    return cache->emplace(key, std::move(gp)).first->second;
+}
+
+struct LaunchShape {
+    int teams = 1, blocks = 1, threads = 32;
+    size_t smem = 0;
+    int team_doubles = 0, sched_words = 0;
+};
+
+LaunchShape choose_shape(bc_ctx* ctx, BlockFn fn, const bc::GroupPlan& gp, bool bicg, int groups) {
+    const int W = gp.geo.W, LW = 32 * W;
+    const int n_pad = (gp.geo.n + 31) & ~31;
+    LaunchShape sh;
+    sh.sched_words = gp.a.steps * LW + (bicg ? gp.at.steps * LW : 0);
+    sh.sched_words = (sh.sched_words + 3) & ~3;
+    sh.team_doubles = gp.a.steps * LW + (bicg ? gp.at.steps * LW : 0) + n_pad * (bicg ? 4 : 2) +
+                      (W > 1 ? 8 * W * 32 : 0);
+    if (!ctx->smem_set[fn]) {
+        check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem),
+                   "cudaFuncSetAttribute");
+        ctx->smem_set[fn] = true;
+    }
+    int best_warps = -1;
+    const int gmax = std::min(W > 1 ? 15 : 32, 256 / LW);
+    for (int G = 1; G <= gmax; ++G) {
+        const size_t smem = sizeof(uint32_t) * sh.sched_words + sizeof(double) * G * sh.team_doubles;
+        if (smem > static_cast<size_t>(kMaxDynSmem)) break;
+        int nb = 0;
+        check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, G * LW, smem),
+                   "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+        const int warps = nb * G * W;
+        if (warps > best_warps) {
+            best_warps = warps;
+            sh.teams = G;
+            sh.smem = smem;
+            sh.blocks = nb;
+        }
+    }
+    if (best_warps <= 0) fail(BC_ERR_INVALID_ARGUMENT, "group does not fit in shared memory");
+    sh.threads = sh.teams * LW;
+    const int need = (groups + sh.teams - 1) / sh.teams;
+    sh.blocks = std::max(1, std::min(need, sh.blocks * ctx->sms));
+    return sh;
+}
+
+// Launch the fused kernel over `groups` groups of kc cells starting at cell0.
+void launch_block(bc_ctx* ctx, const bc::Pattern& pat, const bc::GroupPlan& gp, int algo,
+                  int64_t cell0, int64_t gout0, int groups, const double* values,
+                  const double* rhs, const double* x0, double* x, double tol, int64_t max_iter,
+                  unsigned int* counter, cudaStream_t st) {
+    const KernelCfg* cfg = pick_config(gp.geo);
+    if (!cfg) fail(BC_ERR_INVALID_ARGUMENT, "no kernel configuration for this group size");
+    const bool bicg = algo == BC_ALGO_BICG;
+    BlockFn fn = cfg->fn[bicg ? 0 : 1];
+    const LaunchShape sh = choose_shape(ctx, fn, gp, bicg, groups);
+    bc::BlockParams p{};
+    p.values = values;
+    p.rhs = rhs;
+    p.x0 = x0;
+    p.x_out = x;
+    p.g_iters = ctx->giters.as<int32_t>();
+    p.g_rms = ctx->grms.as<double>();
+    p.g_flags = ctx->gflags.as<uint8_t>();
+    p.words = gp.d_words;
+    p.twords = gp.d_twords;
+    p.vpos = gp.d_vpos;
+    p.tvpos = gp.d_tvpos;
+    p.dpos = gp.d_dpos;
+    p.counter = counter;
+    p.cell_offset = cell0;
+    p.group_offset = gout0;
+    p.group_count = groups;
+    p.n = gp.geo.n;
+    p.species = pat.species;
+    p.nnz = pat.nnz;
+    p.kc = gp.k;
+    p.S = gp.a.steps;
+    p.St = bicg ? gp.at.steps : 0;
+    p.P = gp.geo.P;
+    p.teams = sh.teams;
+    p.team_doubles = sh.team_doubles;
+    p.sched_words = sh.sched_words;
+    p.tol = tol;
+    p.max_iter = max_iter;
+    check_cuda(cudaMemsetAsync(counter, 0, sizeof(unsigned int), st), "cudaMemsetAsync(counter)");
+    fn<<<sh.blocks, sh.threads, sh.smem, st>>>(p);
+    check_cuda(cudaGetLastError(), "block_cells_kernel launch");
+    ctx->launches++;
+}
+
+struct GroupSpan {
+    int64_t cell0, gout0;
+    int k, count;
+};
+
+// plan_kernel (exec_model.cpp:102-161) + the group partition of
+// solve_block_cells (strategies.cpp:209-213).
+void plan_groups(const bc_solve_params* prm, int species, double* cpb, int64_t* n_groups,
+                 std::vector<GroupSpan>* spans) {
+    const int64_t mtpb = prm->max_threads_per_block > 0 ? prm->max_threads_per_block : 1024;
+    if (prm->cells < 1) fail(BC_ERR_INVALID_ARGUMENT, "batched system: no cells");
+    if (species > mtpb)
+        fail(BC_ERR_UNSUPPORTED_MECHANISM, "mechanism needs more threads per cell than a block provides");
+    int64_t k = 1;
+    switch (prm->strategy) {
+        case BC_STRATEGY_ONE_CELL:
+        case BC_STRATEGY_THREAD_PER_CELL:
+            *cpb = 1.0;
+            k = 1;
+            break;
+        case BC_STRATEGY_MULTI_CELLS:
+            *cpb = static_cast<double>(mtpb) / static_cast<double>(species);
+            *n_groups = 1;
+            if (spans) spans->push_back({0, 0, 0, 1});
+            return;
+        case BC_STRATEGY_BLOCK_CELLS:
+            if (prm->cells_per_block > 0) {
+                k = prm->cells_per_block;
+                if (k * species > mtpb)
+                    fail(BC_ERR_INVALID_GROUPING, "requested cells per block exceeds the thread budget");
+            } else if (prm->cells_per_block == 0) {
+                k = mtpb / species;
+            } else {
+                fail(BC_ERR_INVALID_ARGUMENT, "plan_kernel: cells per block must be >= 1");
+            }
+            *cpb = static_cast<double>(k);
+            break;
+        default:
+            fail(BC_ERR_INVALID_ARGUMENT, "run_strategy: unknown strategy");
+    }
+    const int64_t full = prm->cells / k, rem = prm->cells % k;
+    *n_groups = full + (rem ? 1 : 0);
+    if (spans) {
+        if (full) spans->push_back({0, 0, static_cast<int>(k), static_cast<int>(full)});
+        if (rem) spans->push_back({full * k, full, static_cast<int>(rem), 1});
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int bc_ctx_create(int device, bc_ctx** out) {
+    if (!out) return BC_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    bc_ctx* ctx = new (std::nothrow) bc_ctx;
+    if (!ctx) return BC_ERR_NO_MEMORY;
+    ctx->device = device;
+    const int st = guarded(ctx, [&] {
+        check_cuda(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device),
+                   "cudaDeviceGetAttribute");
+        int major = 0;
+        check_cuda(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device),
+                   "cudaDeviceGetAttribute");
+        if (major != 10) fail(BC_ERR_CUDA, "libbc_b200 is built for sm_100a (B200) only");
+        check_cuda(cudaEventCreate(&ctx->e0), "cudaEventCreate");
+        check_cuda(cudaEventCreate(&ctx->e1), "cudaEventCreate");
+        check_cuda(ctx->counters.ensure(64 * sizeof(unsigned int)), "cudaMalloc");
+        return BC_OK;
+    });
+    if (st != BC_OK) {
+        std::fprintf(stderr, "bc_ctx_create: %s\n", ctx->err.c_str());
+        delete ctx;
+        return st;
+    }
+    *out = ctx;
+    return BC_OK;
+}
+
+void bc_ctx_destroy(bc_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    for (DevBuf* b : {&ctx->d_rp, &ctx->d_ci, &ctx->values, &ctx->rhs, &ctx->x, &ctx->giters,
+                      &ctx->grms, &ctx->gflags, &ctx->counters, &ctx->lu_scratch,
+                      &ctx->lu_entries, &ctx->lu_status, &ctx->f_scratch})
+        b->release();
+    for (DevBuf& b : ctx->plan_bufs) b.release();
+    if (ctx->e0) cudaEventDestroy(ctx->e0);
+    if (ctx->e1) cudaEventDestroy(ctx->e1);
+    delete ctx;
+}
+
+const char* bc_last_error(const bc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
+
+int64_t bc_kernel_launches(const bc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int bc_set_pattern(bc_ctx* ctx, int32_t species, const int32_t* row_ptr, const int32_t* col_idx) {
+    if (!ctx) return BC_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        bc::Pattern p = make_pattern(species, row_ptr, col_idx);
+        for (auto& kv : ctx->plans) (void)kv;
+        ctx->plans.clear();
+        for (DevBuf& b : ctx->plan_bufs) b.release();
+        ctx->plan_bufs.clear();
+        check_cuda(ctx->d_rp.ensure(sizeof(int32_t) * p.row_ptr.size()), "cudaMalloc");
+        check_cuda(ctx->d_ci.ensure(sizeof(int32_t) * std::max<size_t>(p.col_idx.size(), 1)), "cudaMalloc");
+        check_cuda(cudaMemcpy(ctx->d_rp.p, p.row_ptr.data(), sizeof(int32_t) * p.row_ptr.size(),
+                              cudaMemcpyHostToDevice), "cudaMemcpy");
+        if (!p.col_idx.empty())
+            check_cuda(cudaMemcpy(ctx->d_ci.p, p.col_idx.data(), sizeof(int32_t) * p.col_idx.size(),
+                                  cudaMemcpyHostToDevice), "cudaMemcpy");
+        ctx->pat = std::move(p);
+        ctx->has_pattern = true;
+        return BC_OK;
+    });
+}
+
+int bc_plan(int32_t species, const bc_solve_params* prm, int64_t* n_groups, double* cpb) {
+    if (!prm || !n_groups || !cpb) return BC_ERR_INVALID_ARGUMENT;
+    return guarded(nullptr, [&] {
+        if (species < 1) fail(BC_ERR_INVALID_ARGUMENT, "batched system: no species");
+        plan_groups(prm, species, cpb, n_groups, nullptr);
+        return BC_OK;
+    });
+}
+
+int bc_schedule_export(int32_t species, const int32_t* row_ptr, const int32_t* col_idx, int32_t k,
+                       int32_t with_t, int32_t* info, uint32_t* words, int32_t* vpos, uint32_t* twords,
+                       int32_t* tvpos) {
+    if (!info || k < 1) return BC_ERR_INVALID_ARGUMENT;
+    return guarded(nullptr, [&] {
+        const bc::Pattern pat = make_pattern(species, row_ptr, col_idx);
+        const bc::GroupPlan gp = bc::build_group_plan(pat, k, with_t != 0);
+        const int v[8] = {gp.geo.n, gp.geo.P, gp.geo.Q, gp.geo.W, gp.geo.R, gp.geo.RV, gp.a.steps,
+                          with_t ? gp.at.steps : 0};
+        std::memcpy(info, v, sizeof v);
+        if (words) std::memcpy(words, gp.a.words.data(), sizeof(uint32_t) * gp.a.words.size());
+        if (vpos) std::memcpy(vpos, gp.a.vpos.data(), sizeof(int32_t) * gp.a.vpos.size());
+        if (with_t && twords) std::memcpy(twords, gp.at.words.data(), sizeof(uint32_t) * gp.at.words.size());
+        if (with_t && tvpos) std::memcpy(tvpos, gp.at.vpos.data(), sizeof(int32_t) * gp.at.vpos.size());
+        return BC_OK;
+    });
+}
+
+int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, const double* rhs,
+             double* x_out, int32_t* group_iters, double* group_rms, uint8_t* group_flags,
+             bc_report* report) {
+    if (!ctx || !prm) return BC_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&]() -> int {
+        if (!ctx->has_pattern) fail(BC_ERR_NO_PATTERN, "bc_set_pattern has not been called");
+        const bc::Pattern& pat = ctx->pat;
+        if (!values || !rhs || !x_out) fail(BC_ERR_INVALID_ARGUMENT, "null values/rhs/x_out");
+        double cpb = 0.0;
+        int64_t n_groups = 0;
+        std::vector<GroupSpan> spans;
+        plan_groups(prm, pat.species, &cpb, &n_groups, &spans);
+        if (!(prm->tol > 0.0)) fail(BC_ERR_INVALID_ARGUMENT, "bicg: tol must be positive");
+        if (prm->max_iter < 1) fail(BC_ERR_INVALID_ARGUMENT, "bicg: max_iter must be >= 1");
+        if (prm->algo != BC_ALGO_BICG && prm->algo != BC_ALGO_BICGSTAB_JACOBI)
+            fail(BC_ERR_INVALID_ARGUMENT, "unknown algorithm");
+        if (prm->strategy == BC_STRATEGY_MULTI_CELLS || prm->strategy == BC_STRATEGY_THREAD_PER_CELL)
+            fail(BC_ERR_INVALID_ARGUMENT, "strategy not available in this build");
+
+        cudaStream_t st = static_cast<cudaStream_t>(prm->stream);
+        const int64_t cells = prm->cells, s = pat.species, nnz = pat.nnz;
+        const size_t vbytes = sizeof(double) * cells * nnz, bbytes = sizeof(double) * cells * s;
+        const double* d_values = values;
+        const double* d_rhs = rhs;
+        double* d_x = x_out;
+        if (!is_device_ptr(values)) {
+            check_cuda(ctx->values.ensure(vbytes), "cudaMalloc(values)");
+            check_cuda(cudaMemcpyAsync(ctx->values.p, values, vbytes, cudaMemcpyHostToDevice, st), "H2D values");
+            d_values = ctx->values.as<double>();
+        }
+        if (!is_device_ptr(rhs)) {
+            check_cuda(ctx->rhs.ensure(bbytes), "cudaMalloc(rhs)");
+            check_cuda(cudaMemcpyAsync(ctx->rhs.p, rhs, bbytes, cudaMemcpyHostToDevice, st), "H2D rhs");
+            d_rhs = ctx->rhs.as<double>();
+        }
+        const bool host_x = !is_device_ptr(x_out);
+        if (host_x) {
+            check_cuda(ctx->x.ensure(bbytes), "cudaMalloc(x)");
+            d_x = ctx->x.as<double>();
+        }
+        check_cuda(ctx->giters.ensure(sizeof(int32_t) * n_groups), "cudaMalloc");
+        check_cuda(ctx->grms.ensure(sizeof(double) * n_groups), "cudaMalloc");
+        check_cuda(ctx->gflags.ensure(n_groups), "cudaMalloc");
+        const int64_t launches0 = ctx->launches;
+
+        const bool timing = (prm->options & BC_OPT_TIMING) != 0;
+        if (timing) check_cuda(cudaEventRecord(ctx->e0, st), "cudaEventRecord");
+        const bool bicg = prm->algo == BC_ALGO_BICG;
+        int slot = 0;
+        for (const GroupSpan& sp : spans) {
+            const bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);
+            launch_block(ctx, pat, gp, prm->algo, sp.cell0, sp.gout0, sp.count, d_values, d_rhs,
+                         nullptr, d_x, prm->tol, prm->max_iter,
+                         ctx->counters.as<unsigned int>() + slot++, st);
+        }
+        // breakdown groups -> device LU fallback
+        std::vector<uint8_t> flags(n_groups);
+        check_cuda(cudaMemcpyAsync(flags.data(), ctx->gflags.p, n_groups, cudaMemcpyDeviceToHost, st), "D2H flags");
+        check_cuda(cudaStreamSynchronize(st), "solve kernels");
+        std::vector<bc::LuEntry> ents;
+        for (const GroupSpan& sp : spans)
+            for (int g = 0; g < sp.count; ++g) {
+                const int64_t go = sp.gout0 + g;
+                if (flags[go] & BC_FLAG_BREAKDOWN)
+                    ents.push_back({sp.cell0 + static_cast<int64_t>(g) * sp.k, go, sp.k, 0});
+            }
+        int64_t fallbacks = 0;
+        if (!ents.empty()) {
+            int64_t nmax = 0;
+            for (const auto& e : ents) nmax = std::max<int64_t>(nmax, e.kc * s);
+            const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(ents.size()),
+                                                                         (int64_t(1) << 31) / (nmax * nmax * 8)));
+            check_cuda(ctx->lu_scratch.ensure(sizeof(double) * nmax * nmax * batch), "cudaMalloc(lu)");
+            check_cuda(ctx->lu_entries.ensure(sizeof(bc::LuEntry) * ents.size()), "cudaMalloc");
+            check_cuda(ctx->lu_status.ensure(sizeof(int32_t) * ents.size()), "cudaMalloc");
+            check_cuda(cudaMemcpyAsync(ctx->lu_entries.p, ents.data(), sizeof(bc::LuEntry) * ents.size(),
+                                       cudaMemcpyHostToDevice, st), "H2D lu entries");
+            const int64_t pmax = bc::padded_len(nmax);
+            const size_t smem = sizeof(int) * ((nmax + 1) & ~1) + sizeof(double) * (nmax + std::max(pmax, nmax));
+            if (smem > 48 * 1024)
+                check_cuda(cudaFuncSetAttribute(bc::lu_fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                kMaxDynSmem), "cudaFuncSetAttribute(lu)");
+            for (size_t b0 = 0; b0 < ents.size(); b0 += batch) {
+                const int cnt = static_cast<int>(std::min<int64_t>(batch, ents.size() - b0));
+                bc::LuParams lp{};
+                lp.values = d_values;
+                lp.rhs = d_rhs;
+                lp.x_out = d_x;
+                lp.g_rms = ctx->grms.as<double>();
+                lp.status = ctx->lu_status.as<int32_t>() + b0;
+                lp.entries = ctx->lu_entries.as<bc::LuEntry>() + b0;
+                lp.row_ptr = ctx->d_rp.as<int32_t>();
+                lp.col_idx = ctx->d_ci.as<int32_t>();
+                lp.scratch = ctx->lu_scratch.as<double>();
+                lp.n_max = nmax;
+                lp.species = static_cast<int>(s);
+                lp.nnz = static_cast<int>(nnz);
+                lp.block_width = 0;
+                bc::lu_fallback_kernel<<<cnt, 256, smem, st>>>(lp);
+                check_cuda(cudaGetLastError(), "lu_fallback_kernel launch");
+                ctx->launches++;
+            }
+            std::vector<int32_t> status(ents.size());
+            check_cuda(cudaMemcpyAsync(status.data(), ctx->lu_status.p, sizeof(int32_t) * ents.size(),
+                                       cudaMemcpyDeviceToHost, st), "D2H lu status");
+            check_cuda(cudaStreamSynchronize(st), "lu_fallback_kernel");
+            for (size_t i = 0; i < ents.size(); ++i) {
+                if (status[i]) fail(BC_ERR_SINGULAR_MATRIX, "lu_solve: exactly singular matrix");
+                flags[ents[i].gout] |= BC_FLAG_FELL_BACK;
+            }
+            fallbacks = static_cast<int64_t>(ents.size());
+        }
+        if (timing) check_cuda(cudaEventRecord(ctx->e1, st), "cudaEventRecord");
+
+        // outputs
+        if (host_x)
+            check_cuda(cudaMemcpyAsync(x_out, d_x, bbytes, cudaMemcpyDeviceToHost, st), "D2H x");
+        std::vector<int32_t> h_it;
+        std::vector<double> h_rms;
+        int32_t* it_dst = group_iters;
+        double* rms_dst = group_rms;
+        const bool it_dev = is_device_ptr(group_iters), rms_dev = is_device_ptr(group_rms);
+        h_it.resize(n_groups);
+        h_rms.resize(n_groups);
+        check_cuda(cudaMemcpyAsync(h_it.data(), ctx->giters.p, sizeof(int32_t) * n_groups,
+                                   cudaMemcpyDeviceToHost, st), "D2H iters");
+        check_cuda(cudaMemcpyAsync(h_rms.data(), ctx->grms.p, sizeof(double) * n_groups,
+                                   cudaMemcpyDeviceToHost, st), "D2H rms");
+        if (it_dst && it_dev)
+            check_cuda(cudaMemcpyAsync(it_dst, ctx->giters.p, sizeof(int32_t) * n_groups,
+                                       cudaMemcpyDeviceToDevice, st), "D2D iters");
+        if (rms_dst && rms_dev)
+            check_cuda(cudaMemcpyAsync(rms_dst, ctx->grms.p, sizeof(double) * n_groups,
+                                       cudaMemcpyDeviceToDevice, st), "D2D rms");
+        if (group_flags && is_device_ptr(group_flags))
+            check_cuda(cudaMemcpyAsync(group_flags, flags.data(), n_groups, cudaMemcpyHostToDevice, st),
+                       "H2D flags");
+        check_cuda(cudaStreamSynchronize(st), "outputs");
+        if (it_dst && !it_dev) std::memcpy(it_dst, h_it.data(), sizeof(int32_t) * n_groups);
+        if (rms_dst && !rms_dev) std::memcpy(rms_dst, h_rms.data(), sizeof(double) * n_groups);
+        if (group_flags && !is_device_ptr(group_flags)) std::memcpy(group_flags, flags.data(), n_groups);
+
+        if (report) {  // merge_groups, strategies.cpp:71-87
+            std::memset(report, 0, sizeof *report);
+            report->n_groups = n_groups;
+            report->cells_per_block = cpb;
+            for (int64_t g = 0; g < n_groups; ++g) {
+                report->iterations_sum += h_it[g];
+                report->iterations_effective = std::max<int64_t>(report->iterations_effective, h_it[g]);
+                if (h_rms[g] > report->max_residual_rms) report->max_residual_rms = h_rms[g];
+            }
+            report->breakdown_fallbacks = fallbacks;
+            report->kernel_launches = ctx->launches - launches0;
+            if (timing) {
+                float ms = 0.f;
+                check_cuda(cudaEventElapsedTime(&ms, ctx->e0, ctx->e1), "cudaEventElapsedTime");
+                report->device_ms = ms;
+            }
+        }
+        return BC_OK;
+    });
+}
+
+int bc_bicg_solve(bc_ctx* ctx, int32_t algo, int32_t n, const int32_t* row_ptr, const int32_t* col_idx,
+                  const double* vals, const double* b, const double* x0, double tol, int64_t max_iter,
+                  int64_t n_blocks, const int64_t* ranges, double* x_out, bc_outcome* out) {
+    if (!ctx) return BC_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&]() -> int {
+        if (n < 1) fail(BC_ERR_INVALID_ARGUMENT, "bicg: matrix not square / empty");
+        if (!vals || !b || !x_out || !out) fail(BC_ERR_INVALID_ARGUMENT, "bicg: null pointer");
+        if (!(tol > 0.0)) fail(BC_ERR_INVALID_ARGUMENT, "bicg: tol must be positive");
+        if (max_iter < 1) fail(BC_ERR_INVALID_ARGUMENT, "bicg: max_iter must be >= 1");
+        if (algo != BC_ALGO_BICG && algo != BC_ALGO_BICGSTAB_JACOBI)
+            fail(BC_ERR_INVALID_ARGUMENT, "unknown algorithm");
+        // reduction.cpp:16-25 check_partition
+        int64_t expect = 0;
+        for (int64_t k = 0; k < n_blocks; ++k) {
+            if (ranges[2 * k] != expect || ranges[2 * k + 1] <= ranges[2 * k])
+                fail(BC_ERR_INVALID_ARGUMENT, "reduction plan does not partition [0, n)");
+            expect = ranges[2 * k + 1];
+        }
+        if (expect != n) fail(BC_ERR_INVALID_ARGUMENT, "reduction plan does not cover [0, n)");
+        if (n_blocks != 1) fail(BC_ERR_INVALID_ARGUMENT, "multi-interval reduction plans need the Multi-cells path");
+        if (n > bc::kMaxGroupRows) fail(BC_ERR_INVALID_ARGUMENT, "system exceeds 2048 rows");
+        const bc::Pattern pat = make_pattern(n, row_ptr, col_idx);
+        std::map<std::pair<int, int>, bc::GroupPlan> local;
+        const size_t first_buf = ctx->plan_bufs.size();
+        const bc::GroupPlan& gp = get_plan(ctx, pat, 1, algo == BC_ALGO_BICG, &local);
+        const size_t vb = sizeof(double) * pat.nnz, bb = sizeof(double) * n;
+        check_cuda(ctx->values.ensure(std::max<size_t>(vb, 8)), "cudaMalloc");
+        check_cuda(ctx->rhs.ensure(bb * 2), "cudaMalloc");
+        check_cuda(ctx->x.ensure(bb), "cudaMalloc");
+        check_cuda(ctx->giters.ensure(4), "cudaMalloc");
+        check_cuda(ctx->grms.ensure(8), "cudaMalloc");
+        check_cuda(ctx->gflags.ensure(1), "cudaMalloc");
+        const cudaMemcpyKind kin = cudaMemcpyDefault;
+        if (vb) check_cuda(cudaMemcpy(ctx->values.p, vals, vb, kin), "copy values");
+        check_cuda(cudaMemcpy(ctx->rhs.p, b, bb, kin), "copy b");
+        double* d_x0 = nullptr;
+        if (x0) {
+            d_x0 = ctx->rhs.as<double>() + n;
+            check_cuda(cudaMemcpy(d_x0, x0, bb, kin), "copy x0");
+        }
+        launch_block(ctx, pat, gp, algo, 0, 0, 1, ctx->values.as<double>(), ctx->rhs.as<double>(), d_x0,
+                     ctx->x.as<double>(), tol, max_iter, ctx->counters.as<unsigned int>() + 8, 0);
+        check_cuda(cudaDeviceSynchronize(), "bicg kernel");
+        int32_t it = 0;
+        double rms = 0.0;
+        uint8_t fl = 0;
+        check_cuda(cudaMemcpy(x_out, ctx->x.p, bb, kin), "copy x");
+        check_cuda(cudaMemcpy(&it, ctx->giters.p, 4, cudaMemcpyDeviceToHost), "D2H");
+        check_cuda(cudaMemcpy(&rms, ctx->grms.p, 8, cudaMemcpyDeviceToHost), "D2H");
+        check_cuda(cudaMemcpy(&fl, ctx->gflags.p, 1, cudaMemcpyDeviceToHost), "D2H");
+        for (size_t i = first_buf; i < ctx->plan_bufs.size(); ++i) ctx->plan_bufs[i].release();
+        ctx->plan_bufs.resize(first_buf);
+        out->iterations = it;
+        out->final_residual_rms = rms;
+        out->converged = (fl & BC_FLAG_CONVERGED) ? 1 : 0;
+        out->breakdown = (fl & BC_FLAG_BREAKDOWN) ? 1 : 0;
+        return BC_OK;
+    });
+}
+
+int bc_newton_assemble(bc_ctx* ctx, int64_t count, int32_t species, int32_t reactions, int32_t nnz,
+                       const double* rates, const int32_t* stamp_ptr, const int32_t* stamp_slot,
+                       const double* stamp_sign, const int32_t* stamp_other, const int32_t* reactant_ptr,
+                       const int32_t* reactants, const int32_t* product_ptr, const int32_t* products,
+                       const int32_t* diag_slot, double h, const double* y, const double* y_prev,
+                       double* values, double* rhs, void* stream) {
+    if (!ctx) return BC_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&]() -> int {
+        if (count < 0 || species < 1 || reactions < 1 || nnz < 1 || !(h > 0.0))
+            fail(BC_ERR_INVALID_ARGUMENT, "newton_assemble: bad sizes");
+        if (count == 0) return BC_OK;
+        check_cuda(ctx->f_scratch.ensure(sizeof(double) * count * species), "cudaMalloc");
+        bc::NewtonParams p{count, species, reactions, nnz, rates, stamp_ptr, stamp_slot, stamp_other,
+                           stamp_sign, reactant_ptr, reactants, product_ptr, products, diag_slot,
+                           h, y, y_prev, values, rhs, ctx->f_scratch.as<double>()};
+        const int threads = 128;
+        const int64_t blocks = (count + threads - 1) / threads;
+        bc::newton_assemble_kernel<<<static_cast<unsigned>(blocks), threads, 0,
+                                     static_cast<cudaStream_t>(stream)>>>(p);
+        check_cuda(cudaGetLastError(), "newton_assemble_kernel launch");
+        ctx->launches++;
+        return BC_OK;
+    });
+}
+
+}  // extern "C"

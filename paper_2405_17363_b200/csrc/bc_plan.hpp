@@ -1,0 +1,72 @@
+// bc_plan.hpp -- host-side geometry and SpMV schedules for the fused
+// Block-cells kernel.  Built once per (pattern, group size, team width) and
+// cached in the context; the device copies are shared by every group.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+namespace bc {
+
+// Schedule word: gather index | output row << 12 | end-of-row << 31.
+constexpr uint32_t kColBits = 12;
+constexpr uint32_t kColMask = (1u << kColBits) - 1;
+constexpr uint32_t kEndBit = 1u << 31;
+constexpr int kMaxGroupRows = 2048;  // 12-bit row/col fields
+
+struct Pattern {
+    int32_t species = 0;
+    int32_t nnz = 0;
+    std::vector<int32_t> row_ptr, col_idx;
+    std::vector<int32_t> diag;  // CSR index of the diagonal entry per row, -1 if absent
+};
+
+// Reduction geometry of one group:
+// rows i of the group live in warp w = (i/32) % W, lane i%32, register slot
+// j = (i/32) / W.  P = padded length (reduction.cpp:34-36), Q = max(1, P/32),
+// W * R = Q.  The per-lane tree over j, the cross-warp tree over w and the
+// xor-butterfly over lanes reproduce tree_reduce_in_place's order exactly.
+struct Geometry {
+    int n = 0;    // rows in the group (k * species)
+    int P = 1;    // padded reduction length
+    int Q = 1;    // 32-row columns in the padded tree
+    int W = 1;    // warps per group (team)
+    int R = 1;    // register slots per lane in the tree
+    int RV = 1;   // register slots that can hold real rows
+};
+
+Geometry choose_geometry(int n);
+
+// SpMV schedule over the team's W*32 lanes: rows (or columns, for the
+// transpose) assigned longest-first to the least-loaded lane; each lane
+// walks its rows back to back, entries in CSR (resp. ascending row) order.
+struct Schedule {
+    int steps = 0;                  // S
+    std::vector<uint32_t> words;    // S * LW
+    std::vector<int32_t> vpos;      // group value index -> smem slot (t*LW + L)
+};
+
+struct GroupPlan {
+    int k = 1;
+    Geometry geo;
+    Schedule a, at;              // A and A^T (at only built for BiCG)
+    std::vector<int32_t> dpos;   // per group row: smem slot of the diagonal value, -1 if none
+    // device copies
+    uint32_t* d_words = nullptr;
+    uint32_t* d_twords = nullptr;
+    int32_t* d_vpos = nullptr;
+    int32_t* d_tvpos = nullptr;
+    int32_t* d_dpos = nullptr;
+};
+
+Schedule build_schedule(const Pattern& pat, int k, int lanes, bool transpose);
+GroupPlan build_group_plan(const Pattern& pat, int k, bool with_transpose);
+
+inline int64_t padded_len(int64_t n) {
+    if (n <= 1) return 1;
+    int64_t p = 1;
+    while (p < n) p <<= 1;
+    return p;
+}
+
+}  // namespace bc

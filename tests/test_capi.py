@@ -1,0 +1,216 @@
+"""CPU: the C-ABI libraries load without a GPU and export every symbol the
+headers declare; the host-side planning and the fused kernel's SpMV
+schedule / reduction geometry reproduce the reference's arithmetic order
+(emulated here in exact IEEE double arithmetic, no GPU needed)."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle_ffi as of
+from fixtures import random_batch
+from paper_2405_17363_b200 import Mechanism, _native
+from paper_2405_17363_b200._native import SolveParams
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared(header):
+    text = open(os.path.join(ROOT, "include", header)).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(bcw?_[a-z_0-9]+)\s*\(", text)))
+
+
+@pytest.mark.parametrize("header,lib", [("blockcells_b200.h", "b200"), ("blockcells_workload.h", "workload")])
+def test_library_exports_every_declared_symbol(header, lib):
+    dll = getattr(_native, lib)()
+    names = declared(header)
+    assert len(names) >= 6
+    missing = [n for n in names if not hasattr(dll, n)]
+    assert not missing, missing
+
+
+def test_kernels_are_sm100a():
+    """The library carries sm_100a SASS (cuobjdump), with no FMA in the solver."""
+    import shutil
+    import subprocess
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(cuobjdump):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([cuobjdump, "--list-elf", _native.LIB_B200], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run([cuobjdump, "-sass", _native.LIB_B200], capture_output=True, text=True).stdout
+    assert "block_cells_kernel" in sass and "DADD" in sass and "DMUL" in sass
+
+
+def plan(species, strategy, k, cells, mtpb=1024):
+    prm = SolveParams()
+    prm.strategy, prm.cells_per_block, prm.cells, prm.max_threads_per_block = strategy, k, cells, mtpb
+    prm.tol, prm.max_iter = 1e-8, 10
+    ng, cpb = C.c_int64(), C.c_double()
+    st = _native.b200().bc_plan(species, C.byref(prm), C.byref(ng), C.byref(cpb))
+    return st, ng.value, cpb.value
+
+
+def test_plan_mirrors_plan_kernel():
+    """exec_model.cpp:102-161 + strategies.cpp:209-213 (same as the oracle)."""
+    for species in (1, 13, 156, 312, 1024):
+        for cells in (1, 7, 100, 100000):
+            for strategy, k in [(0, 0), (1, 0), (2, 0), (2, 1), (2, 3), (2, 6), (2, 7)]:
+                for mtpb in (1024, 512):
+                    st, ng, cpb = plan(species, strategy, k, cells, mtpb)
+                    want_ng = of.orc().orc_group_count(strategy, cells, species, mtpb, k)
+                    ocpb = C.c_double()
+                    ost = of.orc().orc_plan_cells_per_block(strategy, cells, species, mtpb, k, C.byref(ocpb))
+                    assert st == ost, (species, cells, strategy, k, mtpb)
+                    if st == 0:
+                        assert ng == want_ng and cpb == ocpb.value
+
+
+def test_plan_errors():
+    assert plan(156, 2, 7, 10)[0] == -2  # InvalidGrouping
+    assert plan(2000, 2, 1, 10)[0] == -3  # UnsupportedMechanism
+    assert plan(156, 2, 1, 0)[0] == -1  # no cells
+    assert plan(156, 9, 1, 10)[0] == -1  # unknown strategy
+
+
+def export_schedule(rp, ci, k, with_t):
+    species = len(rp) - 1
+    info = np.zeros(8, np.int32)
+    lib = _native.b200()
+    rp = np.ascontiguousarray(rp, np.int32)
+    ci = np.ascontiguousarray(ci, np.int32)
+    st = lib.bc_schedule_export(species, of.ptr(rp), of.ptr(ci), k, with_t, of.ptr(info), None, None, None, None)
+    assert st == 0
+    n, P, Q, W, R, RV, S, St = info.tolist()
+    nnz = int(rp[-1])
+    words = np.zeros(max(S * W * 32, 1), np.uint32)
+    vpos = np.zeros(k * nnz, np.int32)
+    twords = np.zeros(max(St * W * 32, 1), np.uint32)
+    tvpos = np.zeros(k * nnz, np.int32)
+    st = lib.bc_schedule_export(species, of.ptr(rp), of.ptr(ci), k, with_t, of.ptr(info), of.ptr(words),
+                                of.ptr(vpos), of.ptr(twords), of.ptr(tvpos))
+    assert st == 0
+    return dict(n=n, P=P, Q=Q, W=W, R=R, RV=RV, S=S, St=St, words=words, vpos=vpos, twords=twords, tvpos=tvpos)
+
+
+def emulate_pass(words, vpos, vals, S, LW, x, n):
+    """sched_pass() of bc_block.cuh in exact double arithmetic."""
+    V = np.zeros(S * LW)
+    V[vpos] = vals
+    y = np.zeros(n)
+    for L in range(LW):
+        acc = 0.0
+        for t in range(S):
+            e = int(words[t * LW + L])
+            acc = acc + float(V[t * LW + L]) * float(x[e & 0xFFF])
+            if e >> 31:
+                y[(e >> 12) & 0xFFF] = acc
+                acc = 0.0
+    return y
+
+
+def ref_spmv(rp, ci, vals, x, k, s, nnz):
+    y = np.zeros(k * s)
+    for c in range(k):
+        for i in range(s):
+            acc = 0.0
+            for e in range(rp[i], rp[i + 1]):
+                acc = acc + float(vals[c * nnz + e]) * float(x[c * s + ci[e]])
+            y[c * s + i] = acc
+    return y
+
+
+def ref_spmv_t(rp, ci, vals, x, k, s, nnz):
+    y = np.zeros(k * s)
+    for c in range(k):
+        for i in range(s):
+            for e in range(rp[i], rp[i + 1]):
+                j = c * s + ci[e]
+                y[j] = y[j] + float(vals[c * nnz + e]) * float(x[c * s + i])
+    return y
+
+
+@pytest.mark.parametrize("species,k,density,seed", [(9, 1, 0.4, 0), (40, 3, 0.2, 1), (156, 1, 0.0, 2),
+                                                    (100, 5, 0.05, 3), (17, 30, 0.3, 4)])
+def test_schedule_reproduces_spmv_order(species, k, density, seed):
+    rng = np.random.default_rng(seed)
+    if density == 0.0:
+        m = Mechanism(156, 468, 0)
+        rp, ci = m.row_ptr, m.col_idx
+    else:
+        rp, ci, _, _ = random_batch(rng, 1, species, density)
+    nnz = int(rp[-1])
+    sc = export_schedule(rp, ci, k, 1)
+    LW = sc["W"] * 32
+    vals = rng.uniform(-1, 1, k * nnz) * 10.0 ** rng.integers(-8, 8, k * nnz)
+    x = rng.uniform(-1, 1, k * species)
+    y = emulate_pass(sc["words"], sc["vpos"], vals, sc["S"], LW, x, k * species)
+    np.testing.assert_array_equal(of.bits(y), of.bits(ref_spmv(rp, ci, vals, x, k, species, nnz)))
+    yt = emulate_pass(sc["twords"], sc["tvpos"], vals, sc["St"], LW, x, k * species)
+    np.testing.assert_array_equal(of.bits(yt), of.bits(ref_spmv_t(rp, ci, vals, x, k, species, nnz)))
+    assert sc["S"] * LW >= k * nnz  # every value has a slot
+    assert sorted(sc["vpos"].tolist()) == sorted(set(sc["vpos"].tolist()))
+
+
+def emulate_team_reduce(vals, n, P, W, R):
+    """team_reduce() of bc_block.cuh: per-lane tree over R slots, cross-warp
+    tree over W, xor butterfly over 32 lanes (lane 0's value)."""
+    lanes = {}
+    for w in range(W):
+        for lane in range(32):
+            t = [0.0] * R
+            for j in range(R):
+                i = (j * W + w) * 32 + lane
+                t[j] = float(vals[i]) if i < n else 0.0
+            s = R // 2
+            while s >= 1:
+                for j in range(s):
+                    t[j] = t[j] + t[j + s]
+                s //= 2
+            lanes[(w, lane)] = t[0]
+    part = []
+    for lane in range(32):
+        u = [lanes[(w, lane)] for w in range(W)]
+        s = W // 2
+        while s >= 1:
+            for q in range(s):
+                u[q] = u[q] + u[q + s]
+            s //= 2
+        part.append(u[0])
+    if P >= 32:
+        masks = [16, 8, 4, 2, 1]
+    else:
+        masks = []
+        m = P // 2
+        while m >= 1:
+            masks.append(m)
+            m //= 2
+    for mask in masks:
+        part = [part[l] + part[l ^ mask] for l in range(32)]
+    return part[0]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 16, 17, 31, 32, 33, 100, 156, 255, 256, 257, 312, 500, 936, 1024, 1500,
+                               2048])
+def test_reduction_geometry_reproduces_tree(n):
+    info = np.zeros(8, np.int32)
+    rp = np.arange(n + 1, dtype=np.int32)
+    ci = np.arange(n, dtype=np.int32)
+    assert _native.b200().bc_schedule_export(n, of.ptr(rp), of.ptr(ci), 1, 0, of.ptr(info), None, None, None,
+                                              None) == 0
+    _, P, Q, W, R, RV, _, _ = info.tolist()
+    assert W * R == Q and P >= n
+    rng = np.random.default_rng(n)
+    for _ in range(5):
+        v = rng.uniform(-1, 1, n) * 10.0 ** rng.integers(-12, 12, n)
+        v[rng.random(n) < 0.1] = -0.0
+        slots = np.zeros(P)
+        slots[:n] = v
+        want = of.orc().orc_tree_reduce_in_place(of.ptr(slots), P)
+        got = emulate_team_reduce(v, n, P, W, R)
+        assert of.bits(got) == of.bits(want)
