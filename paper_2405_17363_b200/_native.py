@@ -66,7 +66,7 @@ def b200() -> C.CDLL:
         lib.bc_schedule_export.argtypes = [_i32, _c_p, _c_p, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p]
         lib.bc_solve.argtypes = [_c_p, C.POINTER(SolveParams), _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                                  C.POINTER(Report)]
-        lib.bc_bicg_solve.argtypes = [_c_p, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _f64, _i64,
+        lib.bc_bicg_solve.argtypes = [_c_p, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _f64, _i64,
                                       _i64, _c_p, _c_p, C.POINTER(Outcome)]
         lib.bc_kernel_launches.argtypes = [_c_p]
         lib.bc_kernel_launches.restype = _i64
@@ -90,6 +90,6 @@ def workload() -> C.CDLL:
         lib.bcw_newton_batch.argtypes = [_c_p, _i64, _i64, _i64, C.c_int, _f64, _c_p, _c_p, _c_p, _c_p,
                                          C.c_int]
         lib.bcw_rate_constants.argtypes = [_c_p, _i64, _i64, _i64, C.c_int, _c_p, C.c_int]
-        lib.bcw_stamp_program.argtypes = [_c_p] + [_c_p] * 10
+        lib.bcw_stamp_program.argtypes = [_c_p] * 10
         _wl = lib
     return _wl

@@ -50,6 +50,15 @@ struct BlockParams {
     int sched_words;        // shared u32 words of schedules per CTA (padded to even)
     double tol;
     int64_t max_iter;
+    // Staging level for groups too large for shared memory (comparison
+    // strategies only; Block-cells(1) at CB05 size is always level 0):
+    //   0: schedules and values in shared memory
+    //   1: schedules read from global (L1/L2-resident), values in shared memory
+    //   2: schedules and values read from global, values through vidx/tvidx
+    int level;
+    const int32_t* vidx;    // schedule slot -> group value index (level 2)
+    const int32_t* tvidx;
+    const int32_t* didx;    // group row -> group value index of the diagonal, -1 if none
 };
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -81,6 +90,15 @@ struct Ctx {
     double* Yt;   // A^T products (BiCG)
     double* red;  // cross-warp partials [2][4][W][32]
     int red_buf;
+    // SpMV operands: schedule words, values (schedule order, or indexed), steps
+    const uint32_t* Wa;
+    const double* Va;
+    const int32_t* Ia;
+    int Sa;
+    const uint32_t* Wt;
+    const double* Vt;
+    const int32_t* It;
+    int St;
     __device__ __forceinline__ int row(int j) const { return (j * W + tm.w) * 32 + tm.lane; }
     __device__ __forceinline__ bool valid(int j) const { return row(j) < n; }
 };
@@ -139,15 +157,16 @@ __device__ __forceinline__ void team_reduce(Ctx<W, R, RV>& c, const double (&val
 
 // One schedule pass: every lane walks its segments, writing each finished
 // row (column, for A^T) sum into Y.
-template <int W>
-__device__ __forceinline__ void sched_pass(const uint32_t* __restrict__ words, const double* __restrict__ V,
-                                           int steps, int L, const double* X, double* Y) {
+template <int W, bool INDEXED>
+__device__ __forceinline__ void sched_pass_impl(const uint32_t* __restrict__ words, const double* __restrict__ V,
+                                                const int32_t* __restrict__ vidx, int steps, int L,
+                                                const double* X, double* Y) {
     constexpr int LW = W * 32;
     double acc = 0.0;
 #pragma unroll 4
     for (int t = 0; t < steps; ++t) {
         const uint32_t e = words[t * LW + L];
-        const double a = V[t * LW + L];
+        const double a = INDEXED ? V[vidx[t * LW + L]] : V[t * LW + L];
         const double xv = X[e & kColMask];
         acc = dadd(acc, dmul(a, xv));
         if (e & kEndBit) {
@@ -157,15 +176,23 @@ __device__ __forceinline__ void sched_pass(const uint32_t* __restrict__ words, c
     }
 }
 
+template <int W>
+__device__ __forceinline__ void sched_pass(const uint32_t* words, const double* V, const int32_t* vidx,
+                                           int steps, int L, const double* X, double* Y) {
+    if (vidx)
+        sched_pass_impl<W, true>(words, V, vidx, steps, L, X, Y);
+    else
+        sched_pass_impl<W, false>(words, V, nullptr, steps, L, X, Y);
+}
+
 // y = A x over the group (csr.cpp:90-101 semantics).
 template <int W, int R, int RV>
-__device__ __forceinline__ void team_spmv(Ctx<W, R, RV>& c, const uint32_t* words, const double* V,
-                                          int steps, const double (&x)[RV], double (&y)[RV]) {
+__device__ __forceinline__ void team_spmv(Ctx<W, R, RV>& c, const double (&x)[RV], double (&y)[RV]) {
 #pragma unroll
     for (int j = 0; j < RV; ++j)
         if (c.valid(j)) c.Xs[c.row(j)] = x[j];
     c.tm.sync();
-    sched_pass<W>(words, V, steps, c.tm.tid, c.Xs, c.Ys);
+    sched_pass<W>(c.Wa, c.Va, c.Ia, c.Sa, c.tm.tid, c.Xs, c.Ys);
     c.tm.sync();
 #pragma unroll
     for (int j = 0; j < RV; ++j) y[j] = c.valid(j) ? c.Ys[c.row(j)] : 0.0;
@@ -173,11 +200,8 @@ __device__ __forceinline__ void team_spmv(Ctx<W, R, RV>& c, const uint32_t* word
 
 // ap = A p and atps = A^T ps in one pass (BiCG, bicg.cpp:106-107).
 template <int W, int R, int RV>
-__device__ __forceinline__ void team_spmv_pair(Ctx<W, R, RV>& c, const uint32_t* words,
-                                               const double* V, int steps, const uint32_t* twords,
-                                               const double* Vt, int tsteps, const double (&p)[RV],
-                                               const double (&ps)[RV], double (&ap)[RV],
-                                               double (&atps)[RV]) {
+__device__ __forceinline__ void team_spmv_pair(Ctx<W, R, RV>& c, const double (&p)[RV], const double (&ps)[RV],
+                                               double (&ap)[RV], double (&atps)[RV]) {
 #pragma unroll
     for (int j = 0; j < RV; ++j)
         if (c.valid(j)) {
@@ -185,8 +209,8 @@ __device__ __forceinline__ void team_spmv_pair(Ctx<W, R, RV>& c, const uint32_t*
             c.Xs2[c.row(j)] = ps[j];
         }
     c.tm.sync();
-    sched_pass<W>(words, V, steps, c.tm.tid, c.Xs, c.Ys);
-    sched_pass<W>(twords, Vt, tsteps, c.tm.tid, c.Xs2, c.Yt);
+    sched_pass<W>(c.Wa, c.Va, c.Ia, c.Sa, c.tm.tid, c.Xs, c.Ys);
+    sched_pass<W>(c.Wt, c.Vt, c.It, c.St, c.tm.tid, c.Xs2, c.Yt);
     c.tm.sync();
 #pragma unroll
     for (int j = 0; j < RV; ++j) {
@@ -197,10 +221,9 @@ __device__ __forceinline__ void team_spmv_pair(Ctx<W, R, RV>& c, const uint32_t*
 
 // bicg.cpp:61-72 residual_rms: sqrt(tree((b - A x)^2) / n)
 template <int W, int R, int RV>
-__device__ __forceinline__ double fresh_rms(Ctx<W, R, RV>& c, const uint32_t* words, const double* V,
-                                            int steps, const double (&x)[RV], const double (&b)[RV]) {
+__device__ __forceinline__ double fresh_rms(Ctx<W, R, RV>& c, const double (&x)[RV], const double (&b)[RV]) {
     double ax[RV];
-    team_spmv(c, words, V, steps, x, ax);
+    team_spmv(c, x, ax);
     double sq[1][RV];
 #pragma unroll
     for (int j = 0; j < RV; ++j) {
@@ -213,17 +236,20 @@ __device__ __forceinline__ double fresh_rms(Ctx<W, R, RV>& c, const uint32_t* wo
 }
 
 template <int ALGO, int W, int R, int RV>
-__global__ void __launch_bounds__(256) block_cells_kernel(const BlockParams p) {
+__global__ void __launch_bounds__(256, 1) block_cells_kernel(const BlockParams p) {
     constexpr int LW = W * 32;
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* s_words = reinterpret_cast<uint32_t*>(smem);
     uint32_t* s_twords = s_words + p.S * LW;
     double* team_base = reinterpret_cast<double*>(smem + sizeof(uint32_t) * p.sched_words);
+    const bool words_smem = p.level == 0, values_smem = p.level < 2;
 
     // CTA-shared schedules (identical for every group)
-    for (int i = threadIdx.x; i < p.S * LW; i += blockDim.x) s_words[i] = p.words[i];
-    if constexpr (ALGO == kBiCG)
-        for (int i = threadIdx.x; i < p.St * LW; i += blockDim.x) s_twords[i] = p.twords[i];
+    if (words_smem) {
+        for (int i = threadIdx.x; i < p.S * LW; i += blockDim.x) s_words[i] = p.words[i];
+        if constexpr (ALGO == kBiCG)
+            for (int i = threadIdx.x; i < p.St * LW; i += blockDim.x) s_twords[i] = p.twords[i];
+    }
     __syncthreads();
 
     const int team_id = threadIdx.x / LW;
@@ -237,13 +263,19 @@ __global__ void __launch_bounds__(256) block_cells_kernel(const BlockParams p) {
     const int n_pad = (p.n + 31) & ~31;
     double* Vs = team_base + static_cast<size_t>(team_id) * p.team_doubles;
     double* Vt = Vs + p.S * LW;
-    double* tail = Vt + (ALGO == kBiCG ? p.St * LW : 0);
+    double* tail = values_smem ? Vt + (ALGO == kBiCG ? p.St * LW : 0) : Vs;
     c.Xs = tail;
     c.Ys = tail + n_pad;
     c.Xs2 = c.Ys + n_pad;
     c.Yt = c.Xs2 + (ALGO == kBiCG ? n_pad : 0);
     c.red = c.Yt + (ALGO == kBiCG ? n_pad : 0);
     c.red_buf = 0;
+    c.Wa = words_smem ? s_words : p.words;
+    c.Wt = words_smem ? s_twords : p.twords;
+    c.Sa = p.S;
+    c.St = p.St;
+    c.Ia = values_smem ? nullptr : p.vidx;
+    c.It = values_smem ? nullptr : p.tvidx;
     __shared__ int s_group[32];
 
     for (;;) {
@@ -263,11 +295,18 @@ __global__ void __launch_bounds__(256) block_cells_kernel(const BlockParams p) {
         const int64_t cell0 = p.cell_offset + static_cast<int64_t>(gl) * p.kc;
         const double* src = p.values + cell0 * p.nnz;
         const int cnt = p.kc * p.nnz;
-        // stage this group's values into schedule order (once per solve)
-        for (int e = c.tm.tid; e < cnt; e += LW) {
-            const double a = __ldcs(src + e);
-            Vs[p.vpos[e]] = a;
-            if constexpr (ALGO == kBiCG) Vt[p.tvpos[e]] = a;
+        if (values_smem) {
+            // stage this group's values into schedule order (once per solve)
+            for (int e = c.tm.tid; e < cnt; e += LW) {
+                const double a = __ldcs(src + e);
+                Vs[p.vpos[e]] = a;
+                if constexpr (ALGO == kBiCG) Vt[p.tvpos[e]] = a;
+            }
+            c.Va = Vs;
+            c.Vt = Vt;
+        } else {
+            c.Va = src;  // level 2: read through vidx/tvidx (L1/L2)
+            c.Vt = src;
         }
         for (int i = c.tm.tid; i < p.n; i += LW) {
             c.Ys[i] = 0.0;  // empty rows read +0.0, as spmv's sum = 0.0
@@ -294,8 +333,13 @@ __global__ void __launch_bounds__(256) block_cells_kernel(const BlockParams p) {
             for (int j = 0; j < RV; ++j) {
                 double d = 0.0;
                 if (c.valid(j)) {
-                    const int dp = p.dpos[c.row(j)];
-                    d = dp >= 0 ? Vs[dp] : 0.0;
+                    if (values_smem) {
+                        const int dp = p.dpos[c.row(j)];
+                        d = dp >= 0 ? Vs[dp] : 0.0;
+                    } else {
+                        const int di = p.didx[c.row(j)];
+                        d = di >= 0 ? src[di] : 0.0;
+                    }
                     dinv[j] = d != 0.0 ? ddiv(1.0, d) : 1.0;
                 } else {
                     dinv[j] = 0.0;
@@ -304,7 +348,7 @@ __global__ void __launch_bounds__(256) block_cells_kernel(const BlockParams p) {
             double r[RV], rh[RV], pv[RV], v[RV];
             {
                 double ax[RV];
-                team_spmv(c, s_words, Vs, p.S, x, ax);
+                team_spmv(c, x, ax);
 #pragma unroll
                 for (int j = 0; j < RV; ++j) {
                     r[j] = c.valid(j) ? dadd(b[j], -ax[j]) : 0.0;  // 1*b + (-1)*Ax
@@ -324,7 +368,7 @@ __global__ void __launch_bounds__(256) block_cells_kernel(const BlockParams p) {
                 team_reduce<2>(c, q, red2);
             }
             if (__dsqrt_rn(ddiv(red2[0], nd)) <= p.tol) {
-                fres = fresh_rms(c, s_words, Vs, p.S, x, b);
+                fres = fresh_rms(c, x, b);
                 conv = fres <= p.tol;
             }
             if (!conv) {
@@ -340,7 +384,7 @@ __global__ void __launch_bounds__(256) block_cells_kernel(const BlockParams p) {
                         pv[j] = dadd(r[j], dmul(beta, dsub(pv[j], dmul(omega, v[j]))));
                         y[j] = dmul(dinv[j], pv[j]);
                     }
-                    team_spmv(c, s_words, Vs, p.S, y, v);
+                    team_spmv(c, y, v);
                     double den;
                     {
                         double q[1][RV], o[1];
@@ -359,7 +403,7 @@ __global__ void __launch_bounds__(256) block_cells_kernel(const BlockParams p) {
                         x[j] = dadd(x[j], dmul(alpha, y[j]));
                     }
                     double t[RV];
-                    team_spmv(c, s_words, Vs, p.S, z, t);
+                    team_spmv(c, z, t);
                     double tt, ts;
                     {
                         double q[2][RV], o[2];
@@ -395,7 +439,7 @@ __global__ void __launch_bounds__(256) block_cells_kernel(const BlockParams p) {
                     }
                     if (!isfinite(sigma)) { brk = true; break; }
                     if (__dsqrt_rn(ddiv(sigma, nd)) <= p.tol) {
-                        const double f = fresh_rms(c, s_words, Vs, p.S, x, b);
+                        const double f = fresh_rms(c, x, b);
                         if (f <= p.tol) {
                             fres = f;
                             conv = true;
@@ -405,7 +449,7 @@ __global__ void __launch_bounds__(256) block_cells_kernel(const BlockParams p) {
                     if (scalar_breaks(omega)) { brk = true; break; }
                 }
                 if (!conv) {
-                    fres = fresh_rms(c, s_words, Vs, p.S, x, b);
+                    fres = fresh_rms(c, x, b);
                     conv = !brk && fres <= p.tol;
                 }
             }
@@ -414,7 +458,7 @@ __global__ void __launch_bounds__(256) block_cells_kernel(const BlockParams p) {
             double r[RV], rs[RV], pv[RV], ps[RV];
             {
                 double ax[RV];
-                team_spmv(c, s_words, Vs, p.S, x, ax);
+                team_spmv(c, x, ax);
 #pragma unroll
                 for (int j = 0; j < RV; ++j) {
                     r[j] = c.valid(j) ? dadd(b[j], -ax[j]) : 0.0;
@@ -434,7 +478,7 @@ __global__ void __launch_bounds__(256) block_cells_kernel(const BlockParams p) {
                 team_reduce<2>(c, q, red2);
             }
             if (__dsqrt_rn(ddiv(red2[0], nd)) <= p.tol) {
-                fres = fresh_rms(c, s_words, Vs, p.S, x, b);
+                fres = fresh_rms(c, x, b);
                 conv = fres <= p.tol;
             }
             if (!conv) {
@@ -452,7 +496,7 @@ __global__ void __launch_bounds__(256) block_cells_kernel(const BlockParams p) {
                         }
                     }
                     double ap[RV], atps[RV];
-                    team_spmv_pair(c, s_words, Vs, p.S, s_twords, Vt, p.St, pv, ps, ap, atps);
+                    team_spmv_pair(c, pv, ps, ap, atps);
                     double den;
                     {
                         double q[1][RV], o[1];
@@ -486,7 +530,7 @@ __global__ void __launch_bounds__(256) block_cells_kernel(const BlockParams p) {
                     }
                     if (!isfinite(sigma)) { brk = true; break; }
                     if (__dsqrt_rn(ddiv(sigma, nd)) <= p.tol) {
-                        const double f = fresh_rms(c, s_words, Vs, p.S, x, b);
+                        const double f = fresh_rms(c, x, b);
                         if (f <= p.tol) {
                             fres = f;
                             conv = true;
@@ -495,7 +539,7 @@ __global__ void __launch_bounds__(256) block_cells_kernel(const BlockParams p) {
                     }
                 }
                 if (!conv) {
-                    fres = fresh_rms(c, s_words, Vs, p.S, x, b);
+                    fres = fresh_rms(c, x, b);
                     conv = !brk && fres <= p.tol;
                 }
             }

@@ -181,9 +181,12 @@ bc::GroupPlan& get_plan(bc_ctx* ctx, const bc::Pattern& pat, int k, bool with_t,
     gp.d_words = upload(ctx, gp.a.words);
     gp.d_vpos = upload(ctx, gp.a.vpos);
     gp.d_dpos = upload(ctx, gp.dpos);
+    gp.d_vidx = upload(ctx, gp.a.vidx);
+    gp.d_didx = upload(ctx, gp.didx);
     if (with_t) {
         gp.d_twords = upload(ctx, gp.at.words);
         gp.d_tvpos = upload(ctx, gp.at.vpos);
+        gp.d_tvidx = upload(ctx, gp.at.vidx);
     }
     return cache->emplace(key, std::move(gp)).first->second;
 }
@@ -191,43 +194,53 @@ bc::GroupPlan& get_plan(bc_ctx* ctx, const bc::Pattern& pat, int k, bool with_t,
 struct LaunchShape {
     int teams = 1, blocks = 1, threads = 32;
     size_t smem = 0;
-    int team_doubles = 0, sched_words = 0;
+    int team_doubles = 0, sched_words = 0, level = 0;
 };
 
 LaunchShape choose_shape(bc_ctx* ctx, BlockFn fn, const bc::GroupPlan& gp, bool bicg, int groups) {
     const int W = gp.geo.W, LW = 32 * W;
     const int n_pad = (gp.geo.n + 31) & ~31;
-    LaunchShape sh;
-    sh.sched_words = gp.a.steps * LW + (bicg ? gp.at.steps * LW : 0);
-    sh.sched_words = (sh.sched_words + 3) & ~3;
-    sh.team_doubles = gp.a.steps * LW + (bicg ? gp.at.steps * LW : 0) + n_pad * (bicg ? 4 : 2) +
-                      (W > 1 ? 8 * W * 32 : 0);
+    cudaFuncAttributes fa;
+    check_cuda(cudaFuncGetAttributes(&fa, fn), "cudaFuncGetAttributes");
+    const size_t dyn_max = static_cast<size_t>(kMaxDynSmem) - fa.sharedSizeBytes;
     if (!ctx->smem_set[fn]) {
-        check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem),
+        check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn_max)),
                    "cudaFuncSetAttribute");
         ctx->smem_set[fn] = true;
     }
-    int best_warps = -1;
-    const int gmax = std::min(W > 1 ? 15 : 32, 256 / LW);
-    for (int G = 1; G <= gmax; ++G) {
-        const size_t smem = sizeof(uint32_t) * sh.sched_words + sizeof(double) * G * sh.team_doubles;
-        if (smem > static_cast<size_t>(kMaxDynSmem)) break;
-        int nb = 0;
-        check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, G * LW, smem),
-                   "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-        const int warps = nb * G * W;
-        if (warps > best_warps) {
-            best_warps = warps;
-            sh.teams = G;
-            sh.smem = smem;
-            sh.blocks = nb;
+    const int sched = gp.a.steps * LW + (bicg ? gp.at.steps * LW : 0);
+    const int vecs = n_pad * (bicg ? 4 : 2) + (W > 1 ? 8 * W * 32 : 0);
+    for (int level = 0; level <= 2; ++level) {
+        LaunchShape sh;
+        sh.level = level;
+        sh.sched_words = level == 0 ? ((sched + 3) & ~3) : 0;
+        sh.team_doubles = (level < 2 ? sched : 0) + vecs;
+        // Maximise concurrently resident groups (capped by the work available);
+        // ties go to fewer teams per CTA, which spreads small batches over more SMs.
+        int64_t best = -1;
+        const int gmax = std::min(W > 1 ? 15 : 32, 256 / LW);
+        for (int G = 1; G <= gmax; ++G) {
+            const size_t smem = sizeof(uint32_t) * sh.sched_words + sizeof(double) * G * sh.team_doubles;
+            if (smem > dyn_max) break;
+            int nb = 0;
+            check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, G * LW, smem),
+                       "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+            const int64_t conc = std::min<int64_t>(groups, static_cast<int64_t>(nb) * G * ctx->sms);
+            if (nb > 0 && conc > best) {
+                best = conc;
+                sh.teams = G;
+                sh.smem = smem;
+                sh.blocks = nb;
+            }
         }
+        if (best <= 0) continue;
+        sh.threads = sh.teams * LW;
+        const int need = (groups + sh.teams - 1) / sh.teams;
+        sh.blocks = std::max(1, std::min(need, sh.blocks * ctx->sms));
+        return sh;
     }
-    if (best_warps <= 0) fail(BC_ERR_INVALID_ARGUMENT, "group does not fit in shared memory");
-    sh.threads = sh.teams * LW;
-    const int need = (groups + sh.teams - 1) / sh.teams;
-    sh.blocks = std::max(1, std::min(need, sh.blocks * ctx->sms));
-    return sh;
+    fail(BC_ERR_INVALID_ARGUMENT, "group does not fit in shared memory");
+    return LaunchShape{};
 }
 
 // Launch the fused kernel over `groups` groups of kc cells starting at cell0.
@@ -269,6 +282,10 @@ void launch_block(bc_ctx* ctx, const bc::Pattern& pat, const bc::GroupPlan& gp, 
     p.sched_words = sh.sched_words;
     p.tol = tol;
     p.max_iter = max_iter;
+    p.level = sh.level;
+    p.vidx = gp.d_vidx;
+    p.tvidx = gp.d_tvidx;
+    p.didx = gp.d_didx;
     check_cuda(cudaMemsetAsync(counter, 0, sizeof(unsigned int), st), "cudaMemsetAsync(counter)");
     fn<<<sh.blocks, sh.threads, sh.smem, st>>>(p);
     check_cuda(cudaGetLastError(), "block_cells_kernel launch");
@@ -500,7 +517,7 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
             const size_t smem = sizeof(int) * ((nmax + 1) & ~1) + sizeof(double) * (nmax + std::max(pmax, nmax));
             if (smem > 48 * 1024)
                 check_cuda(cudaFuncSetAttribute(bc::lu_fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                kMaxDynSmem), "cudaFuncSetAttribute(lu)");
+                                                kMaxDynSmem - 1024), "cudaFuncSetAttribute(lu)");
             for (size_t b0 = 0; b0 < ents.size(); b0 += batch) {
                 const int cnt = static_cast<int>(std::min<int64_t>(batch, ents.size() - b0));
                 bc::LuParams lp{};

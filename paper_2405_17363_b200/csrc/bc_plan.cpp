@@ -69,6 +69,7 @@ Schedule build_schedule(const Pattern& pat, int k, int lanes, bool transpose) {
     sc.steps = *std::max_element(load.begin(), load.end());
     sc.words.assign(static_cast<size_t>(sc.steps) * lanes, 0u);
     sc.vpos.assign(static_cast<size_t>(k) * nnz, -1);
+    sc.vidx.assign(static_cast<size_t>(sc.steps) * lanes, 0);
     for (int L = 0; L < lanes; ++L) {
         std::sort(lane_segs[L].begin(), lane_segs[L].end(),
                   [&](int a, int b) { return segs[a].out < segs[b].out; });
@@ -81,6 +82,7 @@ Schedule build_schedule(const Pattern& pat, int k, int lanes, bool transpose) {
                 if (q + 1 == sg.ent.size()) w |= kEndBit;
                 sc.words[static_cast<size_t>(t) * lanes + L] = w;
                 sc.vpos[sg.ent[q].first] = t * lanes + L;
+                sc.vidx[static_cast<size_t>(t) * lanes + L] = sg.ent[q].first;
             }
         }
     }
@@ -97,9 +99,13 @@ GroupPlan build_group_plan(const Pattern& pat, int k, bool with_transpose) {
     gp.a = build_schedule(pat, k, lanes, false);
     if (with_transpose) gp.at = build_schedule(pat, k, lanes, true);
     gp.dpos.assign(n, -1);
+    gp.didx.assign(n, -1);
     for (int c = 0; c < k; ++c)
         for (int r = 0; r < pat.species; ++r)
-            if (pat.diag[r] >= 0) gp.dpos[c * pat.species + r] = gp.a.vpos[c * pat.nnz + pat.diag[r]];
+            if (pat.diag[r] >= 0) {
+                gp.dpos[c * pat.species + r] = gp.a.vpos[c * pat.nnz + pat.diag[r]];
+                gp.didx[c * pat.species + r] = c * pat.nnz + pat.diag[r];
+            }
     return gp;
 }
 

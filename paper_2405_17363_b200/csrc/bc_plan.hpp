@@ -44,6 +44,7 @@ struct Schedule {
     int steps = 0;                  // S
     std::vector<uint32_t> words;    // S * LW
     std::vector<int32_t> vpos;      // group value index -> smem slot (t*LW + L)
+    std::vector<int32_t> vidx;      // smem slot -> group value index (0 for padding)
 };
 
 struct GroupPlan {
@@ -51,12 +52,16 @@ struct GroupPlan {
     Geometry geo;
     Schedule a, at;              // A and A^T (at only built for BiCG)
     std::vector<int32_t> dpos;   // per group row: smem slot of the diagonal value, -1 if none
+    std::vector<int32_t> didx;   // per group row: group value index of the diagonal, -1 if none
     // device copies
     uint32_t* d_words = nullptr;
     uint32_t* d_twords = nullptr;
     int32_t* d_vpos = nullptr;
     int32_t* d_tvpos = nullptr;
     int32_t* d_dpos = nullptr;
+    int32_t* d_vidx = nullptr;
+    int32_t* d_tvidx = nullptr;
+    int32_t* d_didx = nullptr;
 };
 
 Schedule build_schedule(const Pattern& pat, int k, int lanes, bool transpose);
