@@ -122,12 +122,14 @@ int bc_plan(int32_t species, const bc_solve_params* prm, int64_t* n_groups,
             double* cells_per_block);
 
 /* Host-side schedule of the fused kernel for a pattern and group size k
- * (no GPU needed; for tests and DESIGN.md).  info[0..7] = n, P, Q, W, R, RV,
- * S (A steps), St (A^T steps, 0 unless with_transpose).  words/vpos (and
- * twords/tvpos) may be NULL to query sizes: words S*W*32, vpos k*nnz. */
+ * (no GPU needed; for tests and DESIGN.md).  info[0..11] = n, P, Q, W, R,
+ * RV, S (A steps), St (A^T steps, 0 unless with_transpose), xslots,
+ * txslots (shared slots of the gathered vectors), modelled gather
+ * wavefronts of one A pass and one A^T pass.  The array outputs may be NULL
+ * to query sizes: words S*W*32, vpos k*nnz, xpos n (row -> gather slot). */
 int bc_schedule_export(int32_t species, const int32_t* row_ptr, const int32_t* col_idx, int32_t k,
                        int32_t with_transpose, int32_t* info, uint32_t* words, int32_t* vpos,
-                       uint32_t* twords, int32_t* tvpos);
+                       int32_t* xpos, uint32_t* twords, int32_t* tvpos, int32_t* txpos);
 
 /*
  * Solve every cell's system A_c x_c = b_c (x0 = 0, as solve_group does).

@@ -59,6 +59,9 @@ struct BlockParams {
     const int32_t* vidx;    // schedule slot -> group value index (level 2)
     const int32_t* tvidx;
     const int32_t* didx;    // group row -> group value index of the diagonal, -1 if none
+    const int32_t* xpos;    // group row -> shared slot of the gathered vector (A pass)
+    const int32_t* txpos;   // same for the A^T pass (BiCG)
+    int xslots, txslots;    // shared slots of the gathered vectors (multiples of 32)
 };
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -84,8 +87,9 @@ template <int W, int R, int RV>
 struct Ctx {
     Team<W> tm;
     int n, P;
-    double* Xs;   // gather source
-    double* Xs2;  // second gather source (BiCG: p~)
+    double* Xs;   // gather source, row(j) stored at slot xa[j]
+    double* Xs2;  // second gather source (BiCG: p~), row(j) at slot xt[j]
+    int xa[RV], xt[RV];
     double* Ys;   // A products
     double* Yt;   // A^T products (BiCG)
     double* red;  // cross-warp partials [2][4][W][32]
@@ -190,7 +194,7 @@ template <int W, int R, int RV>
 __device__ __forceinline__ void team_spmv(Ctx<W, R, RV>& c, const double (&x)[RV], double (&y)[RV]) {
 #pragma unroll
     for (int j = 0; j < RV; ++j)
-        if (c.valid(j)) c.Xs[c.row(j)] = x[j];
+        if (c.valid(j)) c.Xs[c.xa[j]] = x[j];
     c.tm.sync();
     sched_pass<W>(c.Wa, c.Va, c.Ia, c.Sa, c.tm.tid, c.Xs, c.Ys);
     c.tm.sync();
@@ -205,8 +209,8 @@ __device__ __forceinline__ void team_spmv_pair(Ctx<W, R, RV>& c, const double (&
 #pragma unroll
     for (int j = 0; j < RV; ++j)
         if (c.valid(j)) {
-            c.Xs[c.row(j)] = p[j];
-            c.Xs2[c.row(j)] = ps[j];
+            c.Xs[c.xa[j]] = p[j];
+            c.Xs2[c.xt[j]] = ps[j];
         }
     c.tm.sync();
     sched_pass<W>(c.Wa, c.Va, c.Ia, c.Sa, c.tm.tid, c.Xs, c.Ys);
@@ -265,10 +269,15 @@ __global__ void __launch_bounds__(256, 1) block_cells_kernel(const BlockParams p
     double* Vt = Vs + p.S * LW;
     double* tail = values_smem ? Vt + (ALGO == kBiCG ? p.St * LW : 0) : Vs;
     c.Xs = tail;
-    c.Ys = tail + n_pad;
+    c.Ys = tail + p.xslots;
     c.Xs2 = c.Ys + n_pad;
-    c.Yt = c.Xs2 + (ALGO == kBiCG ? n_pad : 0);
+    c.Yt = c.Xs2 + (ALGO == kBiCG ? p.txslots : 0);
     c.red = c.Yt + (ALGO == kBiCG ? n_pad : 0);
+#pragma unroll
+    for (int j = 0; j < RV; ++j) {
+        c.xa[j] = c.valid(j) ? p.xpos[c.row(j)] : 0;
+        c.xt[j] = (ALGO == kBiCG && c.valid(j)) ? p.txpos[c.row(j)] : 0;
+    }
     c.red_buf = 0;
     c.Wa = words_smem ? s_words : p.words;
     c.Wt = words_smem ? s_twords : p.twords;

@@ -183,7 +183,9 @@ bc::GroupPlan& get_plan(bc_ctx* ctx, const bc::Pattern& pat, int k, bool with_t,
     gp.d_dpos = upload(ctx, gp.dpos);
     gp.d_vidx = upload(ctx, gp.a.vidx);
     gp.d_didx = upload(ctx, gp.didx);
+    gp.d_xpos = upload(ctx, gp.a.xpos);
     if (with_t) {
+        gp.d_txpos = upload(ctx, gp.at.xpos);
         gp.d_twords = upload(ctx, gp.at.words);
         gp.d_tvpos = upload(ctx, gp.at.vpos);
         gp.d_tvidx = upload(ctx, gp.at.vidx);
@@ -209,7 +211,8 @@ LaunchShape choose_shape(bc_ctx* ctx, BlockFn fn, const bc::GroupPlan& gp, bool 
         ctx->smem_set[fn] = true;
     }
     const int sched = gp.a.steps * LW + (bicg ? gp.at.steps * LW : 0);
-    const int vecs = n_pad * (bicg ? 4 : 2) + (W > 1 ? 8 * W * 32 : 0);
+    const int xa = (gp.a.xslots + 31) & ~31, xt = bicg ? (gp.at.xslots + 31) & ~31 : 0;
+    const int vecs = xa + n_pad + (bicg ? xt + n_pad : 0) + (W > 1 ? 8 * W * 32 : 0);
     for (int level = 0; level <= 2; ++level) {
         LaunchShape sh;
         sh.level = level;
@@ -286,6 +289,10 @@ void launch_block(bc_ctx* ctx, const bc::Pattern& pat, const bc::GroupPlan& gp, 
     p.vidx = gp.d_vidx;
     p.tvidx = gp.d_tvidx;
     p.didx = gp.d_didx;
+    p.xpos = gp.d_xpos;
+    p.txpos = gp.d_txpos;
+    p.xslots = (gp.a.xslots + 31) & ~31;
+    p.txslots = bicg ? (gp.at.xslots + 31) & ~31 : 0;
     check_cuda(cudaMemsetAsync(counter, 0, sizeof(unsigned int), st), "cudaMemsetAsync(counter)");
     fn<<<sh.blocks, sh.threads, sh.smem, st>>>(p);
     check_cuda(cudaGetLastError(), "block_cells_kernel launch");
@@ -419,17 +426,20 @@ int bc_plan(int32_t species, const bc_solve_params* prm, int64_t* n_groups, doub
 }
 
 int bc_schedule_export(int32_t species, const int32_t* row_ptr, const int32_t* col_idx, int32_t k,
-                       int32_t with_t, int32_t* info, uint32_t* words, int32_t* vpos, uint32_t* twords,
-                       int32_t* tvpos) {
+                       int32_t with_t, int32_t* info, uint32_t* words, int32_t* vpos, int32_t* xpos,
+                       uint32_t* twords, int32_t* tvpos, int32_t* txpos) {
     if (!info || k < 1) return BC_ERR_INVALID_ARGUMENT;
     return guarded(nullptr, [&] {
         const bc::Pattern pat = make_pattern(species, row_ptr, col_idx);
         const bc::GroupPlan gp = bc::build_group_plan(pat, k, with_t != 0);
-        const int v[8] = {gp.geo.n, gp.geo.P, gp.geo.Q, gp.geo.W, gp.geo.R, gp.geo.RV, gp.a.steps,
-                          with_t ? gp.at.steps : 0};
+        const int v[12] = {gp.geo.n, gp.geo.P, gp.geo.Q, gp.geo.W, gp.geo.R, gp.geo.RV, gp.a.steps,
+                           with_t ? gp.at.steps : 0, gp.a.xslots, with_t ? gp.at.xslots : 0,
+                           gp.a.conflict_cost, with_t ? gp.at.conflict_cost : 0};
         std::memcpy(info, v, sizeof v);
         if (words) std::memcpy(words, gp.a.words.data(), sizeof(uint32_t) * gp.a.words.size());
         if (vpos) std::memcpy(vpos, gp.a.vpos.data(), sizeof(int32_t) * gp.a.vpos.size());
+        if (xpos) std::memcpy(xpos, gp.a.xpos.data(), sizeof(int32_t) * gp.a.xpos.size());
+        if (with_t && txpos) std::memcpy(txpos, gp.at.xpos.data(), sizeof(int32_t) * gp.at.xpos.size());
         if (with_t && twords) std::memcpy(twords, gp.at.words.data(), sizeof(uint32_t) * gp.at.words.size());
         if (with_t && tvpos) std::memcpy(tvpos, gp.at.vpos.data(), sizeof(int32_t) * gp.at.vpos.size());
         return BC_OK;
@@ -482,8 +492,9 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
         const int64_t launches0 = ctx->launches;
 
         const bool timing = (prm->options & BC_OPT_TIMING) != 0;
-        if (timing) check_cuda(cudaEventRecord(ctx->e0, st), "cudaEventRecord");
         const bool bicg = prm->algo == BC_ALGO_BICG;
+        for (const GroupSpan& sp : spans) get_plan(ctx, pat, sp.k, bicg, &ctx->plans);  // host work first
+        if (timing) check_cuda(cudaEventRecord(ctx->e0, st), "cudaEventRecord");
         int slot = 0;
         for (const GroupSpan& sp : spans) {
             const bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);

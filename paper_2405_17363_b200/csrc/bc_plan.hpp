@@ -45,6 +45,9 @@ struct Schedule {
     std::vector<uint32_t> words;    // S * LW
     std::vector<int32_t> vpos;      // group value index -> smem slot (t*LW + L)
     std::vector<int32_t> vidx;      // smem slot -> group value index (0 for padding)
+    int xslots = 0;                 // shared-memory slots of the gathered vector
+    std::vector<int32_t> xpos;      // group row -> slot of its gathered value
+    int conflict_cost = 0;          // modelled gather wavefronts per pass
 };
 
 struct GroupPlan {
@@ -62,10 +65,13 @@ struct GroupPlan {
     int32_t* d_vidx = nullptr;
     int32_t* d_tvidx = nullptr;
     int32_t* d_didx = nullptr;
+    int32_t* d_xpos = nullptr;
+    int32_t* d_txpos = nullptr;
 };
 
-Schedule build_schedule(const Pattern& pat, int k, int lanes, bool transpose);
-GroupPlan build_group_plan(const Pattern& pat, int k, bool with_transpose);
+Schedule build_schedule(const Pattern& pat, int k, int lanes, bool transpose, bool optimize = true);
+GroupPlan build_group_plan(const Pattern& pat, int k, bool with_transpose, bool optimize = true);
+int gather_cost(int steps, int lanes, const std::vector<uint32_t>& words);
 
 inline int64_t padded_len(int64_t n) {
     if (n <= 1) return 1;

@@ -80,28 +80,36 @@ def test_plan_errors():
 
 def export_schedule(rp, ci, k, with_t):
     species = len(rp) - 1
-    info = np.zeros(8, np.int32)
+    info = np.zeros(12, np.int32)
     lib = _native.b200()
     rp = np.ascontiguousarray(rp, np.int32)
     ci = np.ascontiguousarray(ci, np.int32)
-    st = lib.bc_schedule_export(species, of.ptr(rp), of.ptr(ci), k, with_t, of.ptr(info), None, None, None, None)
+    st = lib.bc_schedule_export(species, of.ptr(rp), of.ptr(ci), k, with_t, of.ptr(info), None, None, None, None,
+                                None, None)
     assert st == 0
-    n, P, Q, W, R, RV, S, St = info.tolist()
+    n, P, Q, W, R, RV, S, St, xs, txs, cost, tcost = info.tolist()
     nnz = int(rp[-1])
     words = np.zeros(max(S * W * 32, 1), np.uint32)
     vpos = np.zeros(k * nnz, np.int32)
     twords = np.zeros(max(St * W * 32, 1), np.uint32)
     tvpos = np.zeros(k * nnz, np.int32)
+    xpos = np.zeros(n, np.int32)
+    txpos = np.zeros(n, np.int32)
     st = lib.bc_schedule_export(species, of.ptr(rp), of.ptr(ci), k, with_t, of.ptr(info), of.ptr(words),
-                                of.ptr(vpos), of.ptr(twords), of.ptr(tvpos))
+                                of.ptr(vpos), of.ptr(xpos), of.ptr(twords), of.ptr(tvpos), of.ptr(txpos))
     assert st == 0
-    return dict(n=n, P=P, Q=Q, W=W, R=R, RV=RV, S=S, St=St, words=words, vpos=vpos, twords=twords, tvpos=tvpos)
+    return dict(n=n, P=P, Q=Q, W=W, R=R, RV=RV, S=S, St=St, words=words, vpos=vpos, twords=twords, tvpos=tvpos,
+                xpos=xpos, txpos=txpos, xslots=xs, txslots=txs, cost=cost, tcost=tcost)
 
 
-def emulate_pass(words, vpos, vals, S, LW, x, n):
-    """sched_pass() of bc_block.cuh in exact double arithmetic."""
+def emulate_pass(words, vpos, vals, S, LW, x, n, xpos, xslots):
+    """team_spmv() of bc_block.cuh in exact double arithmetic: publish x at its
+    slots, then every lane walks its schedule."""
     V = np.zeros(S * LW)
     V[vpos] = vals
+    X = np.full(xslots, np.nan)  # unused slots must never be read
+    X[xpos] = x
+    x = X
     y = np.zeros(n)
     for L in range(LW):
         acc = 0.0
@@ -149,12 +157,13 @@ def test_schedule_reproduces_spmv_order(species, k, density, seed):
     LW = sc["W"] * 32
     vals = rng.uniform(-1, 1, k * nnz) * 10.0 ** rng.integers(-8, 8, k * nnz)
     x = rng.uniform(-1, 1, k * species)
-    y = emulate_pass(sc["words"], sc["vpos"], vals, sc["S"], LW, x, k * species)
+    y = emulate_pass(sc["words"], sc["vpos"], vals, sc["S"], LW, x, k * species, sc["xpos"], sc["xslots"])
     np.testing.assert_array_equal(of.bits(y), of.bits(ref_spmv(rp, ci, vals, x, k, species, nnz)))
-    yt = emulate_pass(sc["twords"], sc["tvpos"], vals, sc["St"], LW, x, k * species)
+    yt = emulate_pass(sc["twords"], sc["tvpos"], vals, sc["St"], LW, x, k * species, sc["txpos"], sc["txslots"])
     np.testing.assert_array_equal(of.bits(yt), of.bits(ref_spmv_t(rp, ci, vals, x, k, species, nnz)))
     assert sc["S"] * LW >= k * nnz  # every value has a slot
     assert sorted(sc["vpos"].tolist()) == sorted(set(sc["vpos"].tolist()))
+    assert len(set(sc["xpos"].tolist())) == k * species and sc["xpos"].max() < sc["xslots"]
 
 
 def emulate_team_reduce(vals, n, P, W, R):
@@ -198,12 +207,12 @@ def emulate_team_reduce(vals, n, P, W, R):
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 16, 17, 31, 32, 33, 100, 156, 255, 256, 257, 312, 500, 936, 1024, 1500,
                                2048])
 def test_reduction_geometry_reproduces_tree(n):
-    info = np.zeros(8, np.int32)
+    info = np.zeros(12, np.int32)
     rp = np.arange(n + 1, dtype=np.int32)
     ci = np.arange(n, dtype=np.int32)
     assert _native.b200().bc_schedule_export(n, of.ptr(rp), of.ptr(ci), 1, 0, of.ptr(info), None, None, None,
-                                              None) == 0
-    _, P, Q, W, R, RV, _, _ = info.tolist()
+                                              None, None, None) == 0
+    _, P, Q, W, R, RV = info.tolist()[:6]
     assert W * R == Q and P >= n
     rng = np.random.default_rng(n)
     for _ in range(5):
