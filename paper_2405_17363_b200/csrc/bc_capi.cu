@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -15,6 +16,7 @@
 #include "bc_block.cuh"
 #include "bc_lu.cuh"
 #include "bc_newton.cuh"
+#include "bc_tmem.cuh"
 #include "bc_plan.hpp"
 #include "blockcells_b200.h"
 
@@ -244,6 +246,81 @@ LaunchShape choose_shape(bc_ctx* ctx, BlockFn fn, const bc::GroupPlan& gp, bool 
     }
     fail(BC_ERR_INVALID_ARGUMENT, "group does not fit in shared memory");
     return LaunchShape{};
+}
+
+using TmemFn = void (*)(bc::TmemParams);
+
+struct TmemCfg {
+    int R, RV;
+    TmemFn fn;
+};
+
+const TmemCfg kTmemConfigs[] = {
+    {8, 5, &bc::block_cells_tmem_kernel<8, 5>},
+    {8, 8, &bc::block_cells_tmem_kernel<8, 8>},
+    {4, 4, &bc::block_cells_tmem_kernel<4, 4>},
+};
+
+bool tmem_disabled() {
+    const char* e = std::getenv("BC_KERNEL");
+    return e && std::string(e) == "v1";
+}
+
+// The TMEM kernel (bc_tmem.cuh): Jacobi-BiCGSTAB, one warp per group, schedule
+// words + per-group values resident in Tensor Memory.  Returns false when the
+// group does not qualify (the caller then uses the v1 kernel).
+bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, const bc::GroupPlan& gp, int64_t cell0, int64_t gout0,
+                 int groups, const double* values, const double* rhs, double* x, double tol, int64_t max_iter,
+                 unsigned int* counter, cudaStream_t st) {
+    if (tmem_disabled() || gp.geo.W != 1) return false;
+    const TmemCfg* cfg = nullptr;
+    for (const TmemCfg& t : kTmemConfigs)
+        if (t.R == gp.geo.R && t.RV >= gp.geo.RV && (!cfg || t.RV < cfg->RV)) cfg = &t;
+    if (!cfg) return false;
+    const int S8 = (gp.a.steps + 7) & ~7;
+    const int cpq = std::min(4, (512 - S8) / (2 * S8));
+    if (S8 == 0 || cpq < 1) return false;
+    const int warps = 4 * cpq;
+    const int xslots = (gp.a.xslots + 31) & ~31, n_pad = (gp.geo.n + 31) & ~31;
+    const size_t smem = sizeof(int32_t) * S8 * 32 + sizeof(double) * warps * (xslots + n_pad);
+    if (!ctx->smem_set[reinterpret_cast<BlockFn>(cfg->fn)]) {
+        check_cuda(cudaFuncSetAttribute(cfg->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem - 1024),
+                   "cudaFuncSetAttribute(tmem)");
+        ctx->smem_set[reinterpret_cast<BlockFn>(cfg->fn)] = true;
+    }
+    if (smem > static_cast<size_t>(kMaxDynSmem - 1024)) return false;
+    bc::TmemParams p{};
+    p.values = values;
+    p.rhs = rhs;
+    p.x_out = x;
+    p.g_iters = ctx->giters.as<int32_t>();
+    p.g_rms = ctx->grms.as<double>();
+    p.g_flags = ctx->gflags.as<uint8_t>();
+    p.words = gp.d_words;
+    p.vidx = gp.d_vidx;
+    p.didx = gp.d_didx;
+    p.xpos = gp.d_xpos;
+    p.counter = counter;
+    p.cell_offset = cell0;
+    p.group_offset = gout0;
+    p.group_count = groups;
+    p.n = gp.geo.n;
+    p.nnz = pat.nnz;
+    p.S = gp.a.steps;
+    p.S8 = S8;
+    p.P = gp.geo.P;
+    p.species = pat.species;
+    p.kc = gp.k;
+    p.xslots = xslots;
+    p.cells_per_quarter = cpq;
+    p.tol = tol;
+    p.max_iter = max_iter;
+    const int blocks = std::max(1, std::min(ctx->sms, (groups + warps - 1) / warps));
+    check_cuda(cudaMemsetAsync(counter, 0, sizeof(unsigned int), st), "cudaMemsetAsync(counter)");
+    cfg->fn<<<blocks, warps * 32, smem, st>>>(p);
+    check_cuda(cudaGetLastError(), "block_cells_tmem_kernel launch");
+    ctx->launches++;
+    return true;
 }
 
 // Launch the fused kernel over `groups` groups of kc cells starting at cell0.
@@ -498,9 +575,12 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
         int slot = 0;
         for (const GroupSpan& sp : spans) {
             const bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);
+            unsigned int* counter = ctx->counters.as<unsigned int>() + slot++;
+            if (!bicg && launch_tmem(ctx, pat, gp, sp.cell0, sp.gout0, sp.count, d_values, d_rhs, d_x, prm->tol,
+                                     prm->max_iter, counter, st))
+                continue;
             launch_block(ctx, pat, gp, prm->algo, sp.cell0, sp.gout0, sp.count, d_values, d_rhs,
-                         nullptr, d_x, prm->tol, prm->max_iter,
-                         ctx->counters.as<unsigned int>() + slot++, st);
+                         nullptr, d_x, prm->tol, prm->max_iter, counter, st);
         }
         // breakdown groups -> device LU fallback
         std::vector<uint8_t> flags(n_groups);
