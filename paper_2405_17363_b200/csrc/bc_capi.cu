@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -251,15 +252,21 @@ LaunchShape choose_shape(bc_ctx* ctx, BlockFn fn, const bc::GroupPlan& gp, bool 
 using TmemFn = void (*)(bc::TmemParams);
 
 struct TmemCfg {
-    int R, RV;
+    int R, RV, warps;  // warps per CTA (= 4 * groups per lane quarter)
     TmemFn fn;
 };
 
+// 16 warps/SM at <= 128 registers, or 12 warps/SM at <= 168 registers.
 const TmemCfg kTmemConfigs[] = {
-    {8, 5, &bc::block_cells_tmem_kernel<8, 5>},
-    {8, 8, &bc::block_cells_tmem_kernel<8, 8>},
-    {4, 4, &bc::block_cells_tmem_kernel<4, 4>},
+    {8, 5, 16, &bc::block_cells_tmem_kernel<8, 5, 512>}, {8, 5, 12, &bc::block_cells_tmem_kernel<8, 5, 384>},
+    {8, 8, 16, &bc::block_cells_tmem_kernel<8, 8, 512>}, {8, 8, 12, &bc::block_cells_tmem_kernel<8, 8, 384>},
+    {4, 4, 16, &bc::block_cells_tmem_kernel<4, 4, 512>}, {4, 4, 12, &bc::block_cells_tmem_kernel<4, 4, 384>},
 };
+
+int tmem_warps_pref() {
+    const char* e = std::getenv("BC_TMEM_WARPS");
+    return e ? std::atoi(e) : 16;
+}
 
 bool tmem_disabled() {
     const char* e = std::getenv("BC_KERNEL");
@@ -269,26 +276,83 @@ bool tmem_disabled() {
 // The TMEM kernel (bc_tmem.cuh): Jacobi-BiCGSTAB, one warp per group, schedule
 // words + per-group values resident in Tensor Memory.  Returns false when the
 // group does not qualify (the caller then uses the v1 kernel).
-bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, const bc::GroupPlan& gp, int64_t cell0, int64_t gout0,
+// Largest sigma with sqrt(sigma / n) <= tol, both correctly rounded (x86-64
+// SSE2 here, __dsqrt_rn/__ddiv_rn on the GPU), so that the kernel's test
+// sigma <= sigma_max decides exactly as bicg.cpp:84/129 does.  The predicate
+// is monotone in sigma, so a bisection over the ordered bit patterns of
+// non-negative doubles finds the boundary.
+double sigma_threshold(double tol, int n) {
+    auto ok = [&](double s) { return std::sqrt(s / static_cast<double>(n)) <= tol; };
+    uint64_t lo = 0, hi = 0x7FF0000000000000ull;  // ok(+0) is true (tol > 0)
+    double dhi;
+    std::memcpy(&dhi, &hi, 8);
+    if (ok(dhi)) return dhi;  // tol = +inf
+    while (hi - lo > 1) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        double dm;
+        std::memcpy(&dm, &mid, 8);
+        (ok(dm) ? lo : hi) = mid;
+    }
+    double r;
+    std::memcpy(&r, &lo, 8);
+    return r;
+}
+
+void ensure_tmem_schedule(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp) {
+    if (gp.has_tm || tmem_disabled() || gp.geo.W != 1) return;
+    gp.tm = bc::build_tmem_schedule(pat, gp.k);
+    gp.d_tm_words = upload(ctx, gp.tm.words);
+    gp.d_tm_vidx = upload(ctx, gp.tm.vidx);
+    gp.has_tm = true;
+}
+
+// Per-lane owner tables for a kernel instance with RV row slots: copy-0
+// gather slot | Y slot << 16, and the further copies' slots; rows >= n go to
+// the trash slot (after every copy) and read the zero Y slot.
+void ensure_tmem_lane_tables(bc_ctx* ctx, bc::GroupPlan& gp, int RV) {
+    if (gp.tm_lane_rv == RV) return;
+    const int n = gp.geo.n, R = gp.tm.copies, trash = gp.tm.xslots;
+    std::vector<uint32_t> xy(static_cast<size_t>(RV) * 32);
+    std::vector<uint16_t> xmore(static_cast<size_t>(std::max(1, R - 1)) * RV * 32, static_cast<uint16_t>(trash));
+    for (int j = 0; j < RV; ++j)
+        for (int l = 0; l < 32; ++l) {
+            const int row = j * 32 + l;
+            const bool ok = row < n;
+            xy[j * 32 + l] = static_cast<uint32_t>(ok ? gp.tm.xpos[row] : trash) |
+                             (static_cast<uint32_t>(ok ? gp.tm.yslot[row] : gp.tm.yslots) << 16);
+            for (int r = 1; r < R; ++r)
+                xmore[((r - 1) * RV + j) * 32 + l] =
+                    static_cast<uint16_t>(ok ? gp.tm.xpos[static_cast<size_t>(r) * n + row] : trash);
+        }
+    gp.d_tm_lane_xy = upload(ctx, xy);
+    gp.d_tm_lane_xmore = upload(ctx, xmore);
+    gp.tm_lane_rv = RV;
+}
+
+bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t cell0, int64_t gout0,
                  int groups, const double* values, const double* rhs, double* x, double tol, int64_t max_iter,
                  unsigned int* counter, cudaStream_t st) {
     if (tmem_disabled() || gp.geo.W != 1) return false;
     const TmemCfg* cfg = nullptr;
+    const int pref = tmem_warps_pref();
     for (const TmemCfg& t : kTmemConfigs)
-        if (t.R == gp.geo.R && t.RV >= gp.geo.RV && (!cfg || t.RV < cfg->RV)) cfg = &t;
+        if (t.R == gp.geo.R && t.RV >= gp.geo.RV && t.warps == pref && (!cfg || t.RV < cfg->RV)) cfg = &t;
     if (!cfg) return false;
-    const int S8 = (gp.a.steps + 7) & ~7;
-    const int cpq = std::min(4, (512 - S8) / (2 * S8));
-    if (S8 == 0 || cpq < 1) return false;
+    ensure_tmem_schedule(ctx, pat, gp);
+    ensure_tmem_lane_tables(ctx, gp, cfg->RV);
+    const int S = gp.tm.steps;
+    const int cpq = S > 0 ? std::min(cfg->warps / 4, (512 - S / 2) / (2 * S)) : 0;
+    if (cpq < 1) return false;
     const int warps = 4 * cpq;
-    const int xslots = (gp.a.xslots + 31) & ~31, n_pad = (gp.geo.n + 31) & ~31;
-    const size_t smem = sizeof(int32_t) * S8 * 32 + sizeof(double) * warps * (xslots + n_pad);
+    const int xslots = (gp.tm.xslots + 1 + 31) & ~31, yslots = gp.tm.yslots + 32;
+    const size_t xmore_bytes = ((2 * (gp.tm.copies - 1) * cfg->RV * 32) + 15) & ~15;
+    const size_t smem = sizeof(int32_t) * S * 32 + xmore_bytes + sizeof(double) * warps * (xslots + yslots);
+    if (smem > static_cast<size_t>(kMaxDynSmem - 1024)) return false;
     if (!ctx->smem_set[reinterpret_cast<BlockFn>(cfg->fn)]) {
         check_cuda(cudaFuncSetAttribute(cfg->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem - 1024),
                    "cudaFuncSetAttribute(tmem)");
         ctx->smem_set[reinterpret_cast<BlockFn>(cfg->fn)] = true;
     }
-    if (smem > static_cast<size_t>(kMaxDynSmem - 1024)) return false;
     bc::TmemParams p{};
     p.values = values;
     p.rhs = rhs;
@@ -296,25 +360,28 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, const bc::GroupPlan& gp, i
     p.g_iters = ctx->giters.as<int32_t>();
     p.g_rms = ctx->grms.as<double>();
     p.g_flags = ctx->gflags.as<uint8_t>();
-    p.words = gp.d_words;
-    p.vidx = gp.d_vidx;
+    p.words = gp.d_tm_words;
+    p.vidx = gp.d_tm_vidx;
     p.didx = gp.d_didx;
-    p.xpos = gp.d_xpos;
+    p.lane_xy = gp.d_tm_lane_xy;
+    p.lane_xmore = gp.d_tm_lane_xmore;
     p.counter = counter;
     p.cell_offset = cell0;
     p.group_offset = gout0;
     p.group_count = groups;
     p.n = gp.geo.n;
     p.nnz = pat.nnz;
-    p.S = gp.a.steps;
-    p.S8 = S8;
+    p.S = S;
     p.P = gp.geo.P;
     p.species = pat.species;
     p.kc = gp.k;
     p.xslots = xslots;
+    p.yslots = yslots;
+    p.copies = gp.tm.copies;
     p.cells_per_quarter = cpq;
+    p.sigma_max = sigma_threshold(tol, gp.geo.n);
     p.tol = tol;
-    p.max_iter = max_iter;
+    p.max_iter = static_cast<int>(std::min<int64_t>(max_iter, 0x7FFFFFFF));
     const int blocks = std::max(1, std::min(ctx->sms, (groups + warps - 1) / warps));
     check_cuda(cudaMemsetAsync(counter, 0, sizeof(unsigned int), st), "cudaMemsetAsync(counter)");
     cfg->fn<<<blocks, warps * 32, smem, st>>>(p);
@@ -523,6 +590,22 @@ int bc_schedule_export(int32_t species, const int32_t* row_ptr, const int32_t* c
     });
 }
 
+int bc_tmem_schedule_export(int32_t species, const int32_t* row_ptr, const int32_t* col_idx, int32_t k,
+                            int32_t* info, uint16_t* words, int32_t* vidx, int32_t* xpos, int32_t* yslot) {
+    if (!info || k < 1) return BC_ERR_INVALID_ARGUMENT;
+    return guarded(nullptr, [&] {
+        const bc::Pattern pat = make_pattern(species, row_ptr, col_idx);
+        const bc::TmemSchedule ts = bc::build_tmem_schedule(pat, k);
+        const int v[7] = {ts.steps, ts.xslots, ts.zero_slot, ts.yslots, ts.conflict_cost, ts.copies, ts.model_total};
+        std::memcpy(info, v, sizeof v);
+        if (words) std::memcpy(words, ts.words.data(), sizeof(uint16_t) * ts.words.size());
+        if (vidx) std::memcpy(vidx, ts.vidx.data(), sizeof(int32_t) * ts.vidx.size());
+        if (xpos) std::memcpy(xpos, ts.xpos.data(), sizeof(int32_t) * ts.xpos.size());
+        if (yslot) std::memcpy(yslot, ts.yslot.data(), sizeof(int32_t) * ts.yslot.size());
+        return BC_OK;
+    });
+}
+
 int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, const double* rhs,
              double* x_out, int32_t* group_iters, double* group_rms, uint8_t* group_flags,
              bc_report* report) {
@@ -570,11 +653,22 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
 
         const bool timing = (prm->options & BC_OPT_TIMING) != 0;
         const bool bicg = prm->algo == BC_ALGO_BICG;
-        for (const GroupSpan& sp : spans) get_plan(ctx, pat, sp.k, bicg, &ctx->plans);  // host work first
+        for (const GroupSpan& sp : spans) {  // host-side planning before the timed region
+            bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);
+            if (!bicg) {
+                ensure_tmem_schedule(ctx, pat, gp);
+                if (gp.has_tm)
+                    for (const TmemCfg& t : kTmemConfigs)
+                        if (t.R == gp.geo.R && t.RV >= gp.geo.RV) {
+                            ensure_tmem_lane_tables(ctx, gp, t.RV);
+                            break;
+                        }
+            }
+        }
         if (timing) check_cuda(cudaEventRecord(ctx->e0, st), "cudaEventRecord");
         int slot = 0;
         for (const GroupSpan& sp : spans) {
-            const bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);
+            bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);
             unsigned int* counter = ctx->counters.as<unsigned int>() + slot++;
             if (!bicg && launch_tmem(ctx, pat, gp, sp.cell0, sp.gout0, sp.count, d_values, d_rhs, d_x, prm->tol,
                                      prm->max_iter, counter, st))

@@ -50,6 +50,29 @@ struct Schedule {
     int conflict_cost = 0;          // modelled gather wavefronts per pass
 };
 
+// Schedule of the TMEM kernel (bc_tmem.cuh), one warp per group:
+//  * every row is padded to an even number of steps with value-0.0 entries
+//    that gather a dedicated always-zero slot (acc + 0*0 == acc exactly, as a
+//    CSR sum started at +0.0 is never -0.0), so row ends only fall on odd
+//    steps and the end test runs every other step;
+//  * lane L's k-th row lands in Y[k*32 + L] (conflict-free stores, no output
+//    index in the word); yslot maps rows to those slots for the owner lanes;
+//  * words are 16 bits: gather byte offset (slot*8) | end-of-row << 15;
+//  * the gather vector has `copies` independent placements (bc_tmem_plan.cpp).
+struct TmemSchedule {
+    int steps = 0;                  // S, a multiple of 4
+    std::vector<uint16_t> words;    // S * 32
+    std::vector<int32_t> vidx;      // S * 32: group value index, -1 for padding (value 0.0)
+    int copies = 1;                 // independent copies of the gather vector
+    int xslots = 0;                 // gather-vector slots, all copies, incl. zero slots
+    int zero_slot = 0;
+    std::vector<int32_t> xpos;      // [copy][group row] -> gather slot
+    int model_total = 0;            // modelled wavefronts per SpMV (gathers+stores+reads)
+    std::vector<int32_t> yslot;     // group row -> Y slot (k*32 + lane)
+    int yslots = 0;
+    int conflict_cost = 0;          // modelled gather wavefronts per pass
+};
+
 struct GroupPlan {
     int k = 1;
     Geometry geo;
@@ -67,7 +90,17 @@ struct GroupPlan {
     int32_t* d_didx = nullptr;
     int32_t* d_xpos = nullptr;
     int32_t* d_txpos = nullptr;
+    // TMEM-kernel schedule (built on demand: BiCGSTAB, one-warp groups)
+    bool has_tm = false;
+    TmemSchedule tm;
+    uint16_t* d_tm_words = nullptr;
+    int32_t* d_tm_vidx = nullptr;
+    int tm_lane_rv = 0;               // RV the lane tables below were built for
+    uint32_t* d_tm_lane_xy = nullptr;
+    uint16_t* d_tm_lane_xmore = nullptr;
 };
+
+TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize = true);
 
 Schedule build_schedule(const Pattern& pat, int k, int lanes, bool transpose, bool optimize = true);
 GroupPlan build_group_plan(const Pattern& pat, int k, bool with_transpose, bool optimize = true);

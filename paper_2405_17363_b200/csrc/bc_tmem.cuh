@@ -1,26 +1,37 @@
-// bc_tmem.cuh -- Block-cells(1) Jacobi-BiCGSTAB with the SpMV operands in
-// Tensor Memory (the B200 hot path; K1 v2).
+// bc_tmem.cuh -- Block-cells Jacobi-BiCGSTAB with the SpMV operands in Tensor
+// Memory: the B200 hot path (K1 v2).
 //
 // The v1 kernel (bc_block.cuh) is bound by shared-memory wavefronts: per SpMV
 // step a lane loads its schedule word (1 wavefront), its matrix value (2) and
-// the gathered vector entry (~3.7 after placement), plus row-end stores.
-// TMEM (256 KB/SM, read with tcgen05.ld on its own datapath -- measured to
-// overlap completely with LDS traffic, tools/microbench.py) takes the first
-// two off the shared-memory pipe:
+// the gathered vector entry (~3.7), plus row-end stores.  TMEM (256 KB/SM,
+// read with tcgen05.ld on its own datapath -- measured to overlap completely
+// with LDS traffic, tools/microbench.py) takes the first two off the shared-
+// memory pipe:
 //
-//   TMEM lane 32q+L, columns [0, S8)            schedule word of step t for lane L
-//                                               (one copy per lane quarter q, shared
-//                                               by the quarter's warps)
-//   TMEM lane 32q+L, columns [S8 + 2*S8*s, ...) value of step t for lane L of the
-//                                               cell held by warp (q, s), fp64 as
-//                                               two 32-bit columns
+//   TMEM lane 32q+L, columns [0, S/2)        16-bit schedule words of lane L,
+//                                            two steps per column (one copy per
+//                                            lane quarter q, shared by its warps)
+//   TMEM lane 32q+L, columns [S/2 + 2S*s,..) fp64 values of lane L's steps for the
+//                                            group held by warp (q, s)
 //
-// Every step's column address is warp-uniform, which is exactly the
-// tcgen05.ld.32x32b shape (each thread reads its own lane).  A CTA is 16 warps
-// (4 per lane quarter), owns all 512 columns, and stays resident (one per SM);
-// each warp solves one cell at a time, fetched from an atomic counter.
-// Arithmetic, schedule order and reductions are those of bc_block.cuh, so the
-// results are bit-identical to v1 and to the oracle.
+// Every step's column address is warp-uniform -- exactly the tcgen05.ld.32x32b
+// shape (each thread reads its own lane).  A CTA is 4*cells_per_quarter warps,
+// owns all 512 columns and stays resident (one per SM); each warp solves one
+// group at a time, fetched from an atomic counter.  The schedule
+// (bc_plan.hpp TmemSchedule, bc_tmem_plan.cpp) pads rows to even length with
+// zero entries so the row-end test runs every other step, writes lane L's
+// k-th row to Y[k*32+L], and keeps `copies` placements of the gathered vector
+// so that almost every gather is bank-conflict free.
+//
+// Rows beyond n (register slots of the padded reduction tree) carry exact
+// +0.0 through every update -- 0-(+-0) = +0, 0+(+-0) = +0, 0*0 = +0 -- so the
+// arithmetic needs no validity tests: those rows publish into a trash slot and
+// read the always-zero Y slot.  The convergence test sqrt(sigma/n) <= tol is
+// evaluated as sigma <= sigma_max with sigma_max computed on the host as the
+// largest double satisfying it (sqrt and / are correctly rounded and
+// monotone, so the two tests agree for every sigma, NaN included).
+// Arithmetic order and reductions are those of bc_block.cuh and the oracle:
+// results are bit-identical.
 #pragma once
 
 #include <cstdint>
@@ -37,32 +48,35 @@ struct TmemParams {
     int32_t* g_iters;
     double* g_rms;
     uint8_t* g_flags;
-    const uint32_t* words;  // S * 32 (A schedule)
-    const int32_t* vidx;    // S * 32: schedule slot -> value index in the cell
-    const int32_t* didx;    // species: value index of the diagonal, -1 if none
-    const int32_t* xpos;    // species: gather slot of each row
+    const uint16_t* words;  // S * 32: gather byte offset | end << 15
+    const int32_t* vidx;    // S * 32: group value index, -1 = padding (0.0)
+    const int32_t* didx;    // n: group value index of the diagonal, -1 if none
+    const uint32_t* lane_xy;  // RV * 32: copy-0 gather slot | Y slot << 16 per (slot j, lane)
+    const uint16_t* lane_xmore;  // (copies-1) * RV * 32: gather slots of further copies
     unsigned int* counter;
     int64_t cell_offset, group_offset;
     int group_count;
-    int n, nnz, S, S8, P;
+    int n, nnz, S, P;
     int species, kc;        // group = kc cells of `species` rows
-    int xslots;             // shared doubles of the gather vector (multiple of 32)
+    int xslots, yslots;     // shared doubles per warp: X | Y (multiples of 32)
+    int copies;             // copies of the gather vector (1..4)
     int cells_per_quarter;  // warps per lane quarter
-    double tol;
-    int64_t max_iter;
+    double sigma_max;       // sqrt(sigma/n) <= tol  <=>  sigma <= sigma_max
+    double tol;             // the fresh-residual test keeps the literal comparison
+    int max_iter;
 };
 
+__device__ __forceinline__ void tm_ld_x2(uint32_t addr, uint32_t (&r)[2]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n" : "=r"(r[0]), "=r"(r[1]) : "r"(addr));
+}
 __device__ __forceinline__ void tm_ld_x8(uint32_t addr, uint32_t (&r)[8]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                  : "r"(addr));
 }
-__device__ __forceinline__ void tm_ld_x16(uint32_t addr, uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(addr));
+__device__ __forceinline__ void tm_st_x2(uint32_t addr, const uint32_t (&r)[2]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};\n" ::"r"(addr), "r"(r[0]), "r"(r[1])
+                 : "memory");
 }
 __device__ __forceinline__ void tm_st_x8(uint32_t addr, const uint32_t (&r)[8]) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(addr),
@@ -72,43 +86,87 @@ __device__ __forceinline__ void tm_st_x8(uint32_t addr, const uint32_t (&r)[8]) 
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
-// y = A x: publish x at its gather slots, walk the TMEM-resident schedule
-// (8 steps per tcgen05.ld pair), results through the shared Y vector.
-template <int R, int RV>
-__device__ __forceinline__ void tmem_spmv(const Ctx<1, R, RV>& c, uint32_t wcol, uint32_t vcol, int S8,
-                                          const double (&x)[RV], double (&y)[RV]) {
+// Everything a warp needs to run one SpMV of its group.
+template <int RV>
+struct TmemWarp {
+    double* Xs;             // gather vector copies (+ trash slot), this warp
+    double* Ys;             // row sums, lane-major, this warp
+    uint32_t xy[RV];        // copy-0 gather slot | Y slot << 16 of row slot j
+    const uint16_t* xmore;  // shared table of further copies' slots
+    int copies;
+    int lane;
+    uint32_t wcol, vcol;    // TMEM addresses: words, this warp's values
+    int S;
+};
+
+// Four schedule steps out of one TMEM chunk: gathers issued first, then the
+// ordered multiply-add chain; rows end only on odd steps (u = 1, 3).
+__device__ __forceinline__ void tmem_steps4(const char* xb, const uint32_t (&w)[2], const uint32_t (&v)[8],
+                                            double& acc, double*& yp) {
+    const uint32_t w0 = w[0] & 0xFFFFu, w1 = w[0] >> 16, w2 = w[1] & 0xFFFFu, w3 = w[1] >> 16;
+    const double x0 = *reinterpret_cast<const double*>(xb + (w0 & 0x7FFFu));
+    const double x1 = *reinterpret_cast<const double*>(xb + (w1 & 0x7FFFu));
+    const double x2 = *reinterpret_cast<const double*>(xb + (w2 & 0x7FFFu));
+    const double x3 = *reinterpret_cast<const double*>(xb + (w3 & 0x7FFFu));
+    const double a0 = __hiloint2double(static_cast<int>(v[1]), static_cast<int>(v[0]));
+    const double a1 = __hiloint2double(static_cast<int>(v[3]), static_cast<int>(v[2]));
+    const double a2 = __hiloint2double(static_cast<int>(v[5]), static_cast<int>(v[4]));
+    const double a3 = __hiloint2double(static_cast<int>(v[7]), static_cast<int>(v[6]));
+    acc = dadd(acc, dmul(a0, x0));
+    acc = dadd(acc, dmul(a1, x1));
+    if (w1 & 0x8000u) {
+        *yp = acc;
+        yp += 32;
+        acc = 0.0;
+    }
+    acc = dadd(acc, dmul(a2, x2));
+    acc = dadd(acc, dmul(a3, x3));
+    if (w3 & 0x8000u) {
+        *yp = acc;
+        yp += 32;
+        acc = 0.0;
+    }
+}
+
+// y = A x: publish x into every copy of the gather vector, walk the
+// TMEM-resident schedule (4 steps per tcgen05.ld pair; other warps hide the latency),
+// collect the row sums from Y.
+template <int RV>
+__device__ __forceinline__ void tmem_spmv(const TmemWarp<RV>& tw, const double (&x)[RV], double (&y)[RV]) {
 #pragma unroll
-    for (int j = 0; j < RV; ++j)
-        if (c.valid(j)) c.Xs[c.xa[j]] = x[j];
+    for (int j = 0; j < RV; ++j) {
+        tw.Xs[tw.xy[j] & 0xFFFFu] = x[j];
+        for (int r = 1; r < tw.copies; ++r) tw.Xs[tw.xmore[((r - 1) * RV + j) * 32 + tw.lane]] = x[j];
+    }
     __syncwarp();
+    const char* xb = reinterpret_cast<const char*>(tw.Xs);
+    double* yp = tw.Ys + tw.lane;
     double acc = 0.0;
-    for (int t0 = 0; t0 < S8; t0 += 8) {
-        uint32_t w[8], v[16];
-        tm_ld_x8(wcol + t0, w);
-        tm_ld_x16(vcol + 2 * t0, v);
+    for (int t0 = 0; t0 < tw.S; t0 += 4) {
+        uint32_t w[2], v[8];
+        tm_ld_x2(tw.wcol + (t0 >> 1), w);
+        tm_ld_x8(tw.vcol + 2 * t0, v);
         tm_wait_ld();
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const double a = __hiloint2double(static_cast<int>(v[2 * u + 1]), static_cast<int>(v[2 * u]));
-            const double xv = c.Xs[w[u] & kColMask];
-            acc = dadd(acc, dmul(a, xv));
-            if (w[u] & kEndBit) {
-                c.Ys[(w[u] >> kColBits) & kColMask] = acc;
-                acc = 0.0;
-            }
-        }
+        tmem_steps4(xb, w, v, acc, yp);
     }
     __syncwarp();
 #pragma unroll
-    for (int j = 0; j < RV; ++j) y[j] = c.valid(j) ? c.Ys[c.row(j)] : 0.0;
+    for (int j = 0; j < RV; ++j) y[j] = tw.Ys[tw.xy[j] >> 16];
+}
+
+// Slot values of one reduction (team_reduce's contract: rows >= n are +0.0,
+// which holds here by the zero invariant).
+template <int R, int RV>
+__device__ __forceinline__ void tmem_reduce(const Ctx<1, R, RV>& cc, const double (&q)[1][RV], double (&o)[1]) {
+    Ctx<1, R, RV> c = cc;
+    team_reduce<1>(c, q, o);
 }
 
 template <int R, int RV>
-__device__ __forceinline__ double tmem_fresh_rms(const Ctx<1, R, RV>& cc, uint32_t wcol, uint32_t vcol, int S8,
+__device__ __forceinline__ double tmem_fresh_rms(const Ctx<1, R, RV>& c, const TmemWarp<RV>& tw,
                                                  const double (&x)[RV], const double* bsrc) {
-    Ctx<1, R, RV> c = cc;
     double ax[RV];
-    tmem_spmv(c, wcol, vcol, S8, x, ax);
+    tmem_spmv(tw, x, ax);
     double sq[1][RV];
 #pragma unroll
     for (int j = 0; j < RV; ++j) {
@@ -117,20 +175,24 @@ __device__ __forceinline__ double tmem_fresh_rms(const Ctx<1, R, RV>& cc, uint32
         sq[0][j] = dmul(ri, ri);
     }
     double out[1];
-    team_reduce<1>(c, sq, out);
+    tmem_reduce(c, sq, out);
     return __dsqrt_rn(ddiv(out[0], static_cast<double>(c.n)));
 }
 
-template <int R, int RV>
-__global__ void __launch_bounds__(512, 1) block_cells_tmem_kernel(const TmemParams p) {
+template <int R, int RV, int NT>
+__global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t s_taddr;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int quarter = warp % 4, slot = warp / 4;
-    int32_t* s_vidx = reinterpret_cast<int32_t*>(smem);                         // S8*32
-    double* s_vec = reinterpret_cast<double*>(smem + sizeof(int32_t) * p.S8 * 32);  // per warp: X | Y
+    int32_t* s_vidx = reinterpret_cast<int32_t*>(smem);  // S*32
+    uint16_t* s_xmore = reinterpret_cast<uint16_t*>(smem + sizeof(int32_t) * p.S * 32);
+    const int xmore_n = (p.copies - 1) * RV * 32;
+    const int xmore_bytes = (2 * xmore_n + 15) & ~15;
+    double* s_vec = reinterpret_cast<double*>(smem + sizeof(int32_t) * p.S * 32 + xmore_bytes);
 
-    for (int i = threadIdx.x; i < p.S8 * 32; i += blockDim.x) s_vidx[i] = i < p.S * 32 ? p.vidx[i] : 0;
+    for (int i = threadIdx.x; i < p.S * 32; i += blockDim.x) s_vidx[i] = p.vidx[i];
+    for (int i = threadIdx.x; i < xmore_n; i += blockDim.x) s_xmore[i] = p.lane_xmore[i];
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          static_cast<uint32_t>(__cvta_generic_to_shared(&s_taddr))),
@@ -141,15 +203,15 @@ __global__ void __launch_bounds__(512, 1) block_cells_tmem_kernel(const TmemPara
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t lane_base = s_taddr + (static_cast<uint32_t>(32 * quarter) << 16);
-    const uint32_t wcol = lane_base;                                        // words: columns [0, S8)
-    const uint32_t vcol = lane_base + p.S8 + 2u * p.S8 * static_cast<uint32_t>(slot);
-    // words into TMEM, once per quarter (schedule is the same for every cell)
-    if (slot == 0) {
-        for (int t0 = 0; t0 < p.S8; t0 += 8) {
-            uint32_t w[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) w[u] = (t0 + u < p.S) ? p.words[(t0 + u) * 32 + lane] : 0u;
-            tm_st_x8(wcol + t0, w);
+    TmemWarp<RV> tw;
+    tw.wcol = lane_base;  // words: columns [0, S/2)
+    tw.vcol = lane_base + p.S / 2 + 2u * p.S * static_cast<uint32_t>(slot);
+    if (slot == 0) {  // words into TMEM once per lane quarter (same for every group)
+        for (int t0 = 0; t0 < p.S; t0 += 4) {
+            uint32_t w[2];
+            w[0] = p.words[t0 * 32 + lane] | (static_cast<uint32_t>(p.words[(t0 + 1) * 32 + lane]) << 16);
+            w[1] = p.words[(t0 + 2) * 32 + lane] | (static_cast<uint32_t>(p.words[(t0 + 3) * 32 + lane]) << 16);
+            tm_st_x2(tw.wcol + (t0 >> 1), w);
         }
         tm_wait_st();
     }
@@ -165,11 +227,18 @@ __global__ void __launch_bounds__(512, 1) block_cells_tmem_kernel(const TmemPara
     c.tm.lane = lane;
     c.n = p.n;
     c.P = p.P;
-    c.Xs = s_vec + static_cast<size_t>(warp) * (p.xslots + ((p.n + 31) & ~31));
-    c.Ys = c.Xs + p.xslots;
+    tw.Xs = s_vec + static_cast<size_t>(warp) * (p.xslots + p.yslots);
+    tw.Ys = tw.Xs + p.xslots;
+    tw.xmore = s_xmore;
+    tw.copies = p.copies;
+    tw.lane = lane;
+    tw.S = p.S;
 #pragma unroll
-    for (int j = 0; j < RV; ++j) c.xa[j] = c.valid(j) ? p.xpos[c.row(j)] : 0;
+    for (int j = 0; j < RV; ++j) tw.xy[j] = p.lane_xy[j * 32 + lane];
+    for (int i = lane; i < p.xslots + p.yslots; i += 32) tw.Xs[i] = 0.0;  // zero slots stay +0.0
+    __syncwarp();
     const double nd = static_cast<double>(p.n);
+    const double smax = p.sigma_max;
 
     while (active) {
         unsigned int gv = 0;
@@ -180,18 +249,18 @@ __global__ void __launch_bounds__(512, 1) block_cells_tmem_kernel(const TmemPara
         const double* src = p.values + cell0 * p.nnz;
         const double* bsrc = p.rhs + cell0 * p.species;
 
-        // stage this cell's values into TMEM in schedule order (once per solve)
-        for (int t0 = 0; t0 < p.S8; t0 += 4) {
+        // stage this group's values into TMEM in schedule order (once per solve)
+        for (int t0 = 0; t0 < p.S; t0 += 4) {
             uint32_t v[8];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const double a = __ldg(src + s_vidx[(t0 + u) * 32 + lane]);
+                const int vi = s_vidx[(t0 + u) * 32 + lane];
+                const double a = vi >= 0 ? __ldg(src + vi) : 0.0;
                 v[2 * u] = static_cast<uint32_t>(__double2loint(a));
                 v[2 * u + 1] = static_cast<uint32_t>(__double2hiint(a));
             }
-            tm_st_x8(vcol + 2 * t0, v);
+            tm_st_x8(tw.vcol + 2 * t0, v);
         }
-        for (int i = lane; i < p.n; i += 32) c.Ys[i] = 0.0;  // empty rows read +0.0
         tm_wait_st();
         __syncwarp();
 
@@ -199,49 +268,45 @@ __global__ void __launch_bounds__(512, 1) block_cells_tmem_kernel(const TmemPara
 #pragma unroll
         for (int j = 0; j < RV; ++j) {
             x[j] = 0.0;
-            double d = 0.0;
-            if (c.valid(j)) {
-                const int di = p.didx[c.row(j)];
-                d = di >= 0 ? __ldg(src + di) : 0.0;
-                dinv[j] = d != 0.0 ? ddiv(1.0, d) : 1.0;
-            } else {
-                dinv[j] = 0.0;
-            }
+            const int di = c.valid(j) ? p.didx[c.row(j)] : -1;
+            const double d = di >= 0 ? __ldg(src + di) : 0.0;
+            dinv[j] = c.valid(j) ? (d != 0.0 ? ddiv(1.0, d) : 1.0) : 0.0;
         }
-        int64_t iters = 0;
+        int iters = 0;
         bool conv = false, brk = false;
         double fres = 0.0;
         double r[RV], rh[RV], pv[RV], v[RV];
         {
             double ax[RV];
-            tmem_spmv(c, wcol, vcol, p.S8, x, ax);
+            tmem_spmv(tw, x, ax);
 #pragma unroll
             for (int j = 0; j < RV; ++j) {
                 const double bj = c.valid(j) ? __ldcs(bsrc + c.row(j)) : 0.0;
-                r[j] = c.valid(j) ? dadd(bj, -ax[j]) : 0.0;  // 1*b + (-1)*Ax
+                r[j] = dadd(bj, -ax[j]);  // 1*b + (-1)*Ax; rows >= n: 0 + -0 = +0
                 rh[j] = r[j];
                 pv[j] = 0.0;
                 v[j] = 0.0;
             }
         }
-        double red2[2];
+        double sigma, rho_next;
         {
-            double q[2][RV];
+            double q[2][RV], o[2];
 #pragma unroll
             for (int j = 0; j < RV; ++j) {
                 q[0][j] = dmul(r[j], r[j]);
                 q[1][j] = dmul(rh[j], r[j]);
             }
-            team_reduce<2>(c, q, red2);
+            team_reduce<2>(c, q, o);
+            sigma = o[0];
+            rho_next = o[1];
         }
-        if (__dsqrt_rn(ddiv(red2[0], nd)) <= p.tol) {
-            fres = tmem_fresh_rms(c, wcol, vcol, p.S8, x, bsrc);
+        if (sigma <= smax) {
+            fres = tmem_fresh_rms(c, tw, x, bsrc);
             conv = fres <= p.tol;
         }
         if (!conv) {
             double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
-            double rho_next = red2[1];
-            for (int64_t it = 1; it <= p.max_iter; ++it) {
+            for (int it = 1; it <= p.max_iter; ++it) {
                 const double rho = rho_next;
                 if (scalar_breaks(rho)) { brk = true; break; }
                 const double beta = dmul(ddiv(rho, rho_prev), ddiv(alpha, omega));
@@ -251,13 +316,13 @@ __global__ void __launch_bounds__(512, 1) block_cells_tmem_kernel(const TmemPara
                     pv[j] = dadd(r[j], dmul(beta, dsub(pv[j], dmul(omega, v[j]))));
                     y[j] = dmul(dinv[j], pv[j]);
                 }
-                tmem_spmv(c, wcol, vcol, p.S8, y, v);
+                tmem_spmv(tw, y, v);
                 double den;
                 {
                     double q[1][RV], o[1];
 #pragma unroll
                     for (int j = 0; j < RV; ++j) q[0][j] = dmul(rh[j], v[j]);
-                    team_reduce<1>(c, q, o);
+                    tmem_reduce(c, q, o);
                     den = o[0];
                 }
                 if (scalar_breaks(den)) { brk = true; break; }
@@ -265,12 +330,12 @@ __global__ void __launch_bounds__(512, 1) block_cells_tmem_kernel(const TmemPara
                 double z[RV];
 #pragma unroll
                 for (int j = 0; j < RV; ++j) {
-                    r[j] = dsub(r[j], dmul(alpha, v[j]));          // r now holds s
+                    r[j] = dsub(r[j], dmul(alpha, v[j]));                 // r now holds s
                     z[j] = dmul(dinv[j], r[j]);
                     x[j] = dadd(x[j], dmul(alpha, dmul(dinv[j], pv[j])));  // y = dinv*p recomputed
                 }
                 double t[RV];
-                tmem_spmv(c, wcol, vcol, p.S8, z, t);
+                tmem_spmv(tw, z, t);
                 double tt, ts;
                 {
                     double q[2][RV], o[2];
@@ -292,7 +357,6 @@ __global__ void __launch_bounds__(512, 1) block_cells_tmem_kernel(const TmemPara
                 }
                 rho_prev = rho;
                 iters = it;
-                double sigma;
                 {
                     double q[2][RV], o[2];
 #pragma unroll
@@ -305,8 +369,8 @@ __global__ void __launch_bounds__(512, 1) block_cells_tmem_kernel(const TmemPara
                     rho_next = o[1];
                 }
                 if (!isfinite(sigma)) { brk = true; break; }
-                if (__dsqrt_rn(ddiv(sigma, nd)) <= p.tol) {
-                    const double f = tmem_fresh_rms(c, wcol, vcol, p.S8, x, bsrc);
+                if (sigma <= smax) {
+                    const double f = tmem_fresh_rms(c, tw, x, bsrc);
                     if (f <= p.tol) {
                         fres = f;
                         conv = true;
@@ -316,7 +380,7 @@ __global__ void __launch_bounds__(512, 1) block_cells_tmem_kernel(const TmemPara
                 if (scalar_breaks(omega)) { brk = true; break; }
             }
             if (!conv) {
-                fres = tmem_fresh_rms(c, wcol, vcol, p.S8, x, bsrc);
+                fres = tmem_fresh_rms(c, tw, x, bsrc);
                 conv = !brk && fres <= p.tol;
             }
         }
@@ -326,7 +390,7 @@ __global__ void __launch_bounds__(512, 1) block_cells_tmem_kernel(const TmemPara
             if (c.valid(j)) xdst[c.row(j)] = x[j];
         if (lane == 0) {
             const int64_t g = p.group_offset + gl;
-            p.g_iters[g] = static_cast<int32_t>(iters);
+            p.g_iters[g] = iters;
             p.g_rms[g] = fres;
             p.g_flags[g] = static_cast<uint8_t>((conv ? 1 : 0) | (brk ? 2 : 0));
         }

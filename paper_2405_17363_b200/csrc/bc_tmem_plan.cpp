@@ -1,0 +1,428 @@
+// bc_tmem_plan.cpp -- schedule of the Tensor-Memory kernel (bc_tmem.cuh).
+//
+// The kernel's SpMV cost is shared-memory wavefronts (ncu: the LSU data pipe
+// is the bound).  Per SpMV a warp issues, besides the TMEM reads:
+//   * one LDS.64 gather per step          -- wavefronts = sum over the two
+//     half-warps of the largest number of distinct 8-byte slots that fall in
+//     one of the 16 bank pairs (measured exactly, tools/bank_probe.py);
+//   * one STS.64 per odd step with row ends -- lane-major Y[k*32+L] makes each
+//     half-warp's stores conflict-free (1 wavefront per half with an end);
+//   * R*RV publishes of x into the gather vector(s) and RV reads of Y.
+// The gather vector is kept in R independent copies; every access picks the
+// copy whose bank is free (an exact small b-matching per half-warp).  A
+// simulated annealing over the copies' slot placements and over which lane
+// runs which (padded) row, in which order, minimises the total.  Row entries
+// keep their CSR order and rows their values, so this changes speed only.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <numeric>
+#include <stdexcept>
+
+#include "bc_plan.hpp"
+
+namespace bc {
+
+namespace {
+
+constexpr int kLanes = 32;
+
+struct TmOpt {
+    int S = 0, ncol = 0, nrow = 0, R = 1, NS = 16;
+    const std::vector<int>* seg_len;
+    const std::vector<std::vector<int>>* seg_cols;
+    const std::vector<int>* seg_row;
+    std::vector<std::vector<int>> lane_segs;
+    std::vector<int> pos;    // [r * ncol + c] slot within copy r
+    std::vector<int> owner;  // [r * NS + slot] -> column, -1 free
+    std::vector<int> col_at; // [t * 32 + L] column read, -1 = idle tail
+    std::vector<uint8_t> end_at;
+    std::vector<int> row_lane;  // row -> lane computing it
+    std::vector<int> load;
+    std::vector<int> gcost;  // [t * 2 + h]
+    int gsum = 0, pub = 0, yrd = 0, yst = 0;
+
+    int bank(int r, int c) const { return pos[r * ncol + c] & 15; }
+
+    // min over copy choices of the max bank load of distinct columns cols[0..m)
+    int match_cost(const int* cols, int m, int* choice) const {
+        if (m == 0) return 0;
+        for (int cap = (m + 15) / 16; cap <= m; ++cap) {
+            int load_b[16] = {0};
+            int assign[16];
+            for (int i = 0; i < m; ++i) assign[i] = -1;
+            bool ok = true;
+            for (int i = 0; i < m && ok; ++i) {
+                bool vis[16] = {false};
+                ok = augment(i, cols, m, cap, load_b, assign, vis);
+            }
+            if (ok) {
+                if (choice)
+                    for (int i = 0; i < m; ++i) {
+                        choice[i] = 0;
+                        for (int r = 0; r < R; ++r)
+                            if (bank(r, cols[i]) == assign[i]) {
+                                choice[i] = r;
+                                break;
+                            }
+                    }
+                return cap;
+            }
+        }
+        return m;
+    }
+    bool augment(int i, const int* cols, int m, int cap, int* load_b, int* assign, bool* vis) const {
+        for (int r = 0; r < R; ++r) {
+            const int b = bank(r, cols[i]);
+            if (vis[b]) continue;
+            vis[b] = true;
+            if (load_b[b] < cap) {
+                load_b[b]++;
+                assign[i] = b;
+                return true;
+            }
+            for (int i2 = 0; i2 < m; ++i2)
+                if (assign[i2] == b && augment(i2, cols, m, cap, load_b, assign, vis)) {
+                    assign[i] = b;
+                    return true;
+                }
+        }
+        return false;
+    }
+    int distinct(int t, int h, int* cols) const {
+        int m = 0;
+        for (int L = 16 * h; L < 16 * h + 16; ++L) {
+            const int c = col_at[t * kLanes + L];
+            if (c < 0) continue;
+            bool dup = false;
+            for (int q = 0; q < m; ++q) dup |= cols[q] == c;
+            if (!dup) cols[m++] = c;
+        }
+        return m;
+    }
+    int group_cost(int t, int h) const {
+        int cols[16];
+        const int m = distinct(t, h, cols);
+        return match_cost(cols, m, nullptr);
+    }
+    void lay_lane(int L) {
+        for (int t = 0; t < S; ++t) {
+            col_at[t * kLanes + L] = -1;
+            end_at[t * kLanes + L] = 0;
+        }
+        int t = 0;
+        for (int sg : lane_segs[L]) {
+            const auto& cols = (*seg_cols)[sg];
+            for (size_t q = 0; q < cols.size(); ++q, ++t) col_at[t * kLanes + L] = cols[q];
+            end_at[(t - 1) * kLanes + L] = 1;
+            row_lane[(*seg_row)[sg]] = L;
+        }
+        load[L] = t;
+    }
+    int publish_cost() const {  // R*RV STS.64 by the owner lanes (rows 32j+L)
+        int tot = 0;
+        for (int r = 0; r < R; ++r)
+            for (int j = 0; j * 32 < nrow; ++j)
+                for (int h = 0; h < 2; ++h) {
+                    int cnt[16] = {0};
+                    for (int q = 0; q < 16; ++q) {
+                        const int row = 32 * j + 16 * h + q;
+                        if (row < nrow) cnt[bank(r, row)]++;
+                    }
+                    tot += *std::max_element(cnt, cnt + 16);
+                }
+        return tot;
+    }
+    int yread_cost() const {  // RV LDS.64 of Y[k*32+lane(row)]: bank = lane(row) & 15
+        int tot = 0;
+        for (int j = 0; j * 32 < nrow; ++j)
+            for (int h = 0; h < 2; ++h) {
+                int cnt[16] = {0};
+                for (int q = 0; q < 16; ++q) {
+                    const int row = 32 * j + 16 * h + q;
+                    if (row < nrow && row_lane[row] >= 0) cnt[row_lane[row] & 15]++;
+                }
+                tot += *std::max_element(cnt, cnt + 16);
+            }
+        return tot;
+    }
+    int ystore_cost() const {
+        int tot = 0;
+        for (int t = 1; t < S; t += 2)
+            for (int h = 0; h < 2; ++h) {
+                bool any = false;
+                for (int L = 16 * h; L < 16 * h + 16; ++L) any |= end_at[t * kLanes + L] != 0;
+                tot += any;
+            }
+        return tot;
+    }
+    int total() const { return gsum + pub + yrd + yst; }
+    void full_eval() {
+        gsum = 0;
+        for (int t = 0; t < S; ++t)
+            for (int h = 0; h < 2; ++h) gsum += (gcost[t * 2 + h] = group_cost(t, h));
+        pub = publish_cost();
+        yrd = yread_cost();
+        yst = ystore_cost();
+    }
+    // re-evaluate the gather groups of the halves holding lanes A and B
+    int regather_lanes(int A, int B) {
+        int g = gsum;
+        const int ha = A / 16, hb = B / 16;
+        for (int t = 0; t < S; ++t) {
+            const int id = t * 2 + ha;
+            const int c = group_cost(t, ha);
+            g += c - gcost[id];
+            gcost[id] = c;
+            if (hb != ha) {
+                const int id2 = t * 2 + hb;
+                const int c2 = group_cost(t, hb);
+                g += c2 - gcost[id2];
+                gcost[id2] = c2;
+            }
+        }
+        return g;
+    }
+};
+
+}  // namespace
+
+TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
+    if (const char* e = std::getenv("BC_SCHED_OPT")) optimize = optimize && std::atoi(e) != 0;
+    int copies = 2;
+    if (const char* e = std::getenv("BC_GATHER_COPIES")) copies = std::max(1, std::min(4, std::atoi(e)));
+    if (!optimize) copies = 1;
+    constexpr int d = 2;
+    const int s = pat.species, nnz = pat.nnz, n = k * s;
+    const int zero_col = n;  // pseudo-row whose slots always hold +0.0
+    // rows as segments padded to a multiple of d (csr.cpp:90-101 order kept)
+    std::vector<int> seg_row, seg_len;
+    std::vector<std::vector<int>> seg_cols, seg_vals;
+    for (int c = 0; c < k; ++c)
+        for (int r = 0; r < s; ++r) {
+            if (pat.row_ptr[r + 1] == pat.row_ptr[r]) continue;
+            std::vector<int> cols, vals;
+            for (int e = pat.row_ptr[r]; e < pat.row_ptr[r + 1]; ++e) {
+                cols.push_back(c * s + pat.col_idx[e]);
+                vals.push_back(c * nnz + e);
+            }
+            while (cols.size() % d) {
+                cols.push_back(zero_col);
+                vals.push_back(-1);
+            }
+            seg_row.push_back(c * s + r);
+            seg_len.push_back(static_cast<int>(cols.size()));
+            seg_cols.push_back(std::move(cols));
+            seg_vals.push_back(std::move(vals));
+        }
+    TmOpt o;
+    o.seg_len = &seg_len;
+    o.seg_cols = &seg_cols;
+    o.seg_row = &seg_row;
+    o.ncol = n + 1;
+    o.nrow = n;
+    o.R = copies;
+    o.lane_segs.assign(kLanes, {});
+    o.load.assign(kLanes, 0);
+    {  // longest-processing-time start
+        std::vector<int> order(seg_row.size());
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return seg_len[a] > seg_len[b]; });
+        for (int idx : order) {
+            int best = 0;
+            for (int L = 1; L < kLanes; ++L)
+                if (o.load[L] < o.load[best]) best = L;
+            o.load[best] += seg_len[idx];
+            o.lane_segs[best].push_back(idx);
+        }
+    }
+    const int S0 = std::max(4, *std::max_element(o.load.begin(), o.load.end()));
+    o.S = (S0 + 3) & ~3;
+    o.NS = optimize ? ((o.ncol + o.ncol / 4 + 15) / 16) * 16 : ((o.ncol + 15) / 16) * 16;
+    o.pos.resize(static_cast<size_t>(o.R) * o.ncol);
+    o.owner.assign(static_cast<size_t>(o.R) * o.NS, -1);
+    uint64_t rng = 0x243F6A8885A308D3ull ^ static_cast<uint64_t>(n * 977 + nnz);
+    auto rnd = [&]() {
+        rng ^= rng << 13;
+        rng ^= rng >> 7;
+        rng ^= rng << 17;
+        return rng;
+    };
+    for (int r = 0; r < o.R; ++r) {
+        std::vector<int> perm(o.NS);
+        std::iota(perm.begin(), perm.end(), 0);
+        if (r > 0)
+            for (int i = o.NS - 1; i > 0; --i) std::swap(perm[i], perm[rnd() % (i + 1)]);
+        for (int c = 0; c < o.ncol; ++c) {
+            o.pos[r * o.ncol + c] = perm[c];
+            o.owner[r * o.NS + perm[c]] = c;
+        }
+    }
+    o.col_at.assign(static_cast<size_t>(o.S) * kLanes, -1);
+    o.end_at.assign(static_cast<size_t>(o.S) * kLanes, 0);
+    o.row_lane.assign(n, -1);
+    o.gcost.assign(static_cast<size_t>(o.S) * 2, 0);
+    for (int L = 0; L < kLanes; ++L) o.lay_lane(L);
+    o.full_eval();
+
+    if (optimize) {
+        auto urand = [&]() { return static_cast<double>(rnd() >> 11) * 0x1.0p-53; };
+        const long iters = std::max<long>(20000, std::min<long>(200000, 40000000L / (o.S * kLanes)));
+        double T = 1.0;
+        const double cool = std::pow(0.01 / T, 1.0 / static_cast<double>(iters));
+        int cur = o.total(), best = cur;
+        TmOpt best_o = o;
+        std::vector<int> touched;
+        for (long it = 0; it < iters; ++it, T *= cool) {
+            const int kind = static_cast<int>(rnd() % 4);
+            if (kind <= 1) {  // move one column's slot within one copy
+                const int r = static_cast<int>(rnd() % o.R);
+                const int c = static_cast<int>(rnd() % o.ncol);
+                const int slot = static_cast<int>(rnd() % o.NS);
+                const int other = o.owner[r * o.NS + slot];
+                if (other == c) continue;
+                const int old = o.pos[r * o.ncol + c];
+                auto apply = [&](int a_slot, int b_slot) {
+                    o.pos[r * o.ncol + c] = a_slot;
+                    o.owner[r * o.NS + a_slot] = c;
+                    o.owner[r * o.NS + b_slot] = other;
+                    if (other >= 0) o.pos[r * o.ncol + other] = b_slot;
+                };
+                apply(slot, old);
+                touched.clear();
+                for (size_t q = 0; q < o.col_at.size(); ++q)
+                    if (o.col_at[q] == c || (other >= 0 && o.col_at[q] == other))
+                        touched.push_back(static_cast<int>((q / kLanes) * 2 + (q % kLanes) / 16));
+                std::sort(touched.begin(), touched.end());
+                touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
+                int g = o.gsum;
+                std::vector<int> nc(touched.size());
+                for (size_t q = 0; q < touched.size(); ++q) {
+                    nc[q] = o.group_cost(touched[q] / 2, touched[q] % 2);
+                    g += nc[q] - o.gcost[touched[q]];
+                }
+                const int npub = o.publish_cost();
+                const int nt = g + npub + o.yrd + o.yst;
+                if (nt - cur <= 0 || urand() < std::exp(-(nt - cur) / T)) {
+                    for (size_t q = 0; q < touched.size(); ++q) o.gcost[touched[q]] = nc[q];
+                    o.gsum = g;
+                    o.pub = npub;
+                    cur = nt;
+                } else {
+                    apply(old, slot);
+                }
+            } else {
+                // segment moves: reorder within a lane, move or exchange between lanes
+                const int A = static_cast<int>(rnd() % kLanes);
+                int B = kind == 2 ? A : static_cast<int>(rnd() % kLanes);
+                if (o.lane_segs[A].empty()) continue;
+                const auto saveA = o.lane_segs[A], saveB = o.lane_segs[B];
+                if (kind == 2) {
+                    const int m = static_cast<int>(o.lane_segs[A].size());
+                    if (m < 2) continue;
+                    const int i = static_cast<int>(rnd() % m), j = static_cast<int>(rnd() % m);
+                    if (i == j) continue;
+                    std::swap(o.lane_segs[A][i], o.lane_segs[A][j]);
+                } else {
+                    if (A == B) continue;
+                    const int ia = static_cast<int>(rnd() % o.lane_segs[A].size());
+                    const int sa = o.lane_segs[A][ia];
+                    if (o.lane_segs[B].empty() || (rnd() & 1)) {
+                        if (o.load[B] + seg_len[sa] > o.S) continue;
+                        const int ib = static_cast<int>(rnd() % (o.lane_segs[B].size() + 1));
+                        o.lane_segs[A].erase(o.lane_segs[A].begin() + ia);
+                        o.lane_segs[B].insert(o.lane_segs[B].begin() + ib, sa);
+                    } else {
+                        const int ib = static_cast<int>(rnd() % o.lane_segs[B].size());
+                        const int sb = o.lane_segs[B][ib];
+                        if (o.load[A] - seg_len[sa] + seg_len[sb] > o.S ||
+                            o.load[B] - seg_len[sb] + seg_len[sa] > o.S)
+                            continue;
+                        std::swap(o.lane_segs[A][ia], o.lane_segs[B][ib]);
+                    }
+                }
+                const int old_g = o.gsum, old_y = o.yrd, old_s = o.yst;
+                const auto old_gc = o.gcost;
+                o.lay_lane(A);
+                if (B != A) o.lay_lane(B);
+                o.gsum = o.regather_lanes(A, B);
+                o.yrd = o.yread_cost();
+                o.yst = o.ystore_cost();
+                const int nt = o.total();
+                if (nt - cur <= 0 || urand() < std::exp(-(nt - cur) / T)) {
+                    cur = nt;
+                } else {
+                    o.lane_segs[A] = saveA;
+                    o.lane_segs[B] = saveB;
+                    o.lay_lane(A);
+                    if (B != A) o.lay_lane(B);
+                    o.gsum = old_g;
+                    o.gcost = old_gc;
+                    o.yrd = old_y;
+                    o.yst = old_s;
+                }
+            }
+            if (cur < best) {
+                best = cur;
+                best_o = o;
+            }
+        }
+        o = best_o;
+    }
+
+    // emission
+    TmemSchedule ts;
+    ts.steps = o.S;
+    ts.copies = o.R;
+    ts.xslots = o.R * o.NS;
+    ts.zero_slot = o.pos[zero_col];
+    ts.xpos.assign(static_cast<size_t>(o.R) * n, 0);
+    for (int r = 0; r < o.R; ++r)
+        for (int i = 0; i < n; ++i) ts.xpos[static_cast<size_t>(r) * n + i] = r * o.NS + o.pos[r * o.ncol + i];
+    ts.words.assign(static_cast<size_t>(o.S) * kLanes, 0);
+    ts.vidx.assign(static_cast<size_t>(o.S) * kLanes, -1);
+    ts.yslot.assign(n, -1);
+    std::vector<int> vals_at(static_cast<size_t>(o.S) * kLanes, -1);
+    int kmax = 0;
+    for (int L = 0; L < kLanes; ++L) {
+        int t = 0, kk = 0;
+        for (int sg : o.lane_segs[L]) {
+            for (size_t q = 0; q < seg_cols[sg].size(); ++q, ++t) vals_at[t * kLanes + L] = seg_vals[sg][q];
+            ts.yslot[seg_row[sg]] = kk * kLanes + L;
+            ++kk;
+        }
+        kmax = std::max(kmax, kk);
+    }
+    ts.yslots = std::max(1, kmax) * kLanes;
+    for (int& y : ts.yslot)
+        if (y < 0) y = ts.yslots;  // empty rows read the zero slot after the last row slot
+    int cost = 0;
+    for (int t = 0; t < o.S; ++t)
+        for (int h = 0; h < 2; ++h) {
+            int cols[16], choice[16];
+            const int m = o.distinct(t, h, cols);
+            cost += o.match_cost(cols, m, choice);
+            for (int L = 16 * h; L < 16 * h + 16; ++L) {
+                const int id = t * kLanes + L;
+                int c = o.col_at[id], r = 0;
+                if (c < 0) {  // idle tail: broadcast a column the half already reads
+                    c = m > 0 ? cols[0] : zero_col;
+                    r = m > 0 ? choice[0] : 0;
+                } else {
+                    for (int q = 0; q < m; ++q)
+                        if (cols[q] == c) r = choice[q];
+                }
+                const int slot = r * o.NS + o.pos[r * o.ncol + c];
+                uint16_t w = static_cast<uint16_t>(slot * 8);
+                if (o.end_at[id]) w |= 0x8000u;
+                ts.words[id] = w;
+                ts.vidx[id] = vals_at[id];
+            }
+        }
+    ts.conflict_cost = cost;
+    ts.model_total = o.total();
+    if (ts.xslots * 8 > 0x7FFF) throw std::invalid_argument("TMEM schedule: gather vector too large");
+    return ts;
+}
+
+}  // namespace bc

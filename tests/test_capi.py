@@ -223,3 +223,79 @@ def test_reduction_geometry_reproduces_tree(n):
         want = of.orc().orc_tree_reduce_in_place(of.ptr(slots), P)
         got = emulate_team_reduce(v, n, P, W, R)
         assert of.bits(got) == of.bits(want)
+
+
+def export_tmem_schedule(rp, ci, k):
+    species = len(rp) - 1
+    rp = np.ascontiguousarray(rp, np.int32)
+    ci = np.ascontiguousarray(ci, np.int32)
+    info = np.zeros(7, np.int32)
+    lib = _native.b200()
+    assert lib.bc_tmem_schedule_export(species, of.ptr(rp), of.ptr(ci), k, of.ptr(info), None, None, None,
+                                       None) == 0
+    S, copies = int(info[0]), int(info[5])
+    words = np.zeros(S * 32, np.uint16)
+    vidx = np.zeros(S * 32, np.int32)
+    xpos = np.zeros(copies * k * species, np.int32)
+    yslot = np.zeros(k * species, np.int32)
+    assert lib.bc_tmem_schedule_export(species, of.ptr(rp), of.ptr(ci), k, of.ptr(info), of.ptr(words),
+                                       of.ptr(vidx), of.ptr(xpos), of.ptr(yslot)) == 0
+    return dict(S=S, xslots=int(info[1]), zero_slot=int(info[2]), yslots=int(info[3]), cost=int(info[4]),
+                copies=copies, model=int(info[6]), words=words, vidx=vidx, xpos=xpos.reshape(copies, -1),
+                yslot=yslot)
+
+
+def emulate_tmem_spmv(sc, vals, x):
+    """tmem_spmv() of bc_tmem.cuh in exact double arithmetic: zero-initialised
+    X|Y, publish x, lanes walk 16-bit words (byte offset | end << 15), row
+    ends only on odd steps, lane L's k-th row -> Y[k*32+L]."""
+    S = sc["S"]
+    X = np.zeros(sc["xslots"] + 1)
+    for xp in sc["xpos"]:  # every copy of the gather vector
+        X[xp] = x
+    Y = np.zeros(sc["yslots"] + 32)
+    for L in range(32):
+        acc, k = 0.0, 0
+        for t in range(S):
+            w = int(sc["words"][t * 32 + L])
+            vi = int(sc["vidx"][t * 32 + L])
+            a = float(vals[vi]) if vi >= 0 else 0.0
+            acc = acc + a * float(X[(w & 0x7FFF) // 8])
+            if (t & 1) and (w & 0x8000):
+                Y[k * 32 + L] = acc
+                k += 1
+                acc = 0.0
+            elif w & 0x8000:
+                raise AssertionError("row end on an even step")
+    return Y[sc["yslot"]]
+
+
+@pytest.mark.parametrize("species,k,density,seed", [(9, 1, 0.4, 0), (40, 3, 0.2, 1), (156, 1, 0.0, 2),
+                                                    (100, 2, 0.05, 3), (17, 15, 0.3, 4), (60, 1, 0.02, 5)])
+def test_tmem_schedule_reproduces_spmv_order(species, k, density, seed):
+    rng = np.random.default_rng(seed)
+    if density == 0.0:
+        m = Mechanism(156, 468, 0)
+        rp, ci = m.row_ptr, m.col_idx
+    else:
+        rp, ci, _, _ = random_batch(rng, 1, species, density)
+        if seed == 5:  # empty rows
+            rp = rp.copy()
+            keep = np.ones(len(ci), bool)
+            for r in (3, 7):
+                keep[rp[r]:rp[r + 1]] = False
+            lens = np.diff(rp) * 1
+            lens[[3, 7]] = 0
+            ci = ci[keep]
+            rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    nnz = int(rp[-1])
+    sc = export_tmem_schedule(rp, ci, k)
+    assert sc["S"] % 4 == 0
+    vals = rng.uniform(-1, 1, k * nnz) * 10.0 ** rng.integers(-8, 8, k * nnz)
+    x = rng.uniform(-1, 1, k * species)
+    x[rng.random(k * species) < 0.05] = np.inf  # padding must never touch x (0*inf = NaN)
+    y = emulate_tmem_spmv(sc, vals, x)
+    with np.errstate(invalid="ignore"):
+        np.testing.assert_array_equal(of.bits(y), of.bits(ref_spmv(rp, ci, vals, x, k, species, nnz)))
+    used = sc["vidx"][sc["vidx"] >= 0]
+    assert sorted(used.tolist()) == list(range(k * nnz))
