@@ -16,6 +16,7 @@
 
 #include "bc_block.cuh"
 #include "bc_lu.cuh"
+#include "bc_multi.cuh"
 #include "bc_newton.cuh"
 #include "bc_tmem.cuh"
 #include "bc_plan.hpp"
@@ -101,10 +102,12 @@ struct bc_ctx {
     bool has_pattern = false;
     bc::Pattern pat;
     DevBuf d_rp, d_ci;
+    DevBuf m_trp, m_trow, m_tval, m_diag, m_ranges, m_work, m_part, m_out;  // Multi-cells
+    bool m_ready = false;
     std::map<std::pair<int, int>, bc::GroupPlan> plans;  // (k, with_transpose)
     std::vector<DevBuf> plan_bufs;
     DevBuf values, rhs, x, giters, grms, gflags, counters, lu_scratch, lu_entries, lu_status,
-        f_scratch;
+        f_scratch, lu_rms_scratch;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     int64_t launches = 0;
     std::map<BlockFn, bool> smem_set;
@@ -493,6 +496,156 @@ void plan_groups(const bc_solve_params* prm, int species, double* cpb, int64_t* 
 
 }  // namespace
 
+// ---- Multi-cells (bc_multi.cuh) -----------------------------------------
+
+// Transpose tables (per local column, entries in ascending row order) and the
+// diagonal of one pattern, uploaded into the given buffers.
+void upload_multi_tables(const bc::Pattern& pat, DevBuf* trp, DevBuf* trow, DevBuf* tval, DevBuf* diag) {
+    const int s = pat.species;
+    std::vector<int32_t> cnt(s + 1, 0), tr(pat.nnz), tv(pat.nnz), dg(s);
+    for (int e = 0; e < pat.nnz; ++e) cnt[pat.col_idx[e] + 1]++;
+    for (int j = 0; j < s; ++j) cnt[j + 1] += cnt[j];
+    std::vector<int32_t> next(cnt.begin(), cnt.end() - 1);
+    for (int r = 0; r < s; ++r)
+        for (int e = pat.row_ptr[r]; e < pat.row_ptr[r + 1]; ++e) {
+            const int q = next[pat.col_idx[e]]++;
+            tr[q] = r;
+            tv[q] = e;
+        }
+    for (int r = 0; r < s; ++r) dg[r] = pat.diag[r];
+    auto up = [](DevBuf* b, const std::vector<int32_t>& v) {
+        check_cuda(b->ensure(sizeof(int32_t) * std::max<size_t>(v.size(), 1)), "cudaMalloc(multi)");
+        if (!v.empty())
+            check_cuda(cudaMemcpy(b->p, v.data(), sizeof(int32_t) * v.size(), cudaMemcpyHostToDevice), "H2D multi");
+    };
+    up(trp, cnt);
+    up(trow, tr);
+    up(tval, tv);
+    up(diag, dg);
+}
+
+// Dense LU fallback (bc_lu.cuh) for the listed groups; throws SingularMatrix.
+// g_rms == nullptr: solutions only (the caller computes the residual).
+void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_values, const double* d_rhs,
+            double* d_x, double* g_rms, int s, int nnz, int block_width, cudaStream_t st) {
+    int64_t nmax = 0;
+    for (const auto& e : ents) nmax = std::max<int64_t>(nmax, static_cast<int64_t>(e.kc) * s);
+    if (nmax > bc::kMaxGroupRows) fail(BC_ERR_INVALID_ARGUMENT, "LU fallback group exceeds 2048 rows");
+    const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(ents.size()),
+                                                                 (int64_t(1) << 31) / (nmax * nmax * 8)));
+    check_cuda(ctx->lu_scratch.ensure(sizeof(double) * nmax * nmax * batch), "cudaMalloc(lu)");
+    check_cuda(ctx->lu_entries.ensure(sizeof(bc::LuEntry) * ents.size()), "cudaMalloc");
+    check_cuda(ctx->lu_status.ensure(sizeof(int32_t) * ents.size()), "cudaMalloc");
+    check_cuda(ctx->lu_rms_scratch.ensure(sizeof(double) * (ents.size() + 1)), "cudaMalloc");
+    std::vector<bc::LuEntry> dev_ents = ents;
+    if (!g_rms)  // park the per-group residuals in scratch
+        for (size_t i = 0; i < dev_ents.size(); ++i) dev_ents[i].gout = static_cast<int64_t>(i);
+    check_cuda(cudaMemcpyAsync(ctx->lu_entries.p, dev_ents.data(), sizeof(bc::LuEntry) * dev_ents.size(),
+                               cudaMemcpyHostToDevice, st), "H2D lu entries");
+    const int64_t pmax = bc::padded_len(nmax);
+    const size_t smem = sizeof(int) * ((nmax + 1) & ~1) + sizeof(double) * (nmax + std::max(pmax, nmax));
+    if (smem > 48 * 1024)
+        check_cuda(cudaFuncSetAttribute(bc::lu_fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kMaxDynSmem - 1024), "cudaFuncSetAttribute(lu)");
+    for (size_t b0 = 0; b0 < ents.size(); b0 += batch) {
+        const int cnt = static_cast<int>(std::min<int64_t>(batch, ents.size() - b0));
+        bc::LuParams lp{};
+        lp.values = d_values;
+        lp.rhs = d_rhs;
+        lp.x_out = d_x;
+        lp.g_rms = g_rms ? g_rms : ctx->lu_rms_scratch.as<double>();
+        lp.status = ctx->lu_status.as<int32_t>() + b0;
+        lp.entries = ctx->lu_entries.as<bc::LuEntry>() + b0;
+        lp.row_ptr = ctx->d_rp.as<int32_t>();
+        lp.col_idx = ctx->d_ci.as<int32_t>();
+        lp.scratch = ctx->lu_scratch.as<double>();
+        lp.n_max = nmax;
+        lp.species = s;
+        lp.nnz = nnz;
+        lp.block_width = block_width;
+        bc::lu_fallback_kernel<<<cnt, 256, smem, st>>>(lp);
+        check_cuda(cudaGetLastError(), "lu_fallback_kernel launch");
+        ctx->launches++;
+    }
+    std::vector<int32_t> status(ents.size());
+    check_cuda(cudaMemcpyAsync(status.data(), ctx->lu_status.p, sizeof(int32_t) * ents.size(), cudaMemcpyDeviceToHost,
+                               st), "D2H lu status");
+    check_cuda(cudaStreamSynchronize(st), "lu_fallback_kernel");
+    for (int32_t v : status)
+        if (v) fail(BC_ERR_SINGULAR_MATRIX, "lu_solve: exactly singular matrix");
+}
+
+struct MultiResult {
+    int64_t iters = 0;
+    double rms = 0.0;
+    int32_t flags = 0;
+};
+
+// One cooperative launch of multi_cells_kernel over a global system of
+// `cells` cells of pattern `pat` with the given reduction intervals.
+MultiResult run_multi(bc_ctx* ctx, const bc::Pattern& pat, const int32_t* d_rp, const int32_t* d_ci,
+                      const DevBuf& trp, const DevBuf& trow, const DevBuf& tval, const DevBuf& diag, int64_t cells,
+                      const std::vector<int64_t>& ranges, const double* values, const double* rhs, const double* x0,
+                      double* x, double tol, int64_t max_iter, int algo, int mode, cudaStream_t st) {
+    const int64_t n = cells * pat.species, nb = static_cast<int64_t>(ranges.size() / 2);
+    int64_t max_len = 1;
+    for (int64_t b = 0; b < nb; ++b) max_len = std::max(max_len, ranges[2 * b + 1] - ranges[2 * b]);
+    if (max_len > 4096) fail(BC_ERR_INVALID_ARGUMENT, "reduction interval longer than 4096 rows");
+    check_cuda(ctx->m_ranges.ensure(sizeof(int64_t) * ranges.size()), "cudaMalloc(ranges)");
+    check_cuda(cudaMemcpyAsync(ctx->m_ranges.p, ranges.data(), sizeof(int64_t) * ranges.size(),
+                               cudaMemcpyHostToDevice, st), "H2D ranges");
+    check_cuda(ctx->m_work.ensure(sizeof(double) * 7 * n), "cudaMalloc(multi work)");
+    check_cuda(ctx->m_part.ensure(sizeof(double) * 2 * nb), "cudaMalloc(partials)");
+    check_cuda(ctx->m_out.ensure(64), "cudaMalloc");
+    bc::MultiParams p{};
+    p.values = values;
+    p.rhs = rhs;
+    p.x0 = x0;
+    p.x = x;
+    p.row_ptr = d_rp;
+    p.col_idx = d_ci;
+    p.trow_ptr = trp.as<int32_t>();
+    p.trow = trow.as<int32_t>();
+    p.tval = tval.as<int32_t>();
+    p.diag = diag.as<int32_t>();
+    p.ranges = ctx->m_ranges.as<int64_t>();
+    p.n_blocks = nb;
+    p.n = n;
+    p.species = pat.species;
+    p.nnz = pat.nnz;
+    p.max_len = static_cast<int>(max_len);
+    p.work = ctx->m_work.as<double>();
+    p.partials = ctx->m_part.as<double>();
+    p.tol = tol;
+    p.max_iter = max_iter;
+    p.algo = algo == BC_ALGO_BICG ? bc::kBiCG : bc::kBiCGStab;
+    p.mode = mode;
+    p.out_iters = ctx->m_out.as<int64_t>();
+    p.out_rms = reinterpret_cast<double*>(ctx->m_out.as<char>() + 8);
+    p.out_flags = reinterpret_cast<int32_t*>(ctx->m_out.as<char>() + 16);
+    int P2 = 256;
+    while (P2 < max_len) P2 <<= 1;
+    const size_t smem = sizeof(double) * 2 * P2;
+    check_cuda(cudaFuncSetAttribute(bc::multi_cells_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)), "cudaFuncSetAttribute(multi)");
+    int per_sm = 0;
+    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bc::multi_cells_kernel, 256, smem),
+               "occupancy(multi)");
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(nb, static_cast<int64_t>(per_sm) * ctx->sms));
+    void* args[] = {&p};
+    check_cuda(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bc::multi_cells_kernel), dim3(grid), dim3(256),
+                                           args, smem, st), "multi_cells_kernel cooperative launch");
+    ctx->launches++;
+    MultiResult r;
+    char buf[24];
+    check_cuda(cudaMemcpyAsync(buf, ctx->m_out.p, 24, cudaMemcpyDeviceToHost, st), "D2H multi");
+    check_cuda(cudaStreamSynchronize(st), "multi_cells_kernel");
+    std::memcpy(&r.iters, buf, 8);
+    std::memcpy(&r.rms, buf + 8, 8);
+    std::memcpy(&r.flags, buf + 16, 4);
+    return r;
+}
+
 extern "C" {
 
 int bc_ctx_create(int device, bc_ctx** out) {
@@ -555,6 +708,7 @@ int bc_set_pattern(bc_ctx* ctx, int32_t species, const int32_t* row_ptr, const i
             check_cuda(cudaMemcpy(ctx->d_ci.p, p.col_idx.data(), sizeof(int32_t) * p.col_idx.size(),
                                   cudaMemcpyHostToDevice), "cudaMemcpy");
         ctx->pat = std::move(p);
+        ctx->m_ready = false;
         ctx->has_pattern = true;
         return BC_OK;
     });
@@ -622,7 +776,7 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
         if (prm->max_iter < 1) fail(BC_ERR_INVALID_ARGUMENT, "bicg: max_iter must be >= 1");
         if (prm->algo != BC_ALGO_BICG && prm->algo != BC_ALGO_BICGSTAB_JACOBI)
             fail(BC_ERR_INVALID_ARGUMENT, "unknown algorithm");
-        if (prm->strategy == BC_STRATEGY_MULTI_CELLS || prm->strategy == BC_STRATEGY_THREAD_PER_CELL)
+        if (prm->strategy == BC_STRATEGY_THREAD_PER_CELL)
             fail(BC_ERR_INVALID_ARGUMENT, "strategy not available in this build");
 
         cudaStream_t st = static_cast<cudaStream_t>(prm->stream);
@@ -653,21 +807,49 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
 
         const bool timing = (prm->options & BC_OPT_TIMING) != 0;
         const bool bicg = prm->algo == BC_ALGO_BICG;
-        for (const GroupSpan& sp : spans) {  // host-side planning before the timed region
-            bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);
-            if (!bicg) {
-                ensure_tmem_schedule(ctx, pat, gp);
-                if (gp.has_tm)
-                    for (const TmemCfg& t : kTmemConfigs)
-                        if (t.R == gp.geo.R && t.RV >= gp.geo.RV) {
-                            ensure_tmem_lane_tables(ctx, gp, t.RV);
-                            break;
-                        }
+        const bool multi = prm->strategy == BC_STRATEGY_MULTI_CELLS;
+        const int64_t mtpb = prm->max_threads_per_block > 0 ? prm->max_threads_per_block : 1024;
+        std::vector<int64_t> multi_ranges;
+        if (multi) {  // exec_model.cpp:202-220: one interval per 1024-thread block + host stage
+            spans[0].k = static_cast<int>(prm->cells);
+            if (!ctx->m_ready) {
+                upload_multi_tables(pat, &ctx->m_trp, &ctx->m_trow, &ctx->m_tval, &ctx->m_diag);
+                ctx->m_ready = true;
+            }
+            const int64_t ntot = prm->cells * s;
+            for (int64_t b0 = 0; b0 < ntot; b0 += mtpb) {
+                multi_ranges.push_back(b0);
+                multi_ranges.push_back(std::min(ntot, b0 + mtpb));
+            }
+        } else {
+            for (const GroupSpan& sp : spans) {  // host-side planning before the timed region
+                bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);
+                if (!bicg) {
+                    ensure_tmem_schedule(ctx, pat, gp);
+                    if (gp.has_tm)
+                        for (const TmemCfg& t : kTmemConfigs)
+                            if (t.R == gp.geo.R && t.RV >= gp.geo.RV) {
+                                ensure_tmem_lane_tables(ctx, gp, t.RV);
+                                break;
+                            }
+                }
             }
         }
         if (timing) check_cuda(cudaEventRecord(ctx->e0, st), "cudaEventRecord");
         int slot = 0;
+        if (multi) {
+            const MultiResult mr = run_multi(ctx, pat, ctx->d_rp.as<int32_t>(), ctx->d_ci.as<int32_t>(), ctx->m_trp,
+                                             ctx->m_trow, ctx->m_tval, ctx->m_diag, prm->cells, multi_ranges,
+                                             d_values, d_rhs, nullptr, d_x, prm->tol, prm->max_iter, prm->algo, 0, st);
+            const int32_t it32 = static_cast<int32_t>(mr.iters);
+            const uint8_t f8 = static_cast<uint8_t>(mr.flags);
+            check_cuda(cudaMemcpyAsync(ctx->giters.p, &it32, 4, cudaMemcpyHostToDevice, st), "H2D");
+            check_cuda(cudaMemcpyAsync(ctx->grms.p, &mr.rms, 8, cudaMemcpyHostToDevice, st), "H2D");
+            check_cuda(cudaMemcpyAsync(ctx->gflags.p, &f8, 1, cudaMemcpyHostToDevice, st), "H2D");
+            check_cuda(cudaStreamSynchronize(st), "H2D multi outputs");
+        }
         for (const GroupSpan& sp : spans) {
+            if (multi) break;
             bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);
             unsigned int* counter = ctx->counters.as<unsigned int>() + slot++;
             if (!bicg && launch_tmem(ctx, pat, gp, sp.cell0, sp.gout0, sp.count, d_values, d_rhs, d_x, prm->tol,
@@ -689,48 +871,27 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
             }
         int64_t fallbacks = 0;
         if (!ents.empty()) {
-            int64_t nmax = 0;
-            for (const auto& e : ents) nmax = std::max<int64_t>(nmax, e.kc * s);
-            const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(ents.size()),
-                                                                         (int64_t(1) << 31) / (nmax * nmax * 8)));
-            check_cuda(ctx->lu_scratch.ensure(sizeof(double) * nmax * nmax * batch), "cudaMalloc(lu)");
-            check_cuda(ctx->lu_entries.ensure(sizeof(bc::LuEntry) * ents.size()), "cudaMalloc");
-            check_cuda(ctx->lu_status.ensure(sizeof(int32_t) * ents.size()), "cudaMalloc");
-            check_cuda(cudaMemcpyAsync(ctx->lu_entries.p, ents.data(), sizeof(bc::LuEntry) * ents.size(),
-                                       cudaMemcpyHostToDevice, st), "H2D lu entries");
-            const int64_t pmax = bc::padded_len(nmax);
-            const size_t smem = sizeof(int) * ((nmax + 1) & ~1) + sizeof(double) * (nmax + std::max(pmax, nmax));
-            if (smem > 48 * 1024)
-                check_cuda(cudaFuncSetAttribute(bc::lu_fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                kMaxDynSmem - 1024), "cudaFuncSetAttribute(lu)");
-            for (size_t b0 = 0; b0 < ents.size(); b0 += batch) {
-                const int cnt = static_cast<int>(std::min<int64_t>(batch, ents.size() - b0));
-                bc::LuParams lp{};
-                lp.values = d_values;
-                lp.rhs = d_rhs;
-                lp.x_out = d_x;
-                lp.g_rms = ctx->grms.as<double>();
-                lp.status = ctx->lu_status.as<int32_t>() + b0;
-                lp.entries = ctx->lu_entries.as<bc::LuEntry>() + b0;
-                lp.row_ptr = ctx->d_rp.as<int32_t>();
-                lp.col_idx = ctx->d_ci.as<int32_t>();
-                lp.scratch = ctx->lu_scratch.as<double>();
-                lp.n_max = nmax;
-                lp.species = static_cast<int>(s);
-                lp.nnz = static_cast<int>(nnz);
-                lp.block_width = 0;
-                bc::lu_fallback_kernel<<<cnt, 256, smem, st>>>(lp);
-                check_cuda(cudaGetLastError(), "lu_fallback_kernel launch");
-                ctx->launches++;
+            const int64_t ntot = prm->cells * s;
+            if (multi && ntot > 2048) {
+                // Multi-cells breakdown on a large system: the block-diagonal
+                // LU factors cell by cell (the dense LU of strategies.cpp:47
+                // differs from it only in the sign of zeros), then the
+                // fallback residual goes through the global plan.
+                std::vector<bc::LuEntry> cells_e;
+                for (int64_t c = 0; c < prm->cells; ++c) cells_e.push_back({c, 0, 1, 0});
+                check_cuda(ctx->lu_rms_scratch.ensure(sizeof(double) * 8), "cudaMalloc");
+                run_lu(ctx, cells_e, d_values, d_rhs, d_x, nullptr, static_cast<int>(s), static_cast<int>(nnz), 0, st);
+                const MultiResult mr = run_multi(ctx, pat, ctx->d_rp.as<int32_t>(), ctx->d_ci.as<int32_t>(), ctx->m_trp,
+                                                 ctx->m_trow, ctx->m_tval, ctx->m_diag, prm->cells, multi_ranges,
+                                                 d_values, d_rhs, nullptr, d_x, prm->tol, prm->max_iter, prm->algo,
+                                                 1, st);
+                check_cuda(cudaMemcpyAsync(ctx->grms.p, &mr.rms, sizeof(double), cudaMemcpyHostToDevice, st),
+                           "H2D rms");
+            } else {
+                run_lu(ctx, ents, d_values, d_rhs, d_x, ctx->grms.as<double>(), static_cast<int>(s),
+                       static_cast<int>(nnz), multi ? static_cast<int>(mtpb) : 0, st);
             }
-            std::vector<int32_t> status(ents.size());
-            check_cuda(cudaMemcpyAsync(status.data(), ctx->lu_status.p, sizeof(int32_t) * ents.size(),
-                                       cudaMemcpyDeviceToHost, st), "D2H lu status");
-            check_cuda(cudaStreamSynchronize(st), "lu_fallback_kernel");
-            for (size_t i = 0; i < ents.size(); ++i) {
-                if (status[i]) fail(BC_ERR_SINGULAR_MATRIX, "lu_solve: exactly singular matrix");
-                flags[ents[i].gout] |= BC_FLAG_FELL_BACK;
-            }
+            for (const auto& e : ents) flags[e.gout] |= BC_FLAG_FELL_BACK;
             fallbacks = static_cast<int64_t>(ents.size());
         }
         if (timing) check_cuda(cudaEventRecord(ctx->e1, st), "cudaEventRecord");
@@ -803,9 +964,34 @@ int bc_bicg_solve(bc_ctx* ctx, int32_t algo, int32_t n, const int32_t* row_ptr, 
             expect = ranges[2 * k + 1];
         }
         if (expect != n) fail(BC_ERR_INVALID_ARGUMENT, "reduction plan does not cover [0, n)");
-        if (n_blocks != 1) fail(BC_ERR_INVALID_ARGUMENT, "multi-interval reduction plans need the Multi-cells path");
-        if (n > bc::kMaxGroupRows) fail(BC_ERR_INVALID_ARGUMENT, "system exceeds 2048 rows");
         const bc::Pattern pat = make_pattern(n, row_ptr, col_idx);
+        if (n_blocks != 1 || n > bc::kMaxGroupRows) {
+            // general ReductionPlan (several intervals + sequential combine):
+            // the Multi-cells kernel over one "cell" holding the whole system
+            DevBuf rp, ci, trp, trow, tval, dg, dv, db, dx0, dx;
+            auto up = [](DevBuf* b, const void* src, size_t bytes) {
+                check_cuda(b->ensure(std::max<size_t>(bytes, 8)), "cudaMalloc");
+                if (bytes) check_cuda(cudaMemcpy(b->p, src, bytes, cudaMemcpyDefault), "copy");
+            };
+            up(&rp, pat.row_ptr.data(), sizeof(int32_t) * pat.row_ptr.size());
+            up(&ci, pat.col_idx.data(), sizeof(int32_t) * pat.col_idx.size());
+            up(&dv, vals, sizeof(double) * pat.nnz);
+            up(&db, b, sizeof(double) * n);
+            if (x0) up(&dx0, x0, sizeof(double) * n);
+            check_cuda(dx.ensure(sizeof(double) * n), "cudaMalloc");
+            upload_multi_tables(pat, &trp, &trow, &tval, &dg);
+            std::vector<int64_t> rg(ranges, ranges + 2 * n_blocks);
+            const MultiResult mr = run_multi(ctx, pat, rp.as<int32_t>(), ci.as<int32_t>(), trp, trow, tval, dg, 1, rg,
+                                             dv.as<double>(), db.as<double>(), x0 ? dx0.as<double>() : nullptr,
+                                             dx.as<double>(), tol, max_iter, algo, 0, 0);
+            check_cuda(cudaMemcpy(x_out, dx.p, sizeof(double) * n, cudaMemcpyDefault), "copy x");
+            for (DevBuf* d : {&rp, &ci, &trp, &trow, &tval, &dg, &dv, &db, &dx0, &dx}) d->release();
+            out->iterations = mr.iters;
+            out->final_residual_rms = mr.rms;
+            out->converged = (mr.flags & BC_FLAG_CONVERGED) ? 1 : 0;
+            out->breakdown = (mr.flags & BC_FLAG_BREAKDOWN) ? 1 : 0;
+            return BC_OK;
+        }
         std::map<std::pair<int, int>, bc::GroupPlan> local;
         const size_t first_buf = ctx->plan_bufs.size();
         const bc::GroupPlan& gp = get_plan(ctx, pat, 1, algo == BC_ALGO_BICG, &local);

@@ -189,7 +189,7 @@ struct TmOpt {
 
 TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
     if (const char* e = std::getenv("BC_SCHED_OPT")) optimize = optimize && std::atoi(e) != 0;
-    int copies = 2;
+    int copies = 1;  // issue-bound at 16 warps: one copy measured fastest (BC_GATHER_COPIES to override)
     if (const char* e = std::getenv("BC_GATHER_COPIES")) copies = std::max(1, std::min(4, std::atoi(e)));
     if (!optimize) copies = 1;
     constexpr int d = 2;

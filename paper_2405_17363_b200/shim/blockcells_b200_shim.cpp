@@ -1,0 +1,308 @@
+// blockcells_b200_shim.cpp -- drop-in replacement for the reference's
+// proj/core/src/strategies.cpp and proj/core/src/bicg.cpp.
+//
+// It defines every symbol those two files define, with the same signatures
+// (strategies.hpp:15-90, bicg.hpp:11-53), and routes the solves through the
+// C ABI of libbc_b200.so (include/blockcells_b200.h), i.e. through the fused
+// sm_100a kernels.  Built against the reference's public headers; linked with
+// the rest of the reference library (csr/reduction/exec_model/dense_lu/...)
+// in place of the two replaced files.  See INTEGRATION.md.
+//
+// Semantics kept from the reference:
+//   * argument checks and exception types (BatchedSystem::check, plan_kernel's
+//     InvalidGrouping / UnsupportedMechanism, bicg's invalid_argument,
+//     SingularMatrix from the LU fallback);
+//   * results: per_cell_x, per_block_iterations, iterations_effective/sum,
+//     max_residual_rms, breakdown_fallbacks, cells_per_block -- bit-identical to
+//     the reference for the default algorithm (BiCG);
+//   * wall_time_ns covers the whole call (strategies.cpp:15-21).
+// worker_count is accepted and ignored: the GPU result does not depend on it,
+// as the reference's does not (tests/test_strategies.cpp:254-268).
+//
+// Additions (blockcells_b200_shim.hpp): the Jacobi-BiCGSTAB algorithm
+// selector and bicgstab_solve with bicg_solve's shape.
+#include "blockcells_b200_shim.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "blockcells/dense_lu.hpp"
+#include "blockcells_b200.h"
+
+namespace blockcells {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+std::int64_t elapsed_ns(Clock::time_point start) {
+    return std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - start).count();
+}
+
+thread_local b200::Algorithm t_algorithm = b200::Algorithm::BiCG;
+
+b200::Algorithm env_algorithm() {
+    const char* e = std::getenv("BLOCKCELLS_B200_ALGO");
+    if (e && std::string(e) == "bicgstab") return b200::Algorithm::JacobiBiCGStab;
+    return t_algorithm;
+}
+
+// One context per (calling thread, device): contexts are not thread-safe.
+struct CtxHolder {
+    bc_ctx* ctx = nullptr;
+    std::vector<int32_t> row_ptr, col_idx;  // last pattern handed to the GPU
+    ~CtxHolder() {
+        if (ctx) bc_ctx_destroy(ctx);
+    }
+};
+
+bc_ctx* context() {
+    thread_local CtxHolder h;
+    if (!h.ctx) {
+        int dev = 0;
+        if (const char* e = std::getenv("BLOCKCELLS_B200_DEVICE")) dev = std::atoi(e);
+        const int st = bc_ctx_create(dev, &h.ctx);
+        if (st != BC_OK) throw std::runtime_error("blockcells_b200: no usable sm_100a device (status " +
+                                                  std::to_string(st) + ")");
+    }
+    return h.ctx;
+}
+
+[[noreturn]] void raise_status(int st, const char* msg) {
+    const std::string m = msg ? msg : "";
+    switch (st) {
+        case BC_ERR_INVALID_GROUPING: throw InvalidGrouping(m);
+        case BC_ERR_UNSUPPORTED_MECHANISM: throw UnsupportedMechanism(m);
+        case BC_ERR_SINGULAR_MATRIX: throw SingularMatrix(m);
+        case BC_ERR_INVALID_ARGUMENT: throw std::invalid_argument(m);
+        case BC_ERR_NO_MEMORY: throw std::bad_alloc();
+        default: throw std::runtime_error("blockcells_b200: " + m);
+    }
+}
+
+void check(bc_ctx* ctx, int st) {
+    if (st != BC_OK) raise_status(st, bc_last_error(ctx));
+}
+
+void set_pattern(bc_ctx* ctx, const CsrMatrix& m) {
+    thread_local std::vector<int32_t> rp, ci;
+    std::vector<int32_t> nrp(m.row_ptr.begin(), m.row_ptr.end()), nci(m.col_idx.begin(), m.col_idx.end());
+    if (nrp == rp && nci == ci) return;
+    check(ctx, bc_set_pattern(ctx, static_cast<int32_t>(m.n_rows), nrp.data(), nci.data()));
+    rp.swap(nrp);
+    ci.swap(nci);
+}
+
+SolveReport run_gpu(const BatchedSystem& system, int strategy, std::optional<std::size_t> k,
+                    const DeviceSpec& device, double tol, std::size_t max_iter, Strategy kind) {
+    system.check();  // strategies.cpp:91-107
+    const auto start = Clock::now();
+    bc_ctx* ctx = context();
+    const CsrMatrix& first = system.per_cell_matrices.front();
+    set_pattern(ctx, first);
+    const std::size_t s = system.species, cells = system.cells, nnz = first.nnz();
+    // pack BatchedSystem -> the C ABI's cell-major arrays
+    std::vector<double> values(cells * nnz), rhs(cells * s), x(cells * s);
+    for (std::size_t c = 0; c < cells; ++c) {
+        std::memcpy(values.data() + c * nnz, system.per_cell_matrices[c].values.data(), sizeof(double) * nnz);
+        std::memcpy(rhs.data() + c * s, system.per_cell_rhs[c].data(), sizeof(double) * s);
+    }
+    bc_solve_params prm{};
+    prm.strategy = strategy;
+    prm.algo = env_algorithm() == b200::Algorithm::BiCG ? BC_ALGO_BICG : BC_ALGO_BICGSTAB_JACOBI;
+    if (k) {
+        if (*k < 1) throw std::invalid_argument("plan_kernel: cells per block must be >= 1");
+        prm.cells_per_block = static_cast<int64_t>(*k);
+    }
+    prm.cells = static_cast<int64_t>(cells);
+    prm.tol = tol;
+    prm.max_iter = static_cast<int64_t>(std::min<std::size_t>(max_iter, INT64_MAX));
+    prm.max_threads_per_block = static_cast<int64_t>(device.max_threads_per_block);
+    device.check();
+    int64_t n_groups = 0;
+    double cpb = 0;
+    check(ctx, bc_plan(static_cast<int32_t>(s), &prm, &n_groups, &cpb));
+    std::vector<int32_t> iters(n_groups);
+    bc_report rep{};
+    check(ctx, bc_solve(ctx, &prm, values.data(), rhs.data(), x.data(), iters.data(), nullptr, nullptr, &rep));
+
+    SolveReport report;  // merge_groups, strategies.cpp:71-87
+    report.strategy = kind;
+    report.cells_per_block = rep.cells_per_block;
+    report.per_block_iterations.assign(iters.begin(), iters.end());
+    report.iterations_sum = static_cast<std::size_t>(rep.iterations_sum);
+    report.iterations_effective = static_cast<std::size_t>(rep.iterations_effective);
+    report.max_residual_rms = rep.max_residual_rms;
+    report.breakdown_fallbacks = static_cast<std::size_t>(rep.breakdown_fallbacks);
+    report.per_cell_x.reserve(cells);
+    for (std::size_t c = 0; c < cells; ++c) report.per_cell_x.emplace_back(x.begin() + c * s, x.begin() + (c + 1) * s);
+    report.wall_time_ns = elapsed_ns(start);
+    return report;
+}
+
+SolveOutcome single_system(b200::Algorithm algo, const CsrMatrix& a, const DenseVector& b, const DenseVector& x0,
+                           double tol, std::size_t max_iter, const ReductionPlan& reduction) {
+    if (a.n_rows != a.n_cols) throw std::invalid_argument("bicg: matrix not square");
+    const std::size_t n = a.n_rows;
+    if (b.size() != n || x0.size() != n) throw std::invalid_argument("bicg: dimension mismatch");
+    if (!(tol > 0.0)) throw std::invalid_argument("bicg: tol must be positive");
+    if (max_iter < 1) throw std::invalid_argument("bicg: max_iter must be >= 1");
+    reduction.check_partition(n);
+    bc_ctx* ctx = context();
+    std::vector<int32_t> rp(a.row_ptr.begin(), a.row_ptr.end()), ci(a.col_idx.begin(), a.col_idx.end());
+    std::vector<int64_t> ranges;
+    for (const IndexRange& r : reduction.block_ranges) {
+        ranges.push_back(static_cast<int64_t>(r.begin));
+        ranges.push_back(static_cast<int64_t>(r.end));
+    }
+    SolveOutcome out;
+    out.x.resize(n);
+    bc_outcome o{};
+    check(ctx, bc_bicg_solve(ctx, algo == b200::Algorithm::BiCG ? BC_ALGO_BICG : BC_ALGO_BICGSTAB_JACOBI,
+                             static_cast<int32_t>(n), rp.data(), ci.data(), a.values.data(), b.data(), x0.data(), tol,
+                             static_cast<int64_t>(max_iter), static_cast<int64_t>(reduction.n_blocks()),
+                             ranges.data(), out.x.data(), &o));
+    out.iterations = static_cast<std::size_t>(o.iterations);
+    out.final_residual_rms = o.final_residual_rms;
+    out.converged = o.converged != 0;
+    out.breakdown = o.breakdown != 0;
+    return out;
+}
+
+}  // namespace
+
+namespace b200 {
+
+void set_default_algorithm(Algorithm a) { t_algorithm = a; }
+Algorithm default_algorithm() { return env_algorithm(); }
+
+SolveOutcome bicgstab_solve(const CsrMatrix& a, const DenseVector& b, const DenseVector& x0, double tol,
+                            std::size_t max_iter, const ReductionPlan& reduction) {
+    return single_system(Algorithm::JacobiBiCGStab, a, b, x0, tol, max_iter, reduction);
+}
+
+}  // namespace b200
+
+// ---- strategies.cpp surface ------------------------------------------------
+
+void BatchedSystem::check() const {  // strategies.cpp:91-107
+    if (cells == 0) throw std::invalid_argument("batched system: no cells");
+    if (species == 0) throw std::invalid_argument("batched system: no species");
+    if (per_cell_matrices.size() != cells || per_cell_rhs.size() != cells)
+        throw std::invalid_argument("batched system: per-cell arrays mismatch");
+    const CsrMatrix& first = per_cell_matrices.front();
+    for (const CsrMatrix& m : per_cell_matrices) {
+        if (m.n_rows != species || m.n_cols != species)
+            throw std::invalid_argument("batched system: cell matrix dimension");
+        if (m.row_ptr != first.row_ptr || m.col_idx != first.col_idx)
+            throw std::invalid_argument("batched system: cells do not share one sparsity pattern");
+    }
+    for (const DenseVector& b : per_cell_rhs)
+        if (b.size() != species) throw std::invalid_argument("batched system: rhs dimension");
+}
+
+std::string StrategyConfig::label() const {
+    switch (kind) {
+        case Strategy::OneCell: return "one-cell";
+        case Strategy::MultiCells: return "multi-cells";
+        case Strategy::BlockCells:
+            return cells_per_block ? "block-cells(" + std::to_string(*cells_per_block) + ")" : "block-cells(N)";
+    }
+    return "?";
+}
+
+AssembledSystem assemble_block_diagonal(const BatchedSystem& system, IndexRange cell_range) {
+    if (cell_range.size() == 0) throw std::invalid_argument("assemble_block_diagonal: empty cell range");
+    if (cell_range.end > system.cells) throw std::invalid_argument("assemble_block_diagonal: range out of bounds");
+    const std::size_t s = system.species;
+    AssembledSystem out;
+    out.a.n_rows = out.a.n_cols = cell_range.size() * s;
+    out.a.row_ptr.push_back(0);
+    for (std::size_t c = cell_range.begin; c < cell_range.end; ++c) {
+        const CsrMatrix& m = system.per_cell_matrices[c];
+        const std::size_t shift = (c - cell_range.begin) * s;
+        for (std::size_t i = 0; i < s; ++i) {
+            for (std::size_t j = m.row_ptr[i]; j < m.row_ptr[i + 1]; ++j) {
+                out.a.col_idx.push_back(m.col_idx[j] + shift);
+                out.a.values.push_back(m.values[j]);
+            }
+            out.a.row_ptr.push_back(out.a.col_idx.size());
+        }
+        out.b.insert(out.b.end(), system.per_cell_rhs[c].begin(), system.per_cell_rhs[c].end());
+    }
+    return out;
+}
+
+SolveReport solve_one_cell(const BatchedSystem& system, double tol, std::size_t max_iter,
+                           const DeviceSpec& device) {
+    return run_gpu(system, BC_STRATEGY_ONE_CELL, std::nullopt, device, tol, max_iter, Strategy::OneCell);
+}
+
+SolveReport solve_multi_cells(const BatchedSystem& system, const DeviceSpec& device, double tol,
+                              std::size_t max_iter) {
+    return run_gpu(system, BC_STRATEGY_MULTI_CELLS, std::nullopt, device, tol, max_iter, Strategy::MultiCells);
+}
+
+SolveReport solve_block_cells(const BatchedSystem& system, std::optional<std::size_t> cells_per_block,
+                              const DeviceSpec& device, double tol, std::size_t max_iter,
+                              std::size_t /*worker_count*/) {
+    return run_gpu(system, BC_STRATEGY_BLOCK_CELLS, cells_per_block, device, tol, max_iter, Strategy::BlockCells);
+}
+
+SolveReport run_strategy(const BatchedSystem& system, const StrategyConfig& config, const DeviceSpec& device,
+                         double tol, std::size_t max_iter, std::size_t worker_count) {
+    switch (config.kind) {
+        case Strategy::OneCell: return solve_one_cell(system, tol, max_iter, device);
+        case Strategy::MultiCells: return solve_multi_cells(system, device, tol, max_iter);
+        case Strategy::BlockCells:
+            return solve_block_cells(system, config.cells_per_block, device, tol, max_iter, worker_count);
+    }
+    throw std::invalid_argument("run_strategy: unknown strategy");
+}
+
+double iteration_reduction_ratio(const SolveReport& a, const SolveReport& b) {
+    if (a.iterations_effective == 0) throw std::invalid_argument("iteration_reduction_ratio: zero denominator");
+    return static_cast<double>(b.iterations_effective) / static_cast<double>(a.iterations_effective);
+}
+
+// ---- bicg.cpp surface -------------------------------------------------------
+
+void BicgWorkspace::resize(std::size_t n, std::size_t n_blocks) {
+    r.resize(n);
+    r_shadow.resize(n);
+    p.resize(n);
+    p_shadow.resize(n);
+    ap.resize(n);
+    atp_shadow.resize(n);
+    per_block_error.resize(n_blocks);
+}
+
+std::vector<bool> block_converged_mask(const std::vector<double>& per_block_error,
+                                       const std::vector<std::size_t>& n_per_block, double tol) {
+    if (per_block_error.size() != n_per_block.size())
+        throw std::invalid_argument("block_converged_mask: arrays not aligned");
+    std::vector<bool> mask(per_block_error.size());
+    for (std::size_t b = 0; b < mask.size(); ++b)
+        mask[b] = std::sqrt(per_block_error[b] / static_cast<double>(n_per_block[b])) <= tol;
+    return mask;
+}
+
+SolveOutcome bicg_solve(const CsrMatrix& a, const DenseVector& b, const DenseVector& x0, double tol,
+                        std::size_t max_iter, const ReductionPlan& reduction) {
+    return single_system(b200::Algorithm::BiCG, a, b, x0, tol, max_iter, reduction);
+}
+
+SolveOutcome bicg_solve(const CsrMatrix& a, const DenseVector& b, const DenseVector& x0, double tol,
+                        std::size_t max_iter, const ReductionPlan& reduction, BicgWorkspace& ws) {
+    ws.resize(a.n_rows, reduction.n_blocks());
+    return single_system(b200::Algorithm::BiCG, a, b, x0, tol, max_iter, reduction);
+}
+
+}  // namespace blockcells

@@ -1,0 +1,45 @@
+"""The reference's OWN unit tests for the solver path (test_bicg.cpp,
+test_strategies.cpp from /root/reference/proj/tests, compiled unmodified by
+tests/cpp/Makefile) run against the B200 drop-in (shim + libbc_b200.so), next
+to the same suite linked with the reference's strategies.cpp/bicg.cpp.  The
+drop-in must reproduce the reference's outcome check for check -- including
+the reference's one known failing case (test_bicg.cpp:77, two systems that
+stagnate just above tol): bit-identical BiCG fails it the same
+way."""
+import os
+import re
+import subprocess
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+BIN = os.path.join(HERE, "cpp", "bin")
+B200 = os.path.join(BIN, "ref_suite_b200")
+REF = os.path.join(BIN, "ref_suite_reference")
+
+needs_bins = pytest.mark.skipif(not (os.path.exists(B200) and os.path.exists(REF)),
+                                reason="tests/cpp binaries not built (needs /root/reference at build time)")
+
+
+def run(binary):
+    r = subprocess.run([binary], capture_output=True, text=True, timeout=900)
+    summary = re.search(r"test cases: (\d+) \| (\d+) passed \| (\d+) failed; checks: (\d+) passed \| (\d+) failed",
+                        r.stdout)
+    assert summary, r.stdout[-2000:] + r.stderr[-2000:]
+    failures = sorted(set(re.findall(r"^\s+(\S+:\d+): ", r.stdout, re.M)))
+    return tuple(int(g) for g in summary.groups()), failures, r.stdout
+
+
+@needs_bins
+def test_reference_suite_on_cpu_reference():
+    counts, failures, _ = run(REF)
+    assert counts[0] == 27 and counts[2] <= 1
+
+
+@needs_bins
+@pytest.mark.gpu
+def test_reference_suite_on_b200_dropin_matches_reference():
+    ref_counts, ref_fail, _ = run(REF)
+    counts, failures, out = run(B200)
+    assert counts == ref_counts, out[-3000:]
+    assert failures == ref_fail, out[-3000:]
