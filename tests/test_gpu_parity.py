@@ -69,7 +69,8 @@ def m156_batches(m156):
 
 @pytest.mark.parametrize("regime", ["P", "C"])
 @pytest.mark.parametrize("kind,k", [(Strategy.BlockCells, 1), (Strategy.OneCell, None),
-                                    (Strategy.BlockCells, None), (Strategy.BlockCells, 3)])
+                                    (Strategy.BlockCells, None), (Strategy.BlockCells, 3),
+                                    (Strategy.MultiCells, None)])
 def test_m156_bicg_bitwise_vs_reference(solver, m156, m156_batches, regime, kind, k):
     reg, v, b = m156_batches[regime]
     sysm = system_of(m156.row_ptr, m156.col_idx, v, b)
@@ -89,8 +90,10 @@ def test_m156_bicg_bitwise_vs_reference(solver, m156, m156_batches, regime, kind
 
 @pytest.mark.parametrize("regime", ["P", "C"])
 @pytest.mark.parametrize("kind,k", [(Strategy.BlockCells, 1), (Strategy.BlockCells, None),
-                                    (Strategy.BlockCells, 4)])
+                                    (Strategy.BlockCells, 4), (Strategy.MultiCells, None)])
 def test_m156_bicgstab_bitwise_vs_oracle(solver, m156, m156_batches, regime, kind, k):
+    if kind == Strategy.MultiCells and regime == "P":
+        pytest.skip("a Multi-cells breakdown makes the CPU checker densify a 15600^2 system for its LU")
     reg, v, b = m156_batches[regime]
     sysm = system_of(m156.row_ptr, m156.col_idx, v, b)
     rep = run_gpu(solver, sysm, kind, k, Algo.BICGSTAB_JACOBI, reg.tol, reg.max_iter)
@@ -275,3 +278,41 @@ def test_device_newton_assembly_bitwise(solver, m156):
         dv, db = assemble_on_device(solver, m156, 500, 300, 2000, h)
         np.testing.assert_array_equal(of.bits(dv.cpu().numpy()), of.bits(v))
         np.testing.assert_array_equal(of.bits(db.cpu().numpy()), of.bits(b))
+
+
+@pytest.mark.parametrize("algo", [0, 1])
+def test_single_system_multi_interval_plan(solver, algo):
+    """bicg_solve with a host-stage ReductionPlan (test_bicg.cpp:122-182 shapes)."""
+    rng = np.random.default_rng(31)
+    for n, widths in ((32, [16, 16]), (100, [33, 33, 34]), (300, [100, 100, 100]), (2500, [1024, 1024, 452])):
+        rp, ci, v, b = random_batch(rng, 1, n, min(0.3, 6.0 / n))
+        x0 = rng.uniform(-1, 1, n)
+        ranges, s0 = [], 0
+        for w in widths:
+            ranges.append((s0, s0 + w))
+            s0 += w
+        out = solver.bicg_solve(n, rp, ci, v[0], b[0], x0, 1e-13, 300, ReductionPlan(ranges, True), algo=Algo(algo))
+        st, x, o = of.orc_solve_single(algo, rp, ci, v[0], b[0], x0, 1e-13, 300, ranges)
+        assert st == 0
+        np.testing.assert_array_equal(of.bits(out.x), of.bits(x), err_msg=f"n={n}")
+        assert out.iterations == o.iterations and out.converged == bool(o.converged)
+        assert of.bits(out.final_residual_rms) == of.bits(o.final_residual_rms)
+
+
+def test_multi_cells_random_and_breakdown(solver):
+    """Multi-cells over several 1024-row intervals, plus its LU fallback."""
+    rng = np.random.default_rng(7)
+    rp, ci, v, b = random_batch(rng, 90, 13)  # 1170 rows > one interval (test_strategies.cpp:156-176)
+    for algo in (Algo.BICG, Algo.BICGSTAB_JACOBI):
+        rep = run_gpu(solver, system_of(rp, ci, v, b), Strategy.MultiCells, None, algo, 1e-12, 500)
+        st, res = of.orc_solve_batch(1, int(algo), 0, rp, ci, v, b, 1e-12, 500)
+        assert st == 0
+        assert_matches_oracle(rep, res, f"multi {algo}")
+    rp2 = np.array([0, 2, 4], np.int32)
+    ci2 = np.array([0, 1, 0, 1], np.int32)
+    v2 = np.array([[3.0, 1.0, -1.0, 3.0], [0.0, 1.0, -1.0, 0.0]])
+    b2 = np.array([[1.0, 2.0], [3.0, 4.0]])
+    rep = run_gpu(solver, system_of(rp2, ci2, v2, b2), Strategy.MultiCells, None, Algo.BICG, 1e-13, 100)
+    st, res = of.orc_solve_batch(1, 0, 0, rp2, ci2, v2, b2, 1e-13, 100)
+    assert st == 0
+    assert_matches_oracle(rep, res, "multi breakdown")
