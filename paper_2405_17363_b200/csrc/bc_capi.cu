@@ -18,6 +18,7 @@
 #include "bc_lu.cuh"
 #include "bc_multi.cuh"
 #include "bc_newton.cuh"
+#include "bc_thread.cuh"
 #include "bc_tmem.cuh"
 #include "bc_plan.hpp"
 #include "blockcells_b200.h"
@@ -107,7 +108,7 @@ struct bc_ctx {
     std::map<std::pair<int, int>, bc::GroupPlan> plans;  // (k, with_transpose)
     std::vector<DevBuf> plan_bufs;
     DevBuf values, rhs, x, giters, grms, gflags, counters, lu_scratch, lu_entries, lu_status,
-        f_scratch, lu_rms_scratch;
+        f_scratch, lu_rms_scratch, t_values, t_work;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     int64_t launches = 0;
     std::map<BlockFn, bool> smem_set;
@@ -680,7 +681,9 @@ void bc_ctx_destroy(bc_ctx* ctx) {
     cudaSetDevice(ctx->device);
     for (DevBuf* b : {&ctx->d_rp, &ctx->d_ci, &ctx->values, &ctx->rhs, &ctx->x, &ctx->giters,
                       &ctx->grms, &ctx->gflags, &ctx->counters, &ctx->lu_scratch,
-                      &ctx->lu_entries, &ctx->lu_status, &ctx->f_scratch})
+                      &ctx->lu_entries, &ctx->lu_status, &ctx->f_scratch, &ctx->lu_rms_scratch, &ctx->t_values,
+                      &ctx->t_work, &ctx->m_trp, &ctx->m_trow, &ctx->m_tval, &ctx->m_diag, &ctx->m_ranges,
+                      &ctx->m_work, &ctx->m_part, &ctx->m_out})
         b->release();
     for (DevBuf& b : ctx->plan_bufs) b.release();
     if (ctx->e0) cudaEventDestroy(ctx->e0);
@@ -776,8 +779,6 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
         if (prm->max_iter < 1) fail(BC_ERR_INVALID_ARGUMENT, "bicg: max_iter must be >= 1");
         if (prm->algo != BC_ALGO_BICG && prm->algo != BC_ALGO_BICGSTAB_JACOBI)
             fail(BC_ERR_INVALID_ARGUMENT, "unknown algorithm");
-        if (prm->strategy == BC_STRATEGY_THREAD_PER_CELL)
-            fail(BC_ERR_INVALID_ARGUMENT, "strategy not available in this build");
 
         cudaStream_t st = static_cast<cudaStream_t>(prm->stream);
         const int64_t cells = prm->cells, s = pat.species, nnz = pat.nnz;
@@ -808,6 +809,7 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
         const bool timing = (prm->options & BC_OPT_TIMING) != 0;
         const bool bicg = prm->algo == BC_ALGO_BICG;
         const bool multi = prm->strategy == BC_STRATEGY_MULTI_CELLS;
+        const bool tpc = prm->strategy == BC_STRATEGY_THREAD_PER_CELL;
         const int64_t mtpb = prm->max_threads_per_block > 0 ? prm->max_threads_per_block : 1024;
         std::vector<int64_t> multi_ranges;
         if (multi) {  // exec_model.cpp:202-220: one interval per 1024-thread block + host stage
@@ -821,6 +823,13 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
                 multi_ranges.push_back(b0);
                 multi_ranges.push_back(std::min(ntot, b0 + mtpb));
             }
+        } else if (tpc) {
+            if (!ctx->m_ready) {
+                upload_multi_tables(pat, &ctx->m_trp, &ctx->m_trow, &ctx->m_tval, &ctx->m_diag);
+                ctx->m_ready = true;
+            }
+            check_cuda(ctx->t_values.ensure(sizeof(double) * prm->cells * nnz), "cudaMalloc(interleaved)");
+            check_cuda(ctx->t_work.ensure(sizeof(double) * 9 * prm->cells * s), "cudaMalloc(thread work)");
         } else {
             for (const GroupSpan& sp : spans) {  // host-side planning before the timed region
                 bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);
@@ -848,8 +857,40 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
             check_cuda(cudaMemcpyAsync(ctx->gflags.p, &f8, 1, cudaMemcpyHostToDevice, st), "H2D");
             check_cuda(cudaStreamSynchronize(st), "H2D multi outputs");
         }
+        if (tpc) {  // one thread per cell (bc_thread.cuh)
+            const dim3 tb(32, 8), tg(static_cast<unsigned>((prm->cells + 31) / 32), static_cast<unsigned>((nnz + 31) / 32));
+            bc::interleave_kernel<<<tg, tb, 0, st>>>(d_values, ctx->t_values.as<double>(), prm->cells,
+                                                     static_cast<int>(nnz));
+            check_cuda(cudaGetLastError(), "interleave_kernel launch");
+            bc::ThreadParams tp{};
+            tp.values_il = ctx->t_values.as<double>();
+            tp.rhs = d_rhs;
+            tp.x_out = d_x;
+            tp.work = ctx->t_work.as<double>();
+            tp.row_ptr = ctx->d_rp.as<int32_t>();
+            tp.col_idx = ctx->d_ci.as<int32_t>();
+            tp.diag = ctx->m_diag.as<int32_t>();
+            tp.g_iters = ctx->giters.as<int32_t>();
+            tp.g_rms = ctx->grms.as<double>();
+            tp.g_flags = ctx->gflags.as<uint8_t>();
+            tp.cells = prm->cells;
+            tp.species = static_cast<int>(s);
+            tp.nnz = static_cast<int>(nnz);
+            int lg = 0;
+            while ((int64_t(1) << lg) < s) ++lg;
+            tp.log2P = lg;
+            tp.tol = prm->tol;
+            tp.max_iter = prm->max_iter;
+            const unsigned blocks = static_cast<unsigned>((prm->cells + 127) / 128);
+            if (bicg)
+                bc::thread_per_cell_kernel<bc::kBiCG><<<blocks, 128, 0, st>>>(tp);
+            else
+                bc::thread_per_cell_kernel<bc::kBiCGStab><<<blocks, 128, 0, st>>>(tp);
+            check_cuda(cudaGetLastError(), "thread_per_cell_kernel launch");
+            ctx->launches += 2;
+        }
         for (const GroupSpan& sp : spans) {
-            if (multi) break;
+            if (multi || tpc) break;
             bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);
             unsigned int* counter = ctx->counters.as<unsigned int>() + slot++;
             if (!bicg && launch_tmem(ctx, pat, gp, sp.cell0, sp.gout0, sp.count, d_values, d_rhs, d_x, prm->tol,

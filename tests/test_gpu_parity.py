@@ -17,7 +17,7 @@ from paper_2405_17363_b200 import (Algo, BatchedSystem, DeviceSpec, InvalidGroup
 
 pytestmark = pytest.mark.gpu
 
-STRAT_ORC = {Strategy.OneCell: 0, Strategy.MultiCells: 1, Strategy.BlockCells: 2}
+STRAT_ORC = {Strategy.OneCell: 0, Strategy.MultiCells: 1, Strategy.BlockCells: 2, Strategy.ThreadPerCell: 0}
 
 
 def system_of(row_ptr, col_idx, values, rhs):
@@ -70,7 +70,7 @@ def m156_batches(m156):
 @pytest.mark.parametrize("regime", ["P", "C"])
 @pytest.mark.parametrize("kind,k", [(Strategy.BlockCells, 1), (Strategy.OneCell, None),
                                     (Strategy.BlockCells, None), (Strategy.BlockCells, 3),
-                                    (Strategy.MultiCells, None)])
+                                    (Strategy.MultiCells, None), (Strategy.ThreadPerCell, None)])
 def test_m156_bicg_bitwise_vs_reference(solver, m156, m156_batches, regime, kind, k):
     reg, v, b = m156_batches[regime]
     sysm = system_of(m156.row_ptr, m156.col_idx, v, b)
@@ -80,7 +80,7 @@ def test_m156_bicg_bitwise_vs_reference(solver, m156, m156_batches, regime, kind
                                  workers=8)
     assert st == 0
     assert_matches_oracle(rep, res, f"{regime} {kind} {k} vs oracle")
-    if of.have_ref():
+    if of.have_ref() and kind != Strategy.ThreadPerCell:  # cells_per_block differs for the baseline
         st, rres = of.ref_solve_batch(STRAT_ORC[kind], kk, m156.row_ptr, m156.col_idx, v, b, reg.tol, reg.max_iter,
                                       workers=8)
         assert st == 0
@@ -90,7 +90,8 @@ def test_m156_bicg_bitwise_vs_reference(solver, m156, m156_batches, regime, kind
 
 @pytest.mark.parametrize("regime", ["P", "C"])
 @pytest.mark.parametrize("kind,k", [(Strategy.BlockCells, 1), (Strategy.BlockCells, None),
-                                    (Strategy.BlockCells, 4), (Strategy.MultiCells, None)])
+                                    (Strategy.BlockCells, 4), (Strategy.MultiCells, None),
+                                    (Strategy.ThreadPerCell, None)])
 def test_m156_bicgstab_bitwise_vs_oracle(solver, m156, m156_batches, regime, kind, k):
     if kind == Strategy.MultiCells and regime == "P":
         pytest.skip("a Multi-cells breakdown makes the CPU checker densify a 15600^2 system for its LU")
@@ -135,7 +136,7 @@ def test_random_batches_all_groupings(solver, algo):
         rp, ci, v, b = random_batch(rng, cells, species, 0.3)
         sysm = system_of(rp, ci, v, b)
         kmax = max(1, 1024 // species)
-        for kind, k in [(Strategy.OneCell, None), (Strategy.BlockCells, 1),
+        for kind, k in [(Strategy.OneCell, None), (Strategy.ThreadPerCell, None), (Strategy.BlockCells, 1),
                         (Strategy.BlockCells, int(rng.integers(1, min(cells, kmax) + 1))), (Strategy.BlockCells, None)]:
             rep = run_gpu(solver, sysm, kind, k, algo, 1e-12, 300)
             st, res = of.orc_solve_batch(STRAT_ORC[kind], int(algo), 0 if k is None else k, rp, ci, v, b, 1e-12, 300)
