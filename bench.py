@@ -162,6 +162,16 @@ def cpu_reference_rate(values, rhs, row_ptr, col_idx, reg, budget_s, algo_name="
     return nc / dt, cores, sample, kind
 
 
+def strategy_config(name):
+    """block-cells-1 (default) / block-cells-<k> / block-cells-N / one-cell / multi-cells / thread-per-cell"""
+    from paper_2405_17363_b200 import Strategy, StrategyConfig
+    if name.startswith("block-cells-"):
+        k = name.rsplit("-", 1)[-1]
+        return StrategyConfig(Strategy.BlockCells, None if k == "N" else int(k))
+    return {"one-cell": StrategyConfig(Strategy.OneCell), "multi-cells": StrategyConfig(Strategy.MultiCells),
+            "thread-per-cell": StrategyConfig(Strategy.ThreadPerCell)}[name]
+
+
 def make_workload(cells, first, total, reg):
     import numpy as np
     from paper_2405_17363_b200 import Mechanism
@@ -209,7 +219,8 @@ def main_b200(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2405_17363_b200 import Algo, BatchedSystem, DeviceSpec, Solver, Strategy, StrategyConfig
+    from paper_2405_17363_b200 import Algo, BatchedSystem, DeviceSpec, Solver, Strategy
+    from paper_2405_17363_b200.sharding import merge_reports, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -231,10 +242,10 @@ def main_b200(args):
 
     reg = regime(args.regime)
     algo = Algo.BICGSTAB_JACOBI if args.algo == "bicgstab" else Algo.BICG
-    k = int(args.strategy.rsplit("-", 1)[-1]) if args.strategy.startswith("block-cells-") else None
-    cells = args.cells
-    n_total = cells * world
-    first = rank * cells  # contiguous cell ranges; k=1 so every boundary is a group boundary
+    cfg = strategy_config(args.strategy)
+    k = cfg.cells_per_block or (1024 // SPECIES if cfg.kind == Strategy.BlockCells else 1)
+    n_total = args.cells * world  # weak scaling: every rank solves args.cells cells of the global batch
+    first, cells = shard_range(n_total, k, rank, world)  # contiguous, group-aligned ranges, no collectives
     m, h_values, h_rhs = make_workload(cells, first, n_total, reg)
     nnz, n = m.nnz, m.species
 
@@ -244,7 +255,6 @@ def main_b200(args):
     d_rhs = torch.from_numpy(h_rhs).cuda()
     d_x = torch.empty((cells, n), dtype=torch.float64, device="cuda")
     dsys = BatchedSystem(n, cells, m.row_ptr, m.col_idx, d_values, d_rhs)
-    cfg = StrategyConfig(Strategy.BlockCells, k)
     dev = DeviceSpec()
 
     def step(timing=False):
@@ -275,14 +285,23 @@ def main_b200(args):
     value = n_total * args.steps / (total_ms / 1e3)
     rep = reports[-1]
     iters = np.asarray(rep.per_block_iterations)
-    alg_bytes = algorithmic_bytes(iters, n, nnz)  # per launch (one solve of the rank's cells)
+    merged = merge_reports(dict(iterations_effective=rep.iterations_effective, max_residual_rms=rep.max_residual_rms,
+                                iterations_sum=rep.iterations_sum, breakdown_fallbacks=rep.breakdown_fallbacks,
+                                n_groups=len(rep.per_block_iterations)))
+    # it_c of every cell = its group's iteration count
+    sizes = np.full(len(iters), cells // max(len(iters), 1), dtype=np.int64)
+    if cfg.kind == Strategy.BlockCells and len(iters) > 1:
+        sizes[:] = k
+        sizes[-1] = cells - k * (len(iters) - 1)
+    cell_iters = np.repeat(iters, sizes)
+    alg_bytes = algorithmic_bytes(cell_iters, n, nnz)  # per launch (one solve of the rank's cells)
     kmean = statistics.mean(kernel_ms)
     achieved = alg_bytes / (kmean / 1e3) / 1e9
     peak, peak_kind = measured_peak_hbm()
     compulsory = cells * (8 * nnz + 16 * n + 16)
     tr = ncu_traffic()
     flops_per_it = (4 * nnz + 24 * n) if algo == Algo.BICGSTAB_JACOBI else (4 * nnz + 21 * n)
-    fp64 = float(iters.sum()) * flops_per_it / (kmean / 1e3) / 1e12
+    fp64 = float(cell_iters.sum()) * flops_per_it / (kmean / 1e3) / 1e12
 
     # e2e through the public API with pinned host inputs
     e2e = None
@@ -322,8 +341,8 @@ def main_b200(args):
                              f"({n_total} total), {args.strategy}, {'Jacobi-BiCGSTAB' if algo else 'BiCG'}, "
                              f"{reg.name} regime (h={reg.h:g} s, tol={reg.tol:g}, max_iter={reg.max_iter})"),
                 "cells_per_gpu": cells, "global_cells": n_total, "strategy": args.strategy,
-                "algorithm": args.algo, "regime": reg.name, "iterations_sum": int(iters.sum()),
-                "breakdown_fallbacks": rep.breakdown_fallbacks,
+                "algorithm": args.algo, "regime": reg.name, "iterations_sum": int(merged["iterations_sum"]),
+                "breakdown_fallbacks": int(merged["breakdown_fallbacks"]),
                 "l2": f"inputs larger than L2 ({h_values.nbytes / 1e9:.3f} GB values per GPU vs 126 MB L2)",
                 "parallelism": f"cell-range sharding over {world} GPU(s), no collectives",
             },
