@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cells", type=int, default=100_000, help="cells per GPU")
+    ap.add_argument("--species", type=int, default=SPECIES,
+                    help="mechanism size: 156 (CB05-sized M156) or 312 (scaled M312, BASELINE.json configs[4])")
     ap.add_argument("--regime", default="P", choices=["P", "C"])
     ap.add_argument("--algo", default="bicgstab", choices=["bicgstab", "bicg"])
     ap.add_argument("--strategy", default="block-cells-1")
@@ -172,10 +174,22 @@ def strategy_config(name):
             "thread-per-cell": StrategyConfig(Strategy.ThreadPerCell)}[name]
 
 
-def make_workload(cells, first, total, reg):
+def dominant_kernel(cfg, algo, k):
+    """The kernel that carries the step (csrc/bc_capi.cu dispatch)."""
+    from paper_2405_17363_b200 import Algo, Strategy
+    if cfg.kind == Strategy.MultiCells:
+        return "multi_cells_kernel"
+    if cfg.kind == Strategy.ThreadPerCell:
+        return "thread_per_cell_kernel"
+    if algo == Algo.BICGSTAB_JACOBI and (cfg.kind == Strategy.OneCell or k == 1):
+        return "block_cells_tmem_kernel"
+    return "block_cells_kernel"
+
+
+def make_workload(cells, first, total, reg, species=SPECIES):
     import numpy as np
     from paper_2405_17363_b200 import Mechanism
-    m = Mechanism(SPECIES, REACTIONS, SEED)
+    m = Mechanism(species, 3 * species, SEED)  # generate_mechanism(s, 3s, 0), bench.hpp:18,25,32
     try:
         import torch
         values = torch.empty((cells, m.nnz), dtype=torch.float64, pin_memory=torch.cuda.is_available()).numpy()
@@ -193,7 +207,7 @@ def main_reference(args):
         return
     reg = regime(args.regime)
     n_total = args.cells * args.gpus
-    m, values, rhs = make_workload(min(args.cells, 50_000), 0, n_total, reg)
+    m, values, rhs = make_workload(min(args.cells, 50_000), 0, n_total, reg, args.species)
     budget = max(2.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
     rates = []
     for i in range(args.warmup + args.steps):
@@ -205,7 +219,7 @@ def main_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * args.cells / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"M156, {args.cells} cells/GPU, Block-cells(1), {reg.name} regime; reference CPU "
+        "config": {"workload": f"M{args.species}, {args.cells} cells/GPU, Block-cells(1), {reg.name} regime; reference CPU "
                                "solver (unpreconditioned BiCG, its only algorithm) on bounded samples",
                    "algorithm": "bicg (reference)", "regime": reg.name},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
@@ -243,10 +257,10 @@ def main_b200(args):
     reg = regime(args.regime)
     algo = Algo.BICGSTAB_JACOBI if args.algo == "bicgstab" else Algo.BICG
     cfg = strategy_config(args.strategy)
-    k = cfg.cells_per_block or (1024 // SPECIES if cfg.kind == Strategy.BlockCells else 1)
+    k = cfg.cells_per_block or (1024 // args.species if cfg.kind == Strategy.BlockCells else 1)
     n_total = args.cells * world  # weak scaling: every rank solves args.cells cells of the global batch
     first, cells = shard_range(n_total, k, rank, world)  # contiguous, group-aligned ranges, no collectives
-    m, h_values, h_rhs = make_workload(cells, first, n_total, reg)
+    m, h_values, h_rhs = make_workload(cells, first, n_total, reg, args.species)
     nnz, n = m.nnz, m.species
 
     solver = Solver(local)
@@ -299,7 +313,10 @@ def main_b200(args):
     achieved = alg_bytes / (kmean / 1e3) / 1e9
     peak, peak_kind = measured_peak_hbm()
     compulsory = cells * (8 * nnz + 16 * n + 16)
+    kname = dominant_kernel(cfg, algo, k)
     tr = ncu_traffic()
+    if not tr or tr.get("kernel") != kname or tr.get("cells") != cells or tr.get("species", 156) != n:
+        tr = None  # the committed ncu capture is for another workload
     flops_per_it = (4 * nnz + 24 * n) if algo == Algo.BICGSTAB_JACOBI else (4 * nnz + 21 * n)
     fp64 = float(cell_iters.sum()) * flops_per_it / (kmean / 1e3) / 1e12
 
@@ -337,7 +354,7 @@ def main_b200(args):
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {
-                "workload": (f"M156 (156 species, 1556 nnz) first Newton system of step 0, {cells} cells/GPU "
+                "workload": (f"M{n} ({n} species, {nnz} nnz) first Newton system of step 0, {cells} cells/GPU "
                              f"({n_total} total), {args.strategy}, {'Jacobi-BiCGSTAB' if algo else 'BiCG'}, "
                              f"{reg.name} regime (h={reg.h:g} s, tol={reg.tol:g}, max_iter={reg.max_iter})"),
                 "cells_per_gpu": cells, "global_cells": n_total, "strategy": args.strategy,
@@ -348,7 +365,7 @@ def main_b200(args):
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": (tr or {}).get("dram_bytes_per_launch_scaled"),
-                         "kernel": "block_cells_kernel", "kernel_ms": kmean, "algorithmic_bytes": alg_bytes,
+                         "kernel": kname, "kernel_ms": kmean, "algorithmic_bytes": alg_bytes,
                          "peak_kind": peak_kind,
                          "compulsory_bytes": compulsory,
                          "compulsory_frac": compulsory / (kmean / 1e3) / 1e9 / peak,

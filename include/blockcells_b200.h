@@ -132,11 +132,12 @@ int bc_schedule_export(int32_t species, const int32_t* row_ptr, const int32_t* c
                        int32_t* xpos, uint32_t* twords, int32_t* tvpos, int32_t* txpos);
 
 /* Schedule of the Tensor-Memory kernel (one warp per group; see
- * paper_2405_17363_b200/csrc/bc_plan.hpp TmemSchedule).  info[0..6] = S
+ * paper_2405_17363_b200/csrc/bc_plan.hpp TmemSchedule).  info[0..8] = S
  * (steps, multiple of 4), xslots, zero_slot, yslots, modelled gather
  * wavefronts per pass, copies of the gather vector, modelled shared
- * wavefronts per SpMV.  Arrays may be NULL to query sizes: words/vidx S*32,
- * xpos copies*k*species, yslot k*species. */
+ * wavefronts per SpMV, row streams per lane, Y slots per stream.  Arrays may
+ * be NULL to query sizes: words/vidx S*32, xpos copies*k*species, yslot
+ * k*species. */
 int bc_tmem_schedule_export(int32_t species, const int32_t* row_ptr, const int32_t* col_idx, int32_t k,
                             int32_t* info, uint16_t* words, int32_t* vidx, int32_t* xpos, int32_t* yslot);
 

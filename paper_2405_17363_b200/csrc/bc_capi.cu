@@ -256,16 +256,23 @@ LaunchShape choose_shape(bc_ctx* ctx, BlockFn fn, const bc::GroupPlan& gp, bool 
 using TmemFn = void (*)(bc::TmemParams);
 
 struct TmemCfg {
-    int R, RV, warps;  // warps per CTA (= 4 * groups per lane quarter)
+    int R, RV, warps, ST;  // warps per CTA (= 4 * groups per lane quarter), row streams per lane
     TmemFn fn;
 };
 
-// 16 warps/SM at <= 128 registers, or 12 warps/SM at <= 168 registers.
+// 16 warps/SM at <= 128 registers, or 12 warps/SM at <= 168 registers; 8
+// warps (<= 255 registers) for schedules too long for 3 groups per quarter
+// (the scaled mechanism: 312 species).  Each with one or two row streams.
+#define BC_TMEM_CFG(R, RV, W)                                                   \
+    {R, RV, W, 1, &bc::block_cells_tmem_kernel<R, RV, 32 * W, 1>},              \
+    {                                                                           \
+        R, RV, W, 2, &bc::block_cells_tmem_kernel<R, RV, 32 * W, 2>             \
+    }
 const TmemCfg kTmemConfigs[] = {
-    {8, 5, 16, &bc::block_cells_tmem_kernel<8, 5, 512>}, {8, 5, 12, &bc::block_cells_tmem_kernel<8, 5, 384>},
-    {8, 8, 16, &bc::block_cells_tmem_kernel<8, 8, 512>}, {8, 8, 12, &bc::block_cells_tmem_kernel<8, 8, 384>},
-    {4, 4, 16, &bc::block_cells_tmem_kernel<4, 4, 512>}, {4, 4, 12, &bc::block_cells_tmem_kernel<4, 4, 384>},
+    BC_TMEM_CFG(8, 5, 16), BC_TMEM_CFG(8, 5, 12), BC_TMEM_CFG(8, 8, 16),   BC_TMEM_CFG(8, 8, 12),
+    BC_TMEM_CFG(4, 4, 16), BC_TMEM_CFG(4, 4, 12), BC_TMEM_CFG(16, 10, 8), BC_TMEM_CFG(16, 16, 8),
 };
+#undef BC_TMEM_CFG
 
 int tmem_warps_pref() {
     const char* e = std::getenv("BC_TMEM_WARPS");
@@ -333,24 +340,40 @@ void ensure_tmem_lane_tables(bc_ctx* ctx, bc::GroupPlan& gp, int RV) {
     gp.tm_lane_rv = RV;
 }
 
+// Groups per TMEM lane quarter that fit 512 columns: S/2 word columns shared
+// by the quarter, 2S value columns per group.
+int tmem_groups_per_quarter(int S) { return S > 0 ? std::min(4, (512 - S / 2) / (2 * S)) : 0; }
+
+// Kernel instance for a plan: same tree width R, enough row slots, and the
+// most warps the schedule's TMEM footprint allows (capped by BC_TMEM_WARPS).
+const TmemCfg* pick_tmem_cfg(const bc::GroupPlan& gp) {
+    const int cpq = tmem_groups_per_quarter(gp.tm.steps);
+    if (cpq < 1) return nullptr;
+    const int want = std::min(4 * cpq, tmem_warps_pref());
+    const TmemCfg* cfg = nullptr;
+    for (const TmemCfg& t : kTmemConfigs) {
+        if (t.R != gp.geo.R || t.RV < gp.geo.RV || t.warps < want || t.ST != gp.tm.streams) continue;
+        if (!cfg || t.warps < cfg->warps || (t.warps == cfg->warps && t.RV < cfg->RV)) cfg = &t;
+    }
+    return cfg;
+}
+
 bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t cell0, int64_t gout0,
                  int groups, const double* values, const double* rhs, double* x, double tol, int64_t max_iter,
                  unsigned int* counter, cudaStream_t st) {
     if (tmem_disabled() || gp.geo.W != 1) return false;
-    const TmemCfg* cfg = nullptr;
-    const int pref = tmem_warps_pref();
-    for (const TmemCfg& t : kTmemConfigs)
-        if (t.R == gp.geo.R && t.RV >= gp.geo.RV && t.warps == pref && (!cfg || t.RV < cfg->RV)) cfg = &t;
-    if (!cfg) return false;
     ensure_tmem_schedule(ctx, pat, gp);
+    const TmemCfg* cfg = pick_tmem_cfg(gp);
+    if (!cfg) return false;
     ensure_tmem_lane_tables(ctx, gp, cfg->RV);
     const int S = gp.tm.steps;
-    const int cpq = S > 0 ? std::min(cfg->warps / 4, (512 - S / 2) / (2 * S)) : 0;
-    if (cpq < 1) return false;
+    const int cpq = std::min(cfg->warps / 4, tmem_groups_per_quarter(S));
     const int warps = 4 * cpq;
     const int xslots = (gp.tm.xslots + 1 + 31) & ~31, yslots = gp.tm.yslots + 32;
+    const int xalign = static_cast<int>(bc::padded_len(8 * xslots));
     const size_t xmore_bytes = ((2 * (gp.tm.copies - 1) * cfg->RV * 32) + 15) & ~15;
-    const size_t smem = sizeof(int32_t) * S * 32 + xmore_bytes + sizeof(double) * warps * (xslots + yslots);
+    const size_t smem = sizeof(int32_t) * S * 32 + xmore_bytes + static_cast<size_t>(xalign) * (warps + 1) +
+                        sizeof(double) * warps * yslots;
     if (smem > static_cast<size_t>(kMaxDynSmem - 1024)) return false;
     if (!ctx->smem_set[reinterpret_cast<BlockFn>(cfg->fn)]) {
         check_cuda(cudaFuncSetAttribute(cfg->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem - 1024),
@@ -381,6 +404,8 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
     p.kc = gp.k;
     p.xslots = xslots;
     p.yslots = yslots;
+    p.xalign = xalign;
+    p.ystream = gp.tm.ystream;
     p.copies = gp.tm.copies;
     p.cells_per_quarter = cpq;
     p.sigma_max = sigma_threshold(tol, gp.geo.n);
@@ -753,7 +778,8 @@ int bc_tmem_schedule_export(int32_t species, const int32_t* row_ptr, const int32
     return guarded(nullptr, [&] {
         const bc::Pattern pat = make_pattern(species, row_ptr, col_idx);
         const bc::TmemSchedule ts = bc::build_tmem_schedule(pat, k);
-        const int v[7] = {ts.steps, ts.xslots, ts.zero_slot, ts.yslots, ts.conflict_cost, ts.copies, ts.model_total};
+        const int v[9] = {ts.steps,  ts.xslots,      ts.zero_slot, ts.yslots, ts.conflict_cost,
+                          ts.copies, ts.model_total, ts.streams,   ts.ystream};
         std::memcpy(info, v, sizeof v);
         if (words) std::memcpy(words, ts.words.data(), sizeof(uint16_t) * ts.words.size());
         if (vidx) std::memcpy(vidx, ts.vidx.data(), sizeof(int32_t) * ts.vidx.size());
@@ -836,11 +862,7 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
                 if (!bicg) {
                     ensure_tmem_schedule(ctx, pat, gp);
                     if (gp.has_tm)
-                        for (const TmemCfg& t : kTmemConfigs)
-                            if (t.R == gp.geo.R && t.RV >= gp.geo.RV) {
-                                ensure_tmem_lane_tables(ctx, gp, t.RV);
-                                break;
-                            }
+                        if (const TmemCfg* t = pick_tmem_cfg(gp)) ensure_tmem_lane_tables(ctx, gp, t->RV);
                 }
             }
         }

@@ -55,9 +55,17 @@ struct Schedule {
 //    that gather a dedicated always-zero slot (acc + 0*0 == acc exactly, as a
 //    CSR sum started at +0.0 is never -0.0), so row ends only fall on odd
 //    steps and the end test runs every other step;
-//  * lane L's k-th row lands in Y[k*32 + L] (conflict-free stores, no output
-//    index in the word); yslot maps rows to those slots for the owner lanes;
-//  * words are 16 bits: gather byte offset (slot*8) | end-of-row << 15;
+//  * with two streams, a lane runs two rows at a time, interleaved step by
+//    step (even steps: stream 0, odd: stream 1), so that its two dependent
+//    DADD chains overlap; stream 0 rows then end on steps 2 mod 4, stream 1
+//    rows on steps 3 mod 4;
+//  * lane L's k-th row of stream s lands in Y[s*ystream + k*32 + L]
+//    (conflict-free stores, no output index in the word); yslot maps rows to
+//    those slots for the owner lanes;
+//  * words are 16 bits: gather byte offset (slot*8); bit 15 of step 4c+2's
+//    word flags a row ending on step 4c+3, bit 15 of step 4c's a row ending
+//    on step 4c+1 (one stream) or 4c+2 (two streams); odd steps' words have it
+//    clear, so both halves of a TMEM word decode to an address in one op;
 //  * the gather vector has `copies` independent placements (bc_tmem_plan.cpp).
 struct TmemSchedule {
     int steps = 0;                  // S, a multiple of 4
@@ -68,8 +76,10 @@ struct TmemSchedule {
     int zero_slot = 0;
     std::vector<int32_t> xpos;      // [copy][group row] -> gather slot
     int model_total = 0;            // modelled wavefronts per SpMV (gathers+stores+reads)
-    std::vector<int32_t> yslot;     // group row -> Y slot (k*32 + lane)
+    std::vector<int32_t> yslot;     // group row -> Y slot (stream*ystream + k*32 + lane)
     int yslots = 0;
+    int streams = 1;                // interleaved row streams per lane (1 or 2)
+    int ystream = 32;               // Y slots per stream
     int conflict_cost = 0;          // modelled gather wavefronts per pass
 };
 

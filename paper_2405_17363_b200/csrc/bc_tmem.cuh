@@ -59,6 +59,8 @@ struct TmemParams {
     int n, nnz, S, P;
     int species, kc;        // group = kc cells of `species` rows
     int xslots, yslots;     // shared doubles per warp: X | Y (multiples of 32)
+    int xalign;             // bytes per warp X region: a power of two >= 8 * xslots
+    int ystream;            // Y slots per row stream (TmemSchedule::ystream)
     int copies;             // copies of the gather vector (1..4)
     int cells_per_quarter;  // warps per lane quarter
     double sigma_max;       // sqrt(sigma/n) <= tol  <=>  sigma <= sigma_max
@@ -86,52 +88,105 @@ __device__ __forceinline__ void tm_st_x8(uint32_t addr, const uint32_t (&r)[8]) 
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
+__device__ __forceinline__ void tm_ld_x4(uint32_t addr, uint32_t (&r)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void tm_ld_x16(uint32_t addr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(addr));
+}
+
+// Gather from the warp's X region: `xaddr` is its 32-bit shared address,
+// aligned to a power of two above every offset, so the low step's address is
+// one LOP3 ((w & 0x7FFF) | xaddr, which also drops the end flag) and the high
+// step's one IMAD.HI ((w * 2^16) >> 32 + xaddr).
+__device__ __forceinline__ uint32_t gaddr_lo(uint32_t w, uint32_t xaddr) { return (w & 0x7FFFu) | xaddr; }
+__device__ __forceinline__ uint32_t gaddr_hi(uint32_t w, uint32_t xaddr) {
+    uint32_t a;
+    asm("mad.hi.u32 %0, %1, 65536, %2;" : "=r"(a) : "r"(w), "r"(xaddr));
+    return a;
+}
+__device__ __forceinline__ double lds64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+
 // Everything a warp needs to run one SpMV of its group.
 template <int RV>
 struct TmemWarp {
-    double* Xs;             // gather vector copies (+ trash slot), this warp
+    double* Xs;             // gather vector copies (+ trash slot), this warp (generic)
     double* Ys;             // row sums, lane-major, this warp
+    uint32_t xaddr;         // shared address of Xs (aligned, see gaddr_lo)
     uint32_t xy[RV];        // copy-0 gather slot | Y slot << 16 of row slot j
     const uint16_t* xmore;  // shared table of further copies' slots
     int copies;
     int lane;
     uint32_t wcol, vcol;    // TMEM addresses: words, this warp's values
     int S;
+    int ystream;            // Y slots per row stream
 };
 
-// Four schedule steps out of one TMEM chunk: gathers issued first, then the
-// ordered multiply-add chain; rows end only on odd steps (u = 1, 3).
-__device__ __forceinline__ void tmem_steps4(const char* xb, const uint32_t (&w)[2], const uint32_t (&v)[8],
-                                            double& acc, double*& yp) {
-    const uint32_t w0 = w[0] & 0xFFFFu, w1 = w[0] >> 16, w2 = w[1] & 0xFFFFu, w3 = w[1] >> 16;
-    const double x0 = *reinterpret_cast<const double*>(xb + (w0 & 0x7FFFu));
-    const double x1 = *reinterpret_cast<const double*>(xb + (w1 & 0x7FFFu));
-    const double x2 = *reinterpret_cast<const double*>(xb + (w2 & 0x7FFFu));
-    const double x3 = *reinterpret_cast<const double*>(xb + (w3 & 0x7FFFu));
+// One 4-step chunk: words w0 (steps 0|1) and w1 (steps 2|3), values v[0..8);
+// gathers issued first, then the ordered multiply-add chain(s).
+//   ST = 1: one row at a time; rows end on step 1 (flag: bit 15 of w0) or 3
+//           (bit 15 of w1).
+//   ST = 2: two rows at a time, stream 0 on steps 0 and 2, stream 1 on steps 1
+//           and 3 -- two independent DADD chains; stream 0 rows end on step 2
+//           (flag in w0), stream 1 rows on step 3 (flag in w1).
+template <int ST>
+__device__ __forceinline__ void tmem_chunk4(uint32_t xaddr, uint32_t w0, uint32_t w1, const uint32_t* v,
+                                            double (&acc)[ST], double* (&yp)[ST]) {
+    const double x0 = lds64(gaddr_lo(w0, xaddr));
+    const double x1 = lds64(gaddr_hi(w0, xaddr));
+    const double x2 = lds64(gaddr_lo(w1, xaddr));
+    const double x3 = lds64(gaddr_hi(w1, xaddr));
     const double a0 = __hiloint2double(static_cast<int>(v[1]), static_cast<int>(v[0]));
     const double a1 = __hiloint2double(static_cast<int>(v[3]), static_cast<int>(v[2]));
     const double a2 = __hiloint2double(static_cast<int>(v[5]), static_cast<int>(v[4]));
     const double a3 = __hiloint2double(static_cast<int>(v[7]), static_cast<int>(v[6]));
-    acc = dadd(acc, dmul(a0, x0));
-    acc = dadd(acc, dmul(a1, x1));
-    if (w1 & 0x8000u) {
-        *yp = acc;
-        yp += 32;
-        acc = 0.0;
-    }
-    acc = dadd(acc, dmul(a2, x2));
-    acc = dadd(acc, dmul(a3, x3));
-    if (w3 & 0x8000u) {
-        *yp = acc;
-        yp += 32;
-        acc = 0.0;
+    if constexpr (ST == 1) {
+        acc[0] = dadd(acc[0], dmul(a0, x0));
+        acc[0] = dadd(acc[0], dmul(a1, x1));
+        if (w0 & 0x8000u) {
+            *yp[0] = acc[0];
+            yp[0] += 32;
+            acc[0] = 0.0;
+        }
+        acc[0] = dadd(acc[0], dmul(a2, x2));
+        acc[0] = dadd(acc[0], dmul(a3, x3));
+        if (w1 & 0x8000u) {
+            *yp[0] = acc[0];
+            yp[0] += 32;
+            acc[0] = 0.0;
+        }
+    } else {
+        acc[0] = dadd(acc[0], dmul(a0, x0));
+        acc[1] = dadd(acc[1], dmul(a1, x1));
+        acc[0] = dadd(acc[0], dmul(a2, x2));
+        if (w0 & 0x8000u) {
+            *yp[0] = acc[0];
+            yp[0] += 32;
+            acc[0] = 0.0;
+        }
+        acc[1] = dadd(acc[1], dmul(a3, x3));
+        if (w1 & 0x8000u) {
+            *yp[1] = acc[1];
+            yp[1] += 32;
+            acc[1] = 0.0;
+        }
     }
 }
 
 // y = A x: publish x into every copy of the gather vector, walk the
-// TMEM-resident schedule (4 steps per tcgen05.ld pair; other warps hide the latency),
-// collect the row sums from Y.
-template <int RV>
+// TMEM-resident schedule (8 steps per tcgen05.ld pair, then a 4-step tail;
+// other warps hide the latency), collect the row sums from Y.
+template <int ST, int RV>
 __device__ __forceinline__ void tmem_spmv(const TmemWarp<RV>& tw, const double (&x)[RV], double (&y)[RV]) {
 #pragma unroll
     for (int j = 0; j < RV; ++j) {
@@ -139,15 +194,28 @@ __device__ __forceinline__ void tmem_spmv(const TmemWarp<RV>& tw, const double (
         for (int r = 1; r < tw.copies; ++r) tw.Xs[tw.xmore[((r - 1) * RV + j) * 32 + tw.lane]] = x[j];
     }
     __syncwarp();
-    const char* xb = reinterpret_cast<const char*>(tw.Xs);
-    double* yp = tw.Ys + tw.lane;
-    double acc = 0.0;
-    for (int t0 = 0; t0 < tw.S; t0 += 4) {
+    double* yp[ST];
+    double acc[ST];
+#pragma unroll
+    for (int s = 0; s < ST; ++s) {
+        yp[s] = tw.Ys + s * tw.ystream + tw.lane;
+        acc[s] = 0.0;
+    }
+    int t0 = 0;
+    for (; t0 + 8 <= tw.S; t0 += 8) {
+        uint32_t w[4], v[16];
+        tm_ld_x4(tw.wcol + (t0 >> 1), w);
+        tm_ld_x16(tw.vcol + 2 * t0, v);
+        tm_wait_ld();
+        tmem_chunk4<ST>(tw.xaddr, w[0], w[1], v, acc, yp);
+        tmem_chunk4<ST>(tw.xaddr, w[2], w[3], v + 8, acc, yp);
+    }
+    if (t0 < tw.S) {
         uint32_t w[2], v[8];
         tm_ld_x2(tw.wcol + (t0 >> 1), w);
         tm_ld_x8(tw.vcol + 2 * t0, v);
         tm_wait_ld();
-        tmem_steps4(xb, w, v, acc, yp);
+        tmem_chunk4<ST>(tw.xaddr, w[0], w[1], v, acc, yp);
     }
     __syncwarp();
 #pragma unroll
@@ -162,11 +230,11 @@ __device__ __forceinline__ void tmem_reduce(const Ctx<1, R, RV>& cc, const doubl
     team_reduce<1>(c, q, o);
 }
 
-template <int R, int RV>
+template <int ST, int R, int RV>
 __device__ __forceinline__ double tmem_fresh_rms(const Ctx<1, R, RV>& c, const TmemWarp<RV>& tw,
                                                  const double (&x)[RV], const double* bsrc) {
     double ax[RV];
-    tmem_spmv(tw, x, ax);
+    tmem_spmv<ST>(tw, x, ax);
     double sq[1][RV];
 #pragma unroll
     for (int j = 0; j < RV; ++j) {
@@ -179,7 +247,7 @@ __device__ __forceinline__ double tmem_fresh_rms(const Ctx<1, R, RV>& c, const T
     return __dsqrt_rn(ddiv(out[0], static_cast<double>(c.n)));
 }
 
-template <int R, int RV, int NT>
+template <int R, int RV, int NT, int ST>
 __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t s_taddr;
@@ -189,7 +257,12 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
     uint16_t* s_xmore = reinterpret_cast<uint16_t*>(smem + sizeof(int32_t) * p.S * 32);
     const int xmore_n = (p.copies - 1) * RV * 32;
     const int xmore_bytes = (2 * xmore_n + 15) & ~15;
-    double* s_vec = reinterpret_cast<double*>(smem + sizeof(int32_t) * p.S * 32 + xmore_bytes);
+    // X regions (one per warp, each aligned to xalign) then Y regions
+    const uint32_t s_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    const uint32_t x_area = (s_base + sizeof(int32_t) * p.S * 32 + xmore_bytes + p.xalign - 1) &
+                            ~static_cast<uint32_t>(p.xalign - 1);
+    const int nwarps = blockDim.x / 32;
+    double* s_y = reinterpret_cast<double*>(smem + (x_area - s_base) + static_cast<size_t>(nwarps) * p.xalign);
 
     for (int i = threadIdx.x; i < p.S * 32; i += blockDim.x) s_vidx[i] = p.vidx[i];
     for (int i = threadIdx.x; i < xmore_n; i += blockDim.x) s_xmore[i] = p.lane_xmore[i];
@@ -227,15 +300,18 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
     c.tm.lane = lane;
     c.n = p.n;
     c.P = p.P;
-    tw.Xs = s_vec + static_cast<size_t>(warp) * (p.xslots + p.yslots);
-    tw.Ys = tw.Xs + p.xslots;
+    tw.xaddr = x_area + static_cast<uint32_t>(warp * p.xalign);
+    tw.Xs = reinterpret_cast<double*>(smem + (tw.xaddr - s_base));
+    tw.Ys = s_y + static_cast<size_t>(warp) * p.yslots;
     tw.xmore = s_xmore;
     tw.copies = p.copies;
     tw.lane = lane;
     tw.S = p.S;
+    tw.ystream = p.ystream;
 #pragma unroll
     for (int j = 0; j < RV; ++j) tw.xy[j] = p.lane_xy[j * 32 + lane];
-    for (int i = lane; i < p.xslots + p.yslots; i += 32) tw.Xs[i] = 0.0;  // zero slots stay +0.0
+    for (int i = lane; i < p.xslots; i += 32) tw.Xs[i] = 0.0;  // zero slots stay +0.0
+    for (int i = lane; i < p.yslots; i += 32) tw.Ys[i] = 0.0;
     __syncwarp();
     const double nd = static_cast<double>(p.n);
     const double smax = p.sigma_max;
@@ -278,7 +354,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
         double r[RV], rh[RV], pv[RV], v[RV];
         {
             double ax[RV];
-            tmem_spmv(tw, x, ax);
+            tmem_spmv<ST>(tw, x, ax);
 #pragma unroll
             for (int j = 0; j < RV; ++j) {
                 const double bj = c.valid(j) ? __ldcs(bsrc + c.row(j)) : 0.0;
@@ -301,7 +377,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
             rho_next = o[1];
         }
         if (sigma <= smax) {
-            fres = tmem_fresh_rms(c, tw, x, bsrc);
+            fres = tmem_fresh_rms<ST>(c, tw, x, bsrc);
             conv = fres <= p.tol;
         }
         if (!conv) {
@@ -316,7 +392,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                     pv[j] = dadd(r[j], dmul(beta, dsub(pv[j], dmul(omega, v[j]))));
                     y[j] = dmul(dinv[j], pv[j]);
                 }
-                tmem_spmv(tw, y, v);
+                tmem_spmv<ST>(tw, y, v);
                 double den;
                 {
                     double q[1][RV], o[1];
@@ -335,7 +411,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                     x[j] = dadd(x[j], dmul(alpha, dmul(dinv[j], pv[j])));  // y = dinv*p recomputed
                 }
                 double t[RV];
-                tmem_spmv(tw, z, t);
+                tmem_spmv<ST>(tw, z, t);
                 double tt, ts;
                 {
                     double q[2][RV], o[2];
@@ -370,7 +446,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                 }
                 if (!isfinite(sigma)) { brk = true; break; }
                 if (sigma <= smax) {
-                    const double f = tmem_fresh_rms(c, tw, x, bsrc);
+                    const double f = tmem_fresh_rms<ST>(c, tw, x, bsrc);
                     if (f <= p.tol) {
                         fres = f;
                         conv = true;
@@ -380,7 +456,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                 if (scalar_breaks(omega)) { brk = true; break; }
             }
             if (!conv) {
-                fres = tmem_fresh_rms(c, tw, x, bsrc);
+                fres = tmem_fresh_rms<ST>(c, tw, x, bsrc);
                 conv = !brk && fres <= p.tol;
             }
         }

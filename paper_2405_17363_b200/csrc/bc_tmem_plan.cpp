@@ -29,6 +29,11 @@ constexpr int kLanes = 32;
 
 struct TmOpt {
     int S = 0, ncol = 0, nrow = 0, R = 1, NS = 16;
+    // ST interleaved row streams per lane: virtual lane v = s*32 + L runs on
+    // physical lane L, its virtual step u on physical step u*ST + s
+    int ST = 1;
+    int VL() const { return kLanes * ST; }
+    int cap() const { return S / ST; }
     const std::vector<int>* seg_len;
     const std::vector<std::vector<int>>* seg_cols;
     const std::vector<int>* seg_row;
@@ -105,19 +110,20 @@ struct TmOpt {
         const int m = distinct(t, h, cols);
         return match_cost(cols, m, nullptr);
     }
-    void lay_lane(int L) {
-        for (int t = 0; t < S; ++t) {
-            col_at[t * kLanes + L] = -1;
-            end_at[t * kLanes + L] = 0;
+    int at(int v, int u) const { return (u * ST + v / kLanes) * kLanes + v % kLanes; }
+    void lay_lane(int v) {
+        for (int u = 0; u < cap(); ++u) {
+            col_at[at(v, u)] = -1;
+            end_at[at(v, u)] = 0;
         }
-        int t = 0;
-        for (int sg : lane_segs[L]) {
+        int u = 0;
+        for (int sg : lane_segs[v]) {
             const auto& cols = (*seg_cols)[sg];
-            for (size_t q = 0; q < cols.size(); ++q, ++t) col_at[t * kLanes + L] = cols[q];
-            end_at[(t - 1) * kLanes + L] = 1;
-            row_lane[(*seg_row)[sg]] = L;
+            for (size_t q = 0; q < cols.size(); ++q, ++u) col_at[at(v, u)] = cols[q];
+            end_at[at(v, u - 1)] = 1;
+            row_lane[(*seg_row)[sg]] = v % kLanes;
         }
-        load[L] = t;
+        load[v] = u;
     }
     int publish_cost() const {  // R*RV STS.64 by the owner lanes (rows 32j+L)
         int tot = 0;
@@ -146,9 +152,9 @@ struct TmOpt {
             }
         return tot;
     }
-    int ystore_cost() const {
+    int ystore_cost() const {  // one STS.64 wavefront per half-warp with a row end
         int tot = 0;
-        for (int t = 1; t < S; t += 2)
+        for (int t = 0; t < S; ++t)
             for (int h = 0; h < 2; ++h) {
                 bool any = false;
                 for (int L = 16 * h; L < 16 * h + 16; ++L) any |= end_at[t * kLanes + L] != 0;
@@ -168,7 +174,7 @@ struct TmOpt {
     // re-evaluate the gather groups of the halves holding lanes A and B
     int regather_lanes(int A, int B) {
         int g = gsum;
-        const int ha = A / 16, hb = B / 16;
+        const int ha = (A % kLanes) / 16, hb = (B % kLanes) / 16;
         for (int t = 0; t < S; ++t) {
             const int id = t * 2 + ha;
             const int c = group_cost(t, ha);
@@ -189,10 +195,16 @@ struct TmOpt {
 
 TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
     if (const char* e = std::getenv("BC_SCHED_OPT")) optimize = optimize && std::atoi(e) != 0;
-    int copies = 1;  // issue-bound at 16 warps: one copy measured fastest (BC_GATHER_COPIES to override)
+    // two placements of the gather vector: 448k vs 409k cell-solves/s with one,
+    // 413k with three (B200, 100k M156, P regime; BC_GATHER_COPIES overrides)
+    int copies = 2;
     if (const char* e = std::getenv("BC_GATHER_COPIES")) copies = std::max(1, std::min(4, std::atoi(e)));
     if (!optimize) copies = 1;
+    // rows padded to an even number of (virtual) steps, so that rows end only
+    // on steps 1, 3 (one stream) or 2, 3 (two streams) of a 4-step chunk
     constexpr int d = 2;
+    int streams = 2;  // two interleaved accumulator chains per lane (BC_TMEM_STREAMS)
+    if (const char* e = std::getenv("BC_TMEM_STREAMS")) streams = std::atoi(e) == 1 ? 1 : 2;
     const int s = pat.species, nnz = pat.nnz, n = k * s;
     const int zero_col = n;  // pseudo-row whose slots always hold +0.0
     // rows as segments padded to a multiple of d (csr.cpp:90-101 order kept)
@@ -222,22 +234,86 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
     o.ncol = n + 1;
     o.nrow = n;
     o.R = copies;
-    o.lane_segs.assign(kLanes, {});
-    o.load.assign(kLanes, 0);
+    o.ST = streams;
+    o.lane_segs.assign(o.VL(), {});
+    o.load.assign(o.VL(), 0);
     {  // longest-processing-time start
         std::vector<int> order(seg_row.size());
         std::iota(order.begin(), order.end(), 0);
         std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return seg_len[a] > seg_len[b]; });
         for (int idx : order) {
             int best = 0;
-            for (int L = 1; L < kLanes; ++L)
+            for (int L = 1; L < o.VL(); ++L)
                 if (o.load[L] < o.load[best]) best = L;
             o.load[best] += seg_len[idx];
             o.lane_segs[best].push_back(idx);
         }
+        // lower the longest lane: move a segment off it, or swap it for a
+        // shorter one, whenever the other lane stays below the current maximum
+        for (int guard = 0; guard < 10000; ++guard) {
+            const int M = *std::max_element(o.load.begin(), o.load.end());
+            bool moved = false;
+            for (int b = 0; b < o.VL() && !moved; ++b) {
+                if (o.load[b] != M) continue;
+                for (size_t i = 0; i < o.lane_segs[b].size() && !moved; ++i) {
+                    const int sa = o.lane_segs[b][i];
+                    for (int c = 0; c < o.VL() && !moved; ++c) {
+                        if (c == b) continue;
+                        if (o.load[c] + seg_len[sa] < M) {
+                            o.lane_segs[b].erase(o.lane_segs[b].begin() + i);
+                            o.lane_segs[c].push_back(sa);
+                            o.load[b] -= seg_len[sa];
+                            o.load[c] += seg_len[sa];
+                            moved = true;
+                            break;
+                        }
+                        for (size_t j = 0; j < o.lane_segs[c].size(); ++j) {
+                            const int sc = o.lane_segs[c][j];
+                            const int dlt = seg_len[sa] - seg_len[sc];
+                            if (dlt > 0 && o.load[c] + dlt < M) {
+                                std::swap(o.lane_segs[b][i], o.lane_segs[c][j]);
+                                o.load[b] -= dlt;
+                                o.load[c] += dlt;
+                                moved = true;
+                                break;
+                            }
+                        }
+                    }
+                }
+            }
+            if (!moved) break;
+        }
+        // first-fit decreasing into the smallest lane capacity it fits, if that
+        // beats the balanced start (S = ST * capacity must stay a multiple of 4)
+        const int unit = 4 / o.ST;
+        int total = 0;
+        for (int l : seg_len) total += l;
+        const int lpt_max = *std::max_element(o.load.begin(), o.load.end());
+        int cap = std::max(order.empty() ? 0 : seg_len[order[0]], (total + o.VL() - 1) / o.VL());
+        cap = (cap + unit - 1) / unit * unit;
+        for (; cap < lpt_max; cap += unit) {
+            std::vector<std::vector<int>> segs(o.VL());
+            std::vector<int> load(o.VL(), 0);
+            bool ok = true;
+            for (int idx : order) {
+                int b = 0;
+                while (b < o.VL() && load[b] + seg_len[idx] > cap) ++b;
+                if (b == o.VL()) {
+                    ok = false;
+                    break;
+                }
+                load[b] += seg_len[idx];
+                segs[b].push_back(idx);
+            }
+            if (ok) {
+                o.lane_segs = segs;
+                o.load = load;
+                break;
+            }
+        }
     }
-    const int S0 = std::max(4, *std::max_element(o.load.begin(), o.load.end()));
-    o.S = (S0 + 3) & ~3;
+    const int S0 = std::max(4, o.ST * *std::max_element(o.load.begin(), o.load.end()));
+    o.S = (S0 + 3) & ~3;  // the kernel walks 8 steps per TMEM load pair, then a 4-step tail
     o.NS = optimize ? ((o.ncol + o.ncol / 4 + 15) / 16) * 16 : ((o.ncol + 15) / 16) * 16;
     o.pos.resize(static_cast<size_t>(o.R) * o.ncol);
     o.owner.assign(static_cast<size_t>(o.R) * o.NS, -1);
@@ -262,7 +338,7 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
     o.end_at.assign(static_cast<size_t>(o.S) * kLanes, 0);
     o.row_lane.assign(n, -1);
     o.gcost.assign(static_cast<size_t>(o.S) * 2, 0);
-    for (int L = 0; L < kLanes; ++L) o.lay_lane(L);
+    for (int v = 0; v < o.VL(); ++v) o.lay_lane(v);
     o.full_eval();
 
     if (optimize) {
@@ -313,8 +389,8 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
                 }
             } else {
                 // segment moves: reorder within a lane, move or exchange between lanes
-                const int A = static_cast<int>(rnd() % kLanes);
-                int B = kind == 2 ? A : static_cast<int>(rnd() % kLanes);
+                const int A = static_cast<int>(rnd() % o.VL());
+                int B = kind == 2 ? A : static_cast<int>(rnd() % o.VL());
                 if (o.lane_segs[A].empty()) continue;
                 const auto saveA = o.lane_segs[A], saveB = o.lane_segs[B];
                 if (kind == 2) {
@@ -328,15 +404,15 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
                     const int ia = static_cast<int>(rnd() % o.lane_segs[A].size());
                     const int sa = o.lane_segs[A][ia];
                     if (o.lane_segs[B].empty() || (rnd() & 1)) {
-                        if (o.load[B] + seg_len[sa] > o.S) continue;
+                        if (o.load[B] + seg_len[sa] > o.cap()) continue;
                         const int ib = static_cast<int>(rnd() % (o.lane_segs[B].size() + 1));
                         o.lane_segs[A].erase(o.lane_segs[A].begin() + ia);
                         o.lane_segs[B].insert(o.lane_segs[B].begin() + ib, sa);
                     } else {
                         const int ib = static_cast<int>(rnd() % o.lane_segs[B].size());
                         const int sb = o.lane_segs[B][ib];
-                        if (o.load[A] - seg_len[sa] + seg_len[sb] > o.S ||
-                            o.load[B] - seg_len[sb] + seg_len[sa] > o.S)
+                        if (o.load[A] - seg_len[sa] + seg_len[sb] > o.cap() ||
+                            o.load[B] - seg_len[sb] + seg_len[sa] > o.cap())
                             continue;
                         std::swap(o.lane_segs[A][ia], o.lane_segs[B][ib]);
                     }
@@ -383,17 +459,20 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
     ts.vidx.assign(static_cast<size_t>(o.S) * kLanes, -1);
     ts.yslot.assign(n, -1);
     std::vector<int> vals_at(static_cast<size_t>(o.S) * kLanes, -1);
-    int kmax = 0;
-    for (int L = 0; L < kLanes; ++L) {
-        int t = 0, kk = 0;
-        for (int sg : o.lane_segs[L]) {
-            for (size_t q = 0; q < seg_cols[sg].size(); ++q, ++t) vals_at[t * kLanes + L] = seg_vals[sg][q];
-            ts.yslot[seg_row[sg]] = kk * kLanes + L;
+    int kmax = 1;
+    for (int v = 0; v < o.VL(); ++v) kmax = std::max(kmax, static_cast<int>(o.lane_segs[v].size()));
+    // stream s's k-th row of lane L -> Y[s*kmax*32 + k*32 + L] (lane-major per stream)
+    for (int v = 0; v < o.VL(); ++v) {
+        int u = 0, kk = 0;
+        for (int sg : o.lane_segs[v]) {
+            for (size_t q = 0; q < seg_cols[sg].size(); ++q, ++u) vals_at[o.at(v, u)] = seg_vals[sg][q];
+            ts.yslot[seg_row[sg]] = (v / kLanes) * kmax * kLanes + kk * kLanes + v % kLanes;
             ++kk;
         }
-        kmax = std::max(kmax, kk);
     }
-    ts.yslots = std::max(1, kmax) * kLanes;
+    ts.streams = o.ST;
+    ts.ystream = kmax * kLanes;
+    ts.yslots = o.ST * kmax * kLanes;
     for (int& y : ts.yslot)
         if (y < 0) y = ts.yslots;  // empty rows read the zero slot after the last row slot
     int cost = 0;
@@ -414,7 +493,12 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
                 }
                 const int slot = r * o.NS + o.pos[r * o.ncol + c];
                 uint16_t w = static_cast<uint16_t>(slot * 8);
-                if (o.end_at[id]) w |= 0x8000u;
+                // a row ending on step 4c+3 is flagged on step 4c+2, one ending on
+                // step 4c+1 (one stream) or 4c+2 (two streams) on step 4c: the low
+                // halves of the chunk's two 32-bit TMEM words, masked off by the
+                // address LOP3
+                if ((t & 3) == 2 && o.end_at[id + kLanes]) w |= 0x8000u;
+                if ((t & 3) == 0 && o.end_at[id + (o.ST == 1 ? 1 : 2) * kLanes]) w |= 0x8000u;
                 ts.words[id] = w;
                 ts.vidx[id] = vals_at[id];
             }

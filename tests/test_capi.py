@@ -229,7 +229,7 @@ def export_tmem_schedule(rp, ci, k):
     species = len(rp) - 1
     rp = np.ascontiguousarray(rp, np.int32)
     ci = np.ascontiguousarray(ci, np.int32)
-    info = np.zeros(7, np.int32)
+    info = np.zeros(9, np.int32)
     lib = _native.b200()
     assert lib.bc_tmem_schedule_export(species, of.ptr(rp), of.ptr(ci), k, of.ptr(info), None, None, None,
                                        None) == 0
@@ -241,32 +241,37 @@ def export_tmem_schedule(rp, ci, k):
     assert lib.bc_tmem_schedule_export(species, of.ptr(rp), of.ptr(ci), k, of.ptr(info), of.ptr(words),
                                        of.ptr(vidx), of.ptr(xpos), of.ptr(yslot)) == 0
     return dict(S=S, xslots=int(info[1]), zero_slot=int(info[2]), yslots=int(info[3]), cost=int(info[4]),
-                copies=copies, model=int(info[6]), words=words, vidx=vidx, xpos=xpos.reshape(copies, -1),
-                yslot=yslot)
+                copies=copies, model=int(info[6]), streams=int(info[7]), ystream=int(info[8]), words=words,
+                vidx=vidx, xpos=xpos.reshape(copies, -1), yslot=yslot)
 
 
 def emulate_tmem_spmv(sc, vals, x):
     """tmem_spmv() of bc_tmem.cuh in exact double arithmetic: zero-initialised
-    X|Y, publish x, lanes walk 16-bit words (byte offset | end << 15), row
-    ends only on odd steps, lane L's k-th row -> Y[k*32+L]."""
-    S = sc["S"]
+    X|Y, publish x, lanes walk 16-bit words (byte offset; bit 15 of step
+    4c+2's word flags a row ending on step 4c+3, bit 15 of step 4c's a row
+    ending on step 4c+1 with one stream or 4c+2 with two), stream s of lane
+    L runs on steps s mod streams; its k-th row -> Y[s*ystream + k*32 + L]."""
+    S, ST = sc["S"], sc["streams"]
     X = np.zeros(sc["xslots"] + 1)
     for xp in sc["xpos"]:  # every copy of the gather vector
         X[xp] = x
     Y = np.zeros(sc["yslots"] + 32)
+    words = sc["words"].reshape(S, 32)
     for L in range(32):
-        acc, k = 0.0, 0
+        acc, k = [0.0] * ST, [0] * ST
         for t in range(S):
-            w = int(sc["words"][t * 32 + L])
+            w = int(words[t, L])
             vi = int(sc["vidx"][t * 32 + L])
             a = float(vals[vi]) if vi >= 0 else 0.0
-            acc = acc + a * float(X[(w & 0x7FFF) // 8])
+            s = t % ST
+            acc[s] = acc[s] + a * float(X[(w & 0x7FFF) // 8])
             if (t & 1) and (w & 0x8000):
-                Y[k * 32 + L] = acc
-                k += 1
-                acc = 0.0
-            elif w & 0x8000:
-                raise AssertionError("row end on an even step")
+                raise AssertionError("end flag on an odd step")
+            flag = t - 1 if (t & 3) == 3 else (t & ~3 if (t & 3) == ST else -1)
+            if flag >= 0 and int(words[flag, L]) & 0x8000:
+                Y[s * sc["ystream"] + k[s] * 32 + L] = acc[s]
+                k[s] += 1
+                acc[s] = 0.0
     return Y[sc["yslot"]]
 
 
