@@ -256,23 +256,26 @@ LaunchShape choose_shape(bc_ctx* ctx, BlockFn fn, const bc::GroupPlan& gp, bool 
 using TmemFn = void (*)(bc::TmemParams);
 
 struct TmemCfg {
-    int R, RV, warps, ST;  // warps per CTA (= 4 * groups per lane quarter), row streams per lane
+    int R, RV, warps, ST, CP;  // warps per CTA (= 4 * groups per lane quarter), row streams, gather copies
     TmemFn fn;
 };
 
-// 16 warps/SM at <= 128 registers, or 12 warps/SM at <= 168 registers; 8
-// warps (<= 255 registers) for schedules too long for 3 groups per quarter
-// (the scaled mechanism: 312 species).  Each with one or two row streams.
-#define BC_TMEM_CFG(R, RV, W)                                                   \
-    {R, RV, W, 1, &bc::block_cells_tmem_kernel<R, RV, 32 * W, 1>},              \
-    {                                                                           \
-        R, RV, W, 2, &bc::block_cells_tmem_kernel<R, RV, 32 * W, 2>             \
-    }
+// 16 warps/SM at <= 128 registers; 8 warps (<= 255 registers) for schedules
+// too long for 3 groups per quarter (the scaled mechanism: 312 species).
+// Each with one or two row streams and one or two gather-vector copies.
+#define BC_TMEM_CFG1(R, RV, W, ST, CP) \
+    { R, RV, W, ST, CP, &bc::block_cells_tmem_kernel<R, RV, 32 * W, ST, CP> }
+#define BC_TMEM_CFG(R, RV, W)                                                                  \
+    BC_TMEM_CFG1(R, RV, W, 1, 1), BC_TMEM_CFG1(R, RV, W, 1, 2), BC_TMEM_CFG1(R, RV, W, 2, 1), \
+        BC_TMEM_CFG1(R, RV, W, 2, 2)
 const TmemCfg kTmemConfigs[] = {
-    BC_TMEM_CFG(8, 5, 16), BC_TMEM_CFG(8, 5, 12), BC_TMEM_CFG(8, 8, 16),   BC_TMEM_CFG(8, 8, 12),
-    BC_TMEM_CFG(4, 4, 16), BC_TMEM_CFG(4, 4, 12), BC_TMEM_CFG(16, 10, 8), BC_TMEM_CFG(16, 16, 8),
+    BC_TMEM_CFG(8, 5, 16),
+    BC_TMEM_CFG(8, 8, 16),
+    BC_TMEM_CFG(4, 4, 16),
+    BC_TMEM_CFG(16, 10, 8),
 };
 #undef BC_TMEM_CFG
+#undef BC_TMEM_CFG1
 
 int tmem_warps_pref() {
     const char* e = std::getenv("BC_TMEM_WARPS");
@@ -318,25 +321,25 @@ void ensure_tmem_schedule(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp
 }
 
 // Per-lane owner tables for a kernel instance with RV row slots: copy-0
-// gather slot | Y slot << 16, and the further copies' slots; rows >= n go to
-// the trash slot (after every copy) and read the zero Y slot.
+// gather slot | Y slot << 16, and copy 1's slots two row slots per word; rows
+// >= n go to the trash slot (after every copy) and read the zero Y slot.
 void ensure_tmem_lane_tables(bc_ctx* ctx, bc::GroupPlan& gp, int RV) {
     if (gp.tm_lane_rv == RV) return;
-    const int n = gp.geo.n, R = gp.tm.copies, trash = gp.tm.xslots;
+    const int n = gp.geo.n, trash = gp.tm.xslots;
     std::vector<uint32_t> xy(static_cast<size_t>(RV) * 32);
-    std::vector<uint16_t> xmore(static_cast<size_t>(std::max(1, R - 1)) * RV * 32, static_cast<uint16_t>(trash));
+    std::vector<uint32_t> x1(static_cast<size_t>((RV + 1) / 2) * 32, 0u);
     for (int j = 0; j < RV; ++j)
         for (int l = 0; l < 32; ++l) {
             const int row = j * 32 + l;
             const bool ok = row < n;
             xy[j * 32 + l] = static_cast<uint32_t>(ok ? gp.tm.xpos[row] : trash) |
                              (static_cast<uint32_t>(ok ? gp.tm.yslot[row] : gp.tm.yslots) << 16);
-            for (int r = 1; r < R; ++r)
-                xmore[((r - 1) * RV + j) * 32 + l] =
-                    static_cast<uint16_t>(ok ? gp.tm.xpos[static_cast<size_t>(r) * n + row] : trash);
+            const uint32_t s1 =
+                static_cast<uint32_t>(ok && gp.tm.copies > 1 ? gp.tm.xpos[static_cast<size_t>(n) + row] : trash);
+            x1[(j / 2) * 32 + l] |= s1 << (16 * (j % 2));
         }
     gp.d_tm_lane_xy = upload(ctx, xy);
-    gp.d_tm_lane_xmore = upload(ctx, xmore);
+    gp.d_tm_lane_x1 = upload(ctx, x1);
     gp.tm_lane_rv = RV;
 }
 
@@ -352,7 +355,9 @@ const TmemCfg* pick_tmem_cfg(const bc::GroupPlan& gp) {
     const int want = std::min(4 * cpq, tmem_warps_pref());
     const TmemCfg* cfg = nullptr;
     for (const TmemCfg& t : kTmemConfigs) {
-        if (t.R != gp.geo.R || t.RV < gp.geo.RV || t.warps < want || t.ST != gp.tm.streams) continue;
+        if (t.R != gp.geo.R || t.RV < gp.geo.RV || t.warps < want || t.ST != gp.tm.streams ||
+            t.CP != gp.tm.copies)
+            continue;
         if (!cfg || t.warps < cfg->warps || (t.warps == cfg->warps && t.RV < cfg->RV)) cfg = &t;
     }
     return cfg;
@@ -371,8 +376,7 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
     const int warps = 4 * cpq;
     const int xslots = (gp.tm.xslots + 1 + 31) & ~31, yslots = gp.tm.yslots + 32;
     const int xalign = static_cast<int>(bc::padded_len(8 * xslots));
-    const size_t xmore_bytes = ((2 * (gp.tm.copies - 1) * cfg->RV * 32) + 15) & ~15;
-    const size_t smem = sizeof(int32_t) * S * 32 + xmore_bytes + static_cast<size_t>(xalign) * (warps + 1) +
+    const size_t smem = sizeof(int32_t) * S * 32 + static_cast<size_t>(xalign) * (warps + 1) +
                         sizeof(double) * warps * yslots;
     if (smem > static_cast<size_t>(kMaxDynSmem - 1024)) return false;
     if (!ctx->smem_set[reinterpret_cast<BlockFn>(cfg->fn)]) {
@@ -391,7 +395,7 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
     p.vidx = gp.d_tm_vidx;
     p.didx = gp.d_didx;
     p.lane_xy = gp.d_tm_lane_xy;
-    p.lane_xmore = gp.d_tm_lane_xmore;
+    p.lane_x1 = gp.d_tm_lane_x1;
     p.counter = counter;
     p.cell_offset = cell0;
     p.group_offset = gout0;
@@ -406,7 +410,6 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
     p.yslots = yslots;
     p.xalign = xalign;
     p.ystream = gp.tm.ystream;
-    p.copies = gp.tm.copies;
     p.cells_per_quarter = cpq;
     p.sigma_max = sigma_threshold(tol, gp.geo.n);
     p.tol = tol;

@@ -107,7 +107,7 @@ struct GroupPlan {
     int32_t* d_tm_vidx = nullptr;
     int tm_lane_rv = 0;               // RV the lane tables below were built for
     uint32_t* d_tm_lane_xy = nullptr;
-    uint16_t* d_tm_lane_xmore = nullptr;
+    uint32_t* d_tm_lane_x1 = nullptr;
 };
 
 TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize = true);

@@ -52,7 +52,7 @@ struct TmemParams {
     const int32_t* vidx;    // S * 32: group value index, -1 = padding (0.0)
     const int32_t* didx;    // n: group value index of the diagonal, -1 if none
     const uint32_t* lane_xy;  // RV * 32: copy-0 gather slot | Y slot << 16 per (slot j, lane)
-    const uint16_t* lane_xmore;  // (copies-1) * RV * 32: gather slots of further copies
+    const uint32_t* lane_x1;  // ((RV+1)/2) * 32: copy-1 gather slots, two row slots per word
     unsigned int* counter;
     int64_t cell_offset, group_offset;
     int group_count;
@@ -61,7 +61,6 @@ struct TmemParams {
     int xslots, yslots;     // shared doubles per warp: X | Y (multiples of 32)
     int xalign;             // bytes per warp X region: a power of two >= 8 * xslots
     int ystream;            // Y slots per row stream (TmemSchedule::ystream)
-    int copies;             // copies of the gather vector (1..4)
     int cells_per_quarter;  // warps per lane quarter
     double sigma_max;       // sqrt(sigma/n) <= tol  <=>  sigma <= sigma_max
     double tol;             // the fresh-residual test keeps the literal comparison
@@ -124,8 +123,7 @@ struct TmemWarp {
     double* Ys;             // row sums, lane-major, this warp
     uint32_t xaddr;         // shared address of Xs (aligned, see gaddr_lo)
     uint32_t xy[RV];        // copy-0 gather slot | Y slot << 16 of row slot j
-    const uint16_t* xmore;  // shared table of further copies' slots
-    int copies;
+    uint32_t x1[(RV + 1) / 2];  // copy-1 gather slots (CP = 2), row slots 2i | 2i+1 << 16
     int lane;
     uint32_t wcol, vcol;    // TMEM addresses: words, this warp's values
     int S;
@@ -186,12 +184,12 @@ __device__ __forceinline__ void tmem_chunk4(uint32_t xaddr, uint32_t w0, uint32_
 // y = A x: publish x into every copy of the gather vector, walk the
 // TMEM-resident schedule (8 steps per tcgen05.ld pair, then a 4-step tail;
 // other warps hide the latency), collect the row sums from Y.
-template <int ST, int RV>
+template <int ST, int CP, int RV>
 __device__ __forceinline__ void tmem_spmv(const TmemWarp<RV>& tw, const double (&x)[RV], double (&y)[RV]) {
 #pragma unroll
     for (int j = 0; j < RV; ++j) {
         tw.Xs[tw.xy[j] & 0xFFFFu] = x[j];
-        for (int r = 1; r < tw.copies; ++r) tw.Xs[tw.xmore[((r - 1) * RV + j) * 32 + tw.lane]] = x[j];
+        if constexpr (CP == 2) tw.Xs[(tw.x1[j >> 1] >> (16 * (j & 1))) & 0xFFFFu] = x[j];
     }
     __syncwarp();
     double* yp[ST];
@@ -222,19 +220,35 @@ __device__ __forceinline__ void tmem_spmv(const TmemWarp<RV>& tw, const double (
     for (int j = 0; j < RV; ++j) y[j] = tw.Ys[tw.xy[j] >> 16];
 }
 
-// Slot values of one reduction (team_reduce's contract: rows >= n are +0.0,
-// which holds here by the zero invariant).
-template <int R, int RV>
-__device__ __forceinline__ void tmem_reduce(const Ctx<1, R, RV>& cc, const double (&q)[1][RV], double (&o)[1]) {
-    Ctx<1, R, RV> c = cc;
-    team_reduce<1>(c, q, o);
+// Reduce NV values over the group: team_reduce<W = 1> with its
+// validity selects dropped -- rows >= n already hold +0.0 by the zero
+// invariant, exactly the value team_reduce substitutes -- and P = 32 * R >= 32
+// known at compile time: lane tree over R slots, then the xor butterfly.
+template <int NV, int R, int RV>
+__device__ __forceinline__ void tmem_reduce(const double (&vals)[NV][RV], double (&out)[NV]) {
+    static_assert(R >= 1 && RV <= R, "row slots beyond the tree");
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        double t[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) t[j] = j < RV ? vals[v][j < RV ? j : 0] : 0.0;
+#pragma unroll
+        for (int stride = R / 2; stride >= 1; stride /= 2)
+#pragma unroll
+            for (int j = 0; j < stride; ++j) t[j] = dadd(t[j], t[j + stride]);
+        out[v] = t[0];
+    }
+#pragma unroll
+    for (int mask = 16; mask >= 1; mask >>= 1)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) out[v] = dadd(out[v], __shfl_xor_sync(0xffffffffu, out[v], mask));
 }
 
-template <int ST, int R, int RV>
+template <int ST, int CP, int R, int RV>
 __device__ __forceinline__ double tmem_fresh_rms(const Ctx<1, R, RV>& c, const TmemWarp<RV>& tw,
                                                  const double (&x)[RV], const double* bsrc) {
     double ax[RV];
-    tmem_spmv<ST>(tw, x, ax);
+    tmem_spmv<ST, CP>(tw, x, ax);
     double sq[1][RV];
 #pragma unroll
     for (int j = 0; j < RV; ++j) {
@@ -243,29 +257,25 @@ __device__ __forceinline__ double tmem_fresh_rms(const Ctx<1, R, RV>& c, const T
         sq[0][j] = dmul(ri, ri);
     }
     double out[1];
-    tmem_reduce(c, sq, out);
+    tmem_reduce<1, R, RV>(sq, out);
     return __dsqrt_rn(ddiv(out[0], static_cast<double>(c.n)));
 }
 
-template <int R, int RV, int NT, int ST>
+template <int R, int RV, int NT, int ST, int CP>
 __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t s_taddr;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int quarter = warp % 4, slot = warp / 4;
     int32_t* s_vidx = reinterpret_cast<int32_t*>(smem);  // S*32
-    uint16_t* s_xmore = reinterpret_cast<uint16_t*>(smem + sizeof(int32_t) * p.S * 32);
-    const int xmore_n = (p.copies - 1) * RV * 32;
-    const int xmore_bytes = (2 * xmore_n + 15) & ~15;
     // X regions (one per warp, each aligned to xalign) then Y regions
     const uint32_t s_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-    const uint32_t x_area = (s_base + sizeof(int32_t) * p.S * 32 + xmore_bytes + p.xalign - 1) &
+    const uint32_t x_area = (s_base + sizeof(int32_t) * p.S * 32 + p.xalign - 1) &
                             ~static_cast<uint32_t>(p.xalign - 1);
     const int nwarps = blockDim.x / 32;
     double* s_y = reinterpret_cast<double*>(smem + (x_area - s_base) + static_cast<size_t>(nwarps) * p.xalign);
 
     for (int i = threadIdx.x; i < p.S * 32; i += blockDim.x) s_vidx[i] = p.vidx[i];
-    for (int i = threadIdx.x; i < xmore_n; i += blockDim.x) s_xmore[i] = p.lane_xmore[i];
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          static_cast<uint32_t>(__cvta_generic_to_shared(&s_taddr))),
@@ -303,13 +313,13 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
     tw.xaddr = x_area + static_cast<uint32_t>(warp * p.xalign);
     tw.Xs = reinterpret_cast<double*>(smem + (tw.xaddr - s_base));
     tw.Ys = s_y + static_cast<size_t>(warp) * p.yslots;
-    tw.xmore = s_xmore;
-    tw.copies = p.copies;
     tw.lane = lane;
     tw.S = p.S;
     tw.ystream = p.ystream;
 #pragma unroll
     for (int j = 0; j < RV; ++j) tw.xy[j] = p.lane_xy[j * 32 + lane];
+#pragma unroll
+    for (int i = 0; i < (RV + 1) / 2; ++i) tw.x1[i] = CP == 2 ? p.lane_x1[i * 32 + lane] : 0u;
     for (int i = lane; i < p.xslots; i += 32) tw.Xs[i] = 0.0;  // zero slots stay +0.0
     for (int i = lane; i < p.yslots; i += 32) tw.Ys[i] = 0.0;
     __syncwarp();
@@ -354,7 +364,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
         double r[RV], rh[RV], pv[RV], v[RV];
         {
             double ax[RV];
-            tmem_spmv<ST>(tw, x, ax);
+            tmem_spmv<ST, CP>(tw, x, ax);
 #pragma unroll
             for (int j = 0; j < RV; ++j) {
                 const double bj = c.valid(j) ? __ldcs(bsrc + c.row(j)) : 0.0;
@@ -372,12 +382,12 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                 q[0][j] = dmul(r[j], r[j]);
                 q[1][j] = dmul(rh[j], r[j]);
             }
-            team_reduce<2>(c, q, o);
+            tmem_reduce<2, R, RV>(q, o);
             sigma = o[0];
             rho_next = o[1];
         }
         if (sigma <= smax) {
-            fres = tmem_fresh_rms<ST>(c, tw, x, bsrc);
+            fres = tmem_fresh_rms<ST, CP>(c, tw, x, bsrc);
             conv = fres <= p.tol;
         }
         if (!conv) {
@@ -392,13 +402,13 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                     pv[j] = dadd(r[j], dmul(beta, dsub(pv[j], dmul(omega, v[j]))));
                     y[j] = dmul(dinv[j], pv[j]);
                 }
-                tmem_spmv<ST>(tw, y, v);
+                tmem_spmv<ST, CP>(tw, y, v);
                 double den;
                 {
                     double q[1][RV], o[1];
 #pragma unroll
                     for (int j = 0; j < RV; ++j) q[0][j] = dmul(rh[j], v[j]);
-                    tmem_reduce(c, q, o);
+                    tmem_reduce<1, R, RV>(q, o);
                     den = o[0];
                 }
                 if (scalar_breaks(den)) { brk = true; break; }
@@ -411,7 +421,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                     x[j] = dadd(x[j], dmul(alpha, dmul(dinv[j], pv[j])));  // y = dinv*p recomputed
                 }
                 double t[RV];
-                tmem_spmv<ST>(tw, z, t);
+                tmem_spmv<ST, CP>(tw, z, t);
                 double tt, ts;
                 {
                     double q[2][RV], o[2];
@@ -420,7 +430,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                         q[0][j] = dmul(t[j], t[j]);
                         q[1][j] = dmul(t[j], r[j]);
                     }
-                    team_reduce<2>(c, q, o);
+                    tmem_reduce<2, R, RV>(q, o);
                     tt = o[0];
                     ts = o[1];
                 }
@@ -440,13 +450,13 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                         q[0][j] = dmul(r[j], r[j]);
                         q[1][j] = dmul(rh[j], r[j]);
                     }
-                    team_reduce<2>(c, q, o);
+                    tmem_reduce<2, R, RV>(q, o);
                     sigma = o[0];
                     rho_next = o[1];
                 }
                 if (!isfinite(sigma)) { brk = true; break; }
                 if (sigma <= smax) {
-                    const double f = tmem_fresh_rms<ST>(c, tw, x, bsrc);
+                    const double f = tmem_fresh_rms<ST, CP>(c, tw, x, bsrc);
                     if (f <= p.tol) {
                         fres = f;
                         conv = true;
@@ -456,7 +466,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                 if (scalar_breaks(omega)) { brk = true; break; }
             }
             if (!conv) {
-                fres = tmem_fresh_rms<ST>(c, tw, x, bsrc);
+                fres = tmem_fresh_rms<ST, CP>(c, tw, x, bsrc);
                 conv = !brk && fres <= p.tol;
             }
         }

@@ -196,9 +196,9 @@ struct TmOpt {
 TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
     if (const char* e = std::getenv("BC_SCHED_OPT")) optimize = optimize && std::atoi(e) != 0;
     // two placements of the gather vector: 448k vs 409k cell-solves/s with one,
-    // 413k with three (B200, 100k M156, P regime; BC_GATHER_COPIES overrides)
+    // 413k with three (B200, 100k M156, P regime; BC_GATHER_COPIES=1 overrides)
     int copies = 2;
-    if (const char* e = std::getenv("BC_GATHER_COPIES")) copies = std::max(1, std::min(4, std::atoi(e)));
+    if (const char* e = std::getenv("BC_GATHER_COPIES")) copies = std::atoi(e) == 1 ? 1 : 2;
     if (!optimize) copies = 1;
     // rows padded to an even number of (virtual) steps, so that rows end only
     // on steps 1, 3 (one stream) or 2, 3 (two streams) of a 4-step chunk
