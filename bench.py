@@ -174,16 +174,14 @@ def strategy_config(name):
             "thread-per-cell": StrategyConfig(Strategy.ThreadPerCell)}[name]
 
 
-def dominant_kernel(cfg, algo, k):
-    """The kernel that carries the step (csrc/bc_capi.cu dispatch)."""
-    from paper_2405_17363_b200 import Algo, Strategy
-    if cfg.kind == Strategy.MultiCells:
-        return "multi_cells_kernel"
-    if cfg.kind == Strategy.ThreadPerCell:
-        return "thread_per_cell_kernel"
-    if algo == Algo.BICGSTAB_JACOBI and (cfg.kind == Strategy.OneCell or k == 1):
-        return "block_cells_tmem_kernel"
-    return "block_cells_kernel"
+def dominant_kernel(bits):
+    """The solver kernel that carries the step, from SolveReport.kernels."""
+    from paper_2405_17363_b200 import KERNEL_BLOCK, KERNEL_MULTI, KERNEL_THREAD, KERNEL_TMEM
+    for bit, name in ((KERNEL_TMEM, "block_cells_tmem_kernel"), (KERNEL_BLOCK, "block_cells_kernel"),
+                      (KERNEL_MULTI, "multi_cells_kernel"), (KERNEL_THREAD, "thread_per_cell_kernel")):
+        if bits & bit:
+            return name
+    return "lu_fallback_kernel"
 
 
 def make_workload(cells, first, total, reg, species=SPECIES):
@@ -313,7 +311,7 @@ def main_b200(args):
     achieved = alg_bytes / (kmean / 1e3) / 1e9
     peak, peak_kind = measured_peak_hbm()
     compulsory = cells * (8 * nnz + 16 * n + 16)
-    kname = dominant_kernel(cfg, algo, k)
+    kname = dominant_kernel(rep.kernels)
     tr = ncu_traffic()
     if not tr or tr.get("kernel") != kname or tr.get("cells") != cells or tr.get("species", 156) != n:
         tr = None  # the committed ncu capture is for another workload

@@ -97,7 +97,17 @@ typedef struct {
     double cells_per_block;
     double device_ms;             /* solver kernels only, when BC_OPT_TIMING */
     int64_t kernel_launches;      /* kernels this call launched */
+    int32_t kernels;              /* BC_KERNEL_* bits of the kernels this call launched */
+    int32_t reserved;
 } bc_report;
+
+enum {
+    BC_KERNEL_TMEM = 1,   /* block_cells_tmem_kernel (Jacobi-BiCGSTAB, one warp per group, TMEM operands) */
+    BC_KERNEL_BLOCK = 2,  /* block_cells_kernel (BiCG / wide groups, shared-memory operands) */
+    BC_KERNEL_MULTI = 4,  /* multi_cells_kernel (cooperative, grid-wide reductions) */
+    BC_KERNEL_THREAD = 8, /* thread_per_cell_kernel (+ interleave_kernel) */
+    BC_KERNEL_LU = 16     /* lu_fallback_kernel */
+};
 
 typedef struct {
     int64_t iterations;

@@ -10,6 +10,11 @@ from .solver import (  # noqa: F401
     FLAG_BREAKDOWN,
     FLAG_CONVERGED,
     FLAG_FELL_BACK,
+    KERNEL_BLOCK,
+    KERNEL_LU,
+    KERNEL_MULTI,
+    KERNEL_THREAD,
+    KERNEL_TMEM,
     Algo,
     BatchedSystem,
     CudaError,

@@ -31,7 +31,7 @@ class Report(C.Structure):
     _fields_ = [
         ("n_groups", _i64), ("iterations_effective", _i64), ("iterations_sum", _i64),
         ("max_residual_rms", _f64), ("breakdown_fallbacks", _i64), ("cells_per_block", _f64),
-        ("device_ms", _f64), ("kernel_launches", _i64),
+        ("device_ms", _f64), ("kernel_launches", _i64), ("kernels", _i32), ("reserved", _i32),
     ]
 
 

@@ -111,6 +111,7 @@ struct bc_ctx {
         f_scratch, lu_rms_scratch, t_values, t_work;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     int64_t launches = 0;
+    int32_t kernels = 0;  // BC_KERNEL_* bits since the last bc_solve started
     std::map<BlockFn, bool> smem_set;
 };
 
@@ -312,8 +313,12 @@ double sigma_threshold(double tol, int n) {
     return r;
 }
 
+// The TMEM kernel runs a group on one warp whatever the v1 team width: its
+// reduction tree is the full Q = P/32 slots per lane (Q <= 16 instantiated).
+bool tmem_fits(const bc::GroupPlan& gp) { return gp.geo.P >= 32 && gp.geo.Q <= 16; }
+
 void ensure_tmem_schedule(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp) {
-    if (gp.has_tm || tmem_disabled() || gp.geo.W != 1) return;
+    if (gp.has_tm || tmem_disabled() || !tmem_fits(gp)) return;
     gp.tm = bc::build_tmem_schedule(pat, gp.k);
     gp.d_tm_words = upload(ctx, gp.tm.words);
     gp.d_tm_vidx = upload(ctx, gp.tm.vidx);
@@ -355,7 +360,7 @@ const TmemCfg* pick_tmem_cfg(const bc::GroupPlan& gp) {
     const int want = std::min(4 * cpq, tmem_warps_pref());
     const TmemCfg* cfg = nullptr;
     for (const TmemCfg& t : kTmemConfigs) {
-        if (t.R != gp.geo.R || t.RV < gp.geo.RV || t.warps < want || t.ST != gp.tm.streams ||
+        if (t.R != gp.geo.Q || t.RV < (gp.geo.n + 31) / 32 || t.warps < want || t.ST != gp.tm.streams ||
             t.CP != gp.tm.copies)
             continue;
         if (!cfg || t.warps < cfg->warps || (t.warps == cfg->warps && t.RV < cfg->RV)) cfg = &t;
@@ -366,7 +371,7 @@ const TmemCfg* pick_tmem_cfg(const bc::GroupPlan& gp) {
 bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t cell0, int64_t gout0,
                  int groups, const double* values, const double* rhs, double* x, double tol, int64_t max_iter,
                  unsigned int* counter, cudaStream_t st) {
-    if (tmem_disabled() || gp.geo.W != 1) return false;
+    if (tmem_disabled() || !tmem_fits(gp)) return false;
     ensure_tmem_schedule(ctx, pat, gp);
     const TmemCfg* cfg = pick_tmem_cfg(gp);
     if (!cfg) return false;
@@ -419,6 +424,7 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
     cfg->fn<<<blocks, warps * 32, smem, st>>>(p);
     check_cuda(cudaGetLastError(), "block_cells_tmem_kernel launch");
     ctx->launches++;
+    ctx->kernels |= BC_KERNEL_TMEM;
     return true;
 }
 
@@ -473,6 +479,7 @@ void launch_block(bc_ctx* ctx, const bc::Pattern& pat, const bc::GroupPlan& gp, 
     fn<<<sh.blocks, sh.threads, sh.smem, st>>>(p);
     check_cuda(cudaGetLastError(), "block_cells_kernel launch");
     ctx->launches++;
+    ctx->kernels |= BC_KERNEL_BLOCK;
 }
 
 struct GroupSpan {
@@ -595,6 +602,7 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
         bc::lu_fallback_kernel<<<cnt, 256, smem, st>>>(lp);
         check_cuda(cudaGetLastError(), "lu_fallback_kernel launch");
         ctx->launches++;
+        ctx->kernels |= BC_KERNEL_LU;
     }
     std::vector<int32_t> status(ents.size());
     check_cuda(cudaMemcpyAsync(status.data(), ctx->lu_status.p, sizeof(int32_t) * ents.size(), cudaMemcpyDeviceToHost,
@@ -665,6 +673,7 @@ MultiResult run_multi(bc_ctx* ctx, const bc::Pattern& pat, const int32_t* d_rp, 
     check_cuda(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bc::multi_cells_kernel), dim3(grid), dim3(256),
                                            args, smem, st), "multi_cells_kernel cooperative launch");
     ctx->launches++;
+    ctx->kernels |= BC_KERNEL_MULTI;
     MultiResult r;
     char buf[24];
     check_cuda(cudaMemcpyAsync(buf, ctx->m_out.p, 24, cudaMemcpyDeviceToHost, st), "D2H multi");
@@ -834,6 +843,7 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
         check_cuda(ctx->grms.ensure(sizeof(double) * n_groups), "cudaMalloc");
         check_cuda(ctx->gflags.ensure(n_groups), "cudaMalloc");
         const int64_t launches0 = ctx->launches;
+        ctx->kernels = 0;
 
         const bool timing = (prm->options & BC_OPT_TIMING) != 0;
         const bool bicg = prm->algo == BC_ALGO_BICG;
@@ -913,6 +923,7 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
                 bc::thread_per_cell_kernel<bc::kBiCGStab><<<blocks, 128, 0, st>>>(tp);
             check_cuda(cudaGetLastError(), "thread_per_cell_kernel launch");
             ctx->launches += 2;
+            ctx->kernels |= BC_KERNEL_THREAD;
         }
         for (const GroupSpan& sp : spans) {
             if (multi || tpc) break;
@@ -1001,6 +1012,7 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
             }
             report->breakdown_fallbacks = fallbacks;
             report->kernel_launches = ctx->launches - launches0;
+            report->kernels = ctx->kernels;
             if (timing) {
                 float ms = 0.f;
                 check_cuda(cudaEventElapsedTime(&ms, ctx->e0, ctx->e1), "cudaEventElapsedTime");

@@ -113,6 +113,11 @@ class SolveReport:
     per_block_flags: object = None
     device_ms: float = 0.0
     kernel_launches: int = 0
+    kernels: int = 0                     # KERNEL_* bits of the kernels launched
+
+
+# bc_report.kernels bits (include/blockcells_b200.h)
+KERNEL_TMEM, KERNEL_BLOCK, KERNEL_MULTI, KERNEL_THREAD, KERNEL_LU = 1, 2, 4, 8, 16
 
 
 @dataclass
@@ -272,7 +277,7 @@ class Solver:
             per_block_iterations=iters.astype(np.int64).tolist(), max_residual_rms=float(rep.max_residual_rms),
             wall_time_ns=int(wall), breakdown_fallbacks=int(rep.breakdown_fallbacks), per_cell_x=x_out,
             per_block_residual_rms=rms, per_block_flags=flags, device_ms=float(rep.device_ms),
-            kernel_launches=int(rep.kernel_launches))
+            kernel_launches=int(rep.kernel_launches), kernels=int(rep.kernels))
 
     # strategies.hpp:60-77
     def solve_one_cell(self, system, tol, max_iter, device: DeviceSpec = DeviceSpec(), algo=Algo.BICG, **kw):

@@ -12,8 +12,9 @@ import pytest
 
 import oracle_ffi as of
 from fixtures import random_batch
-from paper_2405_17363_b200 import (Algo, BatchedSystem, DeviceSpec, InvalidGrouping, Mechanism, REGIME_C,
-                                   REGIME_P, ReductionPlan, Strategy, StrategyConfig, UnsupportedMechanism)
+from paper_2405_17363_b200 import (KERNEL_BLOCK, KERNEL_MULTI, KERNEL_THREAD, KERNEL_TMEM, Algo, BatchedSystem,
+                                   DeviceSpec, InvalidGrouping, Mechanism, REGIME_C, REGIME_P, ReductionPlan,
+                                   Strategy, StrategyConfig, UnsupportedMechanism)
 
 pytestmark = pytest.mark.gpu
 
@@ -103,6 +104,9 @@ def test_m156_bicgstab_bitwise_vs_oracle(solver, m156, m156_batches, regime, kin
     assert st == 0
     assert_matches_oracle(rep, res, f"bicgstab {regime} {kind} {k}")
     north_star_tolerances(rep, res)
+    want = {Strategy.MultiCells: KERNEL_MULTI, Strategy.ThreadPerCell: KERNEL_THREAD}.get(
+        kind, KERNEL_TMEM if k == 1 else KERNEL_BLOCK)
+    assert rep.kernels & ~16 == want, (rep.kernels, want)  # the intended kernel ran (16 = LU fallback)
     if regime == "C":
         # converging regime: the solution agrees with the reference's dense LU
         for c in range(0, 100, 17):
@@ -123,6 +127,8 @@ def test_m312_block_cells(solver):
                                          REGIME_C.tol, 400, workers=8)
             assert st == 0
             assert_matches_oracle(rep, res, f"M312 {algo} k={k}")
+            if algo == Algo.BICGSTAB_JACOBI and k == 1:
+                assert rep.kernels & KERNEL_TMEM  # the scaled mechanism runs on the TMEM kernel too
 
 
 # --- reference test-suite shapes (tests/test_strategies.cpp, test_bicg.cpp) --
