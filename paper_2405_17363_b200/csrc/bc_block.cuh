@@ -26,6 +26,16 @@ namespace bc {
 
 enum AlgoKind { kBiCG = 0, kBiCGStab = 1 };
 
+// Host inputs streamed in while the kernel runs (bc_solve): the copy engine
+// writes chunk c's values and rhs, then ready[c] = 1.  Group g of a launch
+// belongs to chunk chunk_base + g / chunk_groups; chunk boundaries fall on
+// 128-byte lines, so no line of a chunk is cached before its flag is seen.
+struct InputGate {
+    const unsigned int* ready;
+    unsigned int* err;  // set if a chunk never arrives (a stalled copy engine)
+    int chunk_groups, chunk_base;
+};
+
 struct BlockParams {
     const double* values;   // cells * nnz
     const double* rhs;      // cells * species
@@ -62,7 +72,25 @@ struct BlockParams {
     const int32_t* xpos;    // group row -> shared slot of the gathered vector (A pass)
     const int32_t* txpos;   // same for the A^T pass (BiCG)
     int xslots, txslots;    // shared slots of the gathered vectors (multiples of 32)
+    InputGate gate;         // streamed host inputs (bc_solve), or gate.ready == nullptr
 };
+
+// One thread waits for group g's chunk (acquire), the caller then syncs its team.
+__device__ __forceinline__ void gate_wait(const InputGate& gt, int g) {
+    if (!gt.ready) return;
+    const unsigned int* f = gt.ready + gt.chunk_base + g / gt.chunk_groups;
+    const long long t0 = clock64();
+    for (;;) {
+        unsigned int v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (v) break;
+        if (clock64() - t0 > (20ll << 30)) {  // ~10 s at 2 GHz
+            atomicExch(gt.err, 1u);
+            break;
+        }
+        __nanosleep(500);
+    }
+}
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
@@ -300,6 +328,10 @@ __global__ void __launch_bounds__(256, 1) block_cells_kernel(const BlockParams p
             c.tm.sync();
         }
         if (gl >= p.group_count) break;
+        if (p.gate.ready) {
+            if (c.tm.tid == 0) gate_wait(p.gate, gl);
+            c.tm.sync();
+        }
 
         const int64_t cell0 = p.cell_offset + static_cast<int64_t>(gl) * p.kc;
         const double* src = p.values + cell0 * p.nnz;

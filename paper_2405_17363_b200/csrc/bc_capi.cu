@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <numeric>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -61,6 +62,17 @@ void check_cuda(cudaError_t e, const char* what) {
         throw Status(BC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Device address of page-locked host memory (cudaHostAlloc / cudaHostRegister),
+// or nullptr for pageable or device memory.
+void* mapped_host_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (!p || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 bool is_device_ptr(const void* p) {
     if (!p) return false;
     cudaPointerAttributes a;
@@ -110,6 +122,11 @@ struct bc_ctx {
     DevBuf values, rhs, x, giters, grms, gflags, counters, lu_scratch, lu_entries, lu_status,
         f_scratch, lu_rms_scratch, t_values, t_work;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
+    // host-input pipeline: chunk copies + ready flags on copy_st, gated kernels on st
+    cudaStream_t copy_st = nullptr;
+    cudaEvent_t pipe_ev[2] = {nullptr, nullptr};
+    DevBuf pipe_flags;                  // kPipeFlags ready flags + 1 error word
+    unsigned int* h_ones = nullptr;     // pinned source of the flag writes
     int64_t launches = 0;
     int32_t kernels = 0;  // BC_KERNEL_* bits since the last bc_solve started
     std::map<BlockFn, bool> smem_set;
@@ -256,6 +273,16 @@ LaunchShape choose_shape(bc_ctx* ctx, BlockFn fn, const bc::GroupPlan& gp, bool 
 
 using TmemFn = void (*)(bc::TmemParams);
 
+// Host-input pipeline (bc_solve): chunks per span, and the smallest batch worth it.
+constexpr int kPipeChunksMax = 64;          // per span
+constexpr int kPipeFlags = 2 * kPipeChunksMax;  // Block-cells has at most two spans
+int pipe_chunks() {  // BC_PIPE_CHUNKS overrides the default 32
+    const char* e = std::getenv("BC_PIPE_CHUNKS");
+    const int c = e ? std::atoi(e) : 32;
+    return std::max(1, std::min(kPipeChunksMax, c));
+}
+constexpr int64_t kPipeMinCells = 4096;
+
 struct TmemCfg {
     int R, RV, warps, ST, CP;  // warps per CTA (= 4 * groups per lane quarter), row streams, gather copies
     TmemFn fn;
@@ -370,7 +397,7 @@ const TmemCfg* pick_tmem_cfg(const bc::GroupPlan& gp) {
 
 bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t cell0, int64_t gout0,
                  int groups, const double* values, const double* rhs, double* x, double tol, int64_t max_iter,
-                 unsigned int* counter, cudaStream_t st) {
+                 unsigned int* counter, cudaStream_t st, const bc::InputGate& gate = bc::InputGate{}) {
     if (tmem_disabled() || !tmem_fits(gp)) return false;
     ensure_tmem_schedule(ctx, pat, gp);
     const TmemCfg* cfg = pick_tmem_cfg(gp);
@@ -419,6 +446,7 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
     p.sigma_max = sigma_threshold(tol, gp.geo.n);
     p.tol = tol;
     p.max_iter = static_cast<int>(std::min<int64_t>(max_iter, 0x7FFFFFFF));
+    p.gate = gate;
     const int blocks = std::max(1, std::min(ctx->sms, (groups + warps - 1) / warps));
     check_cuda(cudaMemsetAsync(counter, 0, sizeof(unsigned int), st), "cudaMemsetAsync(counter)");
     cfg->fn<<<blocks, warps * 32, smem, st>>>(p);
@@ -432,7 +460,7 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
 void launch_block(bc_ctx* ctx, const bc::Pattern& pat, const bc::GroupPlan& gp, int algo,
                   int64_t cell0, int64_t gout0, int groups, const double* values,
                   const double* rhs, const double* x0, double* x, double tol, int64_t max_iter,
-                  unsigned int* counter, cudaStream_t st) {
+                  unsigned int* counter, cudaStream_t st, const bc::InputGate& gate = bc::InputGate{}) {
     const KernelCfg* cfg = pick_config(gp.geo);
     if (!cfg) fail(BC_ERR_INVALID_ARGUMENT, "no kernel configuration for this group size");
     const bool bicg = algo == BC_ALGO_BICG;
@@ -468,6 +496,7 @@ void launch_block(bc_ctx* ctx, const bc::Pattern& pat, const bc::GroupPlan& gp, 
     p.tol = tol;
     p.max_iter = max_iter;
     p.level = sh.level;
+    p.gate = gate;
     p.vidx = gp.d_vidx;
     p.tvidx = gp.d_tvidx;
     p.didx = gp.d_didx;
@@ -702,6 +731,13 @@ int bc_ctx_create(int device, bc_ctx** out) {
         check_cuda(cudaEventCreate(&ctx->e0), "cudaEventCreate");
         check_cuda(cudaEventCreate(&ctx->e1), "cudaEventCreate");
         check_cuda(ctx->counters.ensure(64 * sizeof(unsigned int)), "cudaMalloc");
+        check_cuda(cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking), "cudaStreamCreate");
+        for (cudaEvent_t& e : ctx->pipe_ev)
+            check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        check_cuda(ctx->pipe_flags.ensure(sizeof(unsigned int) * (kPipeFlags + 1)), "cudaMalloc(flags)");
+        check_cuda(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_ones), sizeof(unsigned int), cudaHostAllocDefault),
+                   "cudaHostAlloc");
+        ctx->h_ones[0] = 1u;
         return BC_OK;
     });
     if (st != BC_OK) {
@@ -725,6 +761,11 @@ void bc_ctx_destroy(bc_ctx* ctx) {
     for (DevBuf& b : ctx->plan_bufs) b.release();
     if (ctx->e0) cudaEventDestroy(ctx->e0);
     if (ctx->e1) cudaEventDestroy(ctx->e1);
+    for (cudaEvent_t e : ctx->pipe_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->copy_st) cudaStreamDestroy(ctx->copy_st);
+    ctx->pipe_flags.release();
+    if (ctx->h_ones) cudaFreeHost(ctx->h_ones);
     delete ctx;
 }
 
@@ -824,17 +865,38 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
         const double* d_values = values;
         const double* d_rhs = rhs;
         double* d_x = x_out;
-        if (!is_device_ptr(values)) {
+        // Host inputs of a Block-cells / One-cell solve stream in by chunks while
+        // the kernel runs: every chunk's copy is queued on copy_st BEFORE the
+        // launch, followed by its ready flag; the kernel's warps wait for the
+        // flag of their group's chunk (InputGate).  Queued first, the copies
+        // also complete first wherever work is serialised (profilers,
+        // CUDA_LAUNCH_BLOCKING), so the gate can never wait on later work.
+        const bool pipelined = !is_device_ptr(values) && !is_device_ptr(rhs) &&
+                               prm->strategy != BC_STRATEGY_MULTI_CELLS &&
+                               prm->strategy != BC_STRATEGY_THREAD_PER_CELL && cells >= kPipeMinCells &&
+                               std::getenv("BC_NO_PIPELINE") == nullptr;
+        if (pipelined) {
+            check_cuda(ctx->values.ensure(vbytes), "cudaMalloc(values)");
+            check_cuda(ctx->rhs.ensure(bbytes), "cudaMalloc(rhs)");
+            d_values = ctx->values.as<double>();
+            d_rhs = ctx->rhs.as<double>();
+        } else if (!is_device_ptr(values)) {
             check_cuda(ctx->values.ensure(vbytes), "cudaMalloc(values)");
             check_cuda(cudaMemcpyAsync(ctx->values.p, values, vbytes, cudaMemcpyHostToDevice, st), "H2D values");
             d_values = ctx->values.as<double>();
         }
-        if (!is_device_ptr(rhs)) {
+        if (!pipelined && !is_device_ptr(rhs)) {
             check_cuda(ctx->rhs.ensure(bbytes), "cudaMalloc(rhs)");
             check_cuda(cudaMemcpyAsync(ctx->rhs.p, rhs, bbytes, cudaMemcpyHostToDevice, st), "H2D rhs");
             d_rhs = ctx->rhs.as<double>();
         }
-        const bool host_x = !is_device_ptr(x_out);
+        bool host_x = !is_device_ptr(x_out);
+        if (host_x && pipelined) {  // pinned x_out: the kernels write the solution straight to host memory
+            if (double* mapped = static_cast<double*>(mapped_host_ptr(x_out))) {
+                d_x = mapped;
+                host_x = false;
+            }
+        }
         if (host_x) {
             check_cuda(ctx->x.ensure(bbytes), "cudaMalloc(x)");
             d_x = ctx->x.as<double>();
@@ -925,20 +987,56 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
             ctx->launches += 2;
             ctx->kernels |= BC_KERNEL_THREAD;
         }
-        for (const GroupSpan& sp : spans) {
+        // streamed inputs: chunks of each span, each a whole number of 128-byte
+        // lines of values and rhs; all copies and flags queued before the launches
+        std::vector<bc::InputGate> gates(spans.size(), bc::InputGate{nullptr, nullptr, 1, 0});
+        if (pipelined) {
+            unsigned int* flags_d = ctx->pipe_flags.as<unsigned int>();
+            check_cuda(cudaMemsetAsync(flags_d, 0, sizeof(unsigned int) * (kPipeFlags + 1), st), "memset flags");
+            check_cuda(cudaEventRecord(ctx->pipe_ev[0], st), "cudaEventRecord");
+            check_cuda(cudaStreamWaitEvent(ctx->copy_st, ctx->pipe_ev[0]), "cudaStreamWaitEvent");
+            int base = 0;
+            for (size_t i = 0; i < spans.size(); ++i) {
+                const GroupSpan& sp = spans[i];
+                const int align = 16 / std::gcd(16, sp.k);
+                int per = std::max(align, (sp.count + pipe_chunks() - 1) / pipe_chunks());
+                per = (per + align - 1) / align * align;
+                gates[i] = bc::InputGate{flags_d, flags_d + kPipeFlags, per, base};
+                for (int g0 = 0; g0 < sp.count; g0 += per, ++base) {
+                    const int64_t c0 = sp.cell0 + static_cast<int64_t>(g0) * sp.k;
+                    const int64_t nc = static_cast<int64_t>(std::min(per, sp.count - g0)) * sp.k;
+                    check_cuda(cudaMemcpyAsync(ctx->values.as<double>() + c0 * nnz, values + c0 * nnz,
+                                               sizeof(double) * nc * nnz, cudaMemcpyHostToDevice, ctx->copy_st),
+                               "H2D values chunk");
+                    check_cuda(cudaMemcpyAsync(ctx->rhs.as<double>() + c0 * s, rhs + c0 * s, sizeof(double) * nc * s,
+                                               cudaMemcpyHostToDevice, ctx->copy_st), "H2D rhs chunk");
+                    check_cuda(cudaMemcpyAsync(flags_d + base, ctx->h_ones, sizeof(unsigned int),
+                                               cudaMemcpyHostToDevice, ctx->copy_st), "H2D ready flag");
+                }
+            }
+            if (base > kPipeFlags) fail(BC_ERR_INVALID_ARGUMENT, "input pipeline: too many chunks");
+            check_cuda(cudaEventRecord(ctx->pipe_ev[1], ctx->copy_st), "cudaEventRecord");
+        }
+        for (size_t i = 0; i < spans.size(); ++i) {
             if (multi || tpc) break;
+            const GroupSpan& sp = spans[i];
             bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);
             unsigned int* counter = ctx->counters.as<unsigned int>() + slot++;
-            if (!bicg && launch_tmem(ctx, pat, gp, sp.cell0, sp.gout0, sp.count, d_values, d_rhs, d_x, prm->tol,
-                                     prm->max_iter, counter, st))
-                continue;
-            launch_block(ctx, pat, gp, prm->algo, sp.cell0, sp.gout0, sp.count, d_values, d_rhs,
-                         nullptr, d_x, prm->tol, prm->max_iter, counter, st);
+            if (bicg || !launch_tmem(ctx, pat, gp, sp.cell0, sp.gout0, sp.count, d_values, d_rhs, d_x, prm->tol,
+                                     prm->max_iter, counter, st, gates[i]))
+                launch_block(ctx, pat, gp, prm->algo, sp.cell0, sp.gout0, sp.count, d_values, d_rhs, nullptr, d_x,
+                             prm->tol, prm->max_iter, counter, st, gates[i]);
         }
+        if (pipelined) check_cuda(cudaStreamWaitEvent(st, ctx->pipe_ev[1]), "cudaStreamWaitEvent");  // join
         // breakdown groups -> device LU fallback
         std::vector<uint8_t> flags(n_groups);
         check_cuda(cudaMemcpyAsync(flags.data(), ctx->gflags.p, n_groups, cudaMemcpyDeviceToHost, st), "D2H flags");
+        unsigned int gate_err = 0;
+        if (pipelined)
+            check_cuda(cudaMemcpyAsync(&gate_err, ctx->pipe_flags.as<unsigned int>() + kPipeFlags, sizeof gate_err,
+                                       cudaMemcpyDeviceToHost, st), "D2H gate error");
         check_cuda(cudaStreamSynchronize(st), "solve kernels");
+        if (gate_err) fail(BC_ERR_CUDA, "input pipeline: a chunk of the host inputs never arrived");
         std::vector<bc::LuEntry> ents;
         for (const GroupSpan& sp : spans)
             for (int g = 0; g < sp.count; ++g) {

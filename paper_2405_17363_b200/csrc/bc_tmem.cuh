@@ -65,6 +65,7 @@ struct TmemParams {
     double sigma_max;       // sqrt(sigma/n) <= tol  <=>  sigma <= sigma_max
     double tol;             // the fresh-residual test keeps the literal comparison
     int max_iter;
+    InputGate gate;         // streamed host inputs (bc_solve), or gate.ready == nullptr
 };
 
 __device__ __forceinline__ void tm_ld_x2(uint32_t addr, uint32_t (&r)[2]) {
@@ -331,6 +332,10 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
         if (lane == 0) gv = atomicAdd(p.counter, 1u);
         const int gl = static_cast<int>(__shfl_sync(0xffffffffu, gv, 0));
         if (gl >= p.group_count) break;
+        if (p.gate.ready) {
+            if (lane == 0) gate_wait(p.gate, gl);
+            __syncwarp();
+        }
         const int64_t cell0 = p.cell_offset + static_cast<int64_t>(gl) * p.kc;
         const double* src = p.values + cell0 * p.nnz;
         const double* bsrc = p.rhs + cell0 * p.species;

@@ -278,6 +278,34 @@ def test_device_resident_equals_host(solver, m156):
     assert dev.per_block_iterations == host.per_block_iterations
 
 
+@pytest.mark.parametrize("algo,k,pinned", [(Algo.BICGSTAB_JACOBI, 1, True), (Algo.BICGSTAB_JACOBI, 1, False),
+                                           (Algo.BICG, 4, True)])
+def test_pipelined_host_inputs_equal_device(solver, m156, algo, k, pinned):
+    """Host inputs of >= 4096 cells stream in by chunks while the kernel runs,
+    its warps gated on per-chunk ready flags (bc_solve); a pinned x_out is
+    written in place by the kernels.  Same bits as device-resident inputs, the
+    remainder group of k=4 over 6001 cells included."""
+    import torch
+    cells = 6001
+    v, b = m156.newton_batch(0, cells, cells, 1.0)
+    if pinned:
+        v = torch.from_numpy(v).pin_memory().numpy()
+        b = torch.from_numpy(b).pin_memory().numpy()
+    host = run_gpu(solver, system_of(m156.row_ptr, m156.col_idx, v, b), Strategy.BlockCells, k, algo, 1e-10, 300)
+    dv, db = torch.from_numpy(np.ascontiguousarray(v)).cuda(), torch.from_numpy(np.ascontiguousarray(b)).cuda()
+    dev = run_gpu(solver, system_of(m156.row_ptr, m156.col_idx, dv, db), Strategy.BlockCells, k, algo, 1e-10, 300)
+    np.testing.assert_array_equal(of.bits(dev.per_cell_x.cpu().numpy()), of.bits(host.per_cell_x))
+    assert dev.per_block_iterations == host.per_block_iterations
+    assert of.bits(dev.max_residual_rms) == of.bits(host.max_residual_rms)
+    assert host.kernel_launches == dev.kernel_launches  # one gated launch per span
+    if pinned:  # zero-copy solution
+        xo = torch.empty((cells, m156.species), dtype=torch.float64, pin_memory=True).numpy()
+        zc = solver.run_strategy(system_of(m156.row_ptr, m156.col_idx, v, b), StrategyConfig(Strategy.BlockCells, k),
+                                 DeviceSpec(), 1e-10, 300, 1, algo, x_out=xo)
+        np.testing.assert_array_equal(of.bits(xo), of.bits(host.per_cell_x))
+        assert zc.per_block_iterations == host.per_block_iterations
+
+
 def test_device_newton_assembly_bitwise(solver, m156):
     from paper_2405_17363_b200.workload import assemble_on_device
     for h in (120.0, 1.0):
