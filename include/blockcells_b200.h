@@ -22,6 +22,7 @@
  *   BC_ERR_INVALID_GROUPING      blockcells::InvalidGrouping      exec_model.hpp:19-21
  *   BC_ERR_UNSUPPORTED_MECHANISM blockcells::UnsupportedMechanism exec_model.hpp:14-16
  *   BC_ERR_SINGULAR_MATRIX       blockcells::SingularMatrix       dense_lu.hpp:12-14 (LU fallback)
+ *   BC_ERR_SOLVER_ABORT          blockcells::SolverAbort          simulate.hpp:15-19 (bc_simulate)
  * Numerical breakdown is a per-group flag, never an error (bicg.hpp:39-41).
  *
  * Pointers passed to bc_solve / bc_bicg_solve may be host (pageable or
@@ -47,7 +48,8 @@ typedef enum {
     BC_ERR_SINGULAR_MATRIX = -4,
     BC_ERR_CUDA = -5,
     BC_ERR_NO_PATTERN = -6,
-    BC_ERR_NO_MEMORY = -7
+    BC_ERR_NO_MEMORY = -7,
+    BC_ERR_SOLVER_ABORT = -8
 } bc_status;
 
 /* Strategy (exec_model.hpp:23) plus the two comparison baselines. */
@@ -193,6 +195,61 @@ int bc_newton_assemble(bc_ctx* ctx, int64_t count, int32_t species, int32_t reac
                        const int32_t* products, const int32_t* diag_slot, double h,
                        const double* y, const double* y_prev, double* values, double* rhs,
                        void* stream);
+
+/*
+ * Device-resident backward-Euler simulation: replaces
+ * run_simulation (simulate.hpp:76-78, simulate.cpp:72-178) with every
+ * per-cell array kept in HBM.  Per Newton iteration: bc_newton_assemble's
+ * kernel builds A = I - hJ(y), b = -(y - y_prev - h f(y)) from the current
+ * states; the configured strategy solves (bc_solve on device memory), or the
+ * device LU when use_direct_reference; one fused kernel adds the update and
+ * max-reduces |dy| and |y| (max is order-free, so bit-equal to the host
+ * loop); only those two numbers cross to the host for the Newton test
+ * |dy|_inf < newton_rtol * |y|_inf.  Negative states are clipped (counted)
+ * after each step.  A non-finite state returns BC_ERR_SOLVER_ABORT with
+ * *abort_step set, as SolverAbort does.
+ */
+typedef struct { /* SimulationConfig (simulate.hpp:39-55) */
+    int64_t cells;
+    int64_t steps;
+    double dt_seconds;
+    double tol;
+    int64_t max_iter;
+    int32_t strategy;             /* bc_strategy                          */
+    int32_t algo;                 /* bc_algo                              */
+    int64_t cells_per_block;      /* 0 = "N"                              */
+    int64_t max_threads_per_block;
+    int32_t use_direct_reference; /* LinearSolverChoice: dense LU per cell */
+    int32_t reserved;
+    double newton_rtol;
+    int64_t max_newton_iterations;
+    void* stream;
+} bc_sim_params;
+
+typedef struct { /* StepStats (simulate.hpp:59-68) */
+    int64_t step;
+    int64_t newton_iterations;
+    int64_t iterations_effective;
+    int64_t iterations_sum;
+    double max_residual_rms;
+    int64_t wall_time_ns;
+    int64_t breakdown_fallbacks;
+    int64_t clip_events;
+} bc_step_stats;
+
+typedef struct { /* the mechanism's evaluator tables (blockcells_workload.h bcw_stamp_program), host memory */
+    int32_t species, reactions, nnz, stamps;
+    const int32_t *row_ptr, *col_idx; /* Jacobian pattern */
+    const int32_t *stamp_ptr, *stamp_slot, *stamp_other;
+    const double* stamp_sign;
+    const int32_t *reactant_ptr, *reactants, *product_ptr, *products, *diag_slot;
+} bc_mechanism_tables;
+
+/* rates: cells*reactions (host, rate_constants per cell); states: cells*species
+ * (host or device) in: initial states, out: final states; per_step: steps
+ * entries (host). */
+int bc_simulate(bc_ctx* ctx, const bc_sim_params* prm, const bc_mechanism_tables* mech,
+                const double* rates, double* states, bc_step_stats* per_step, int64_t* abort_step);
 
 #ifdef __cplusplus
 }

@@ -220,4 +220,59 @@ int ref_newton_batch(int64_t species, int64_t reactions, uint64_t seed, int64_t 
     }
 }
 
+typedef struct {
+    int64_t step, newton_iterations, iterations_effective, iterations_sum;
+    double max_residual_rms;
+    int64_t wall_time_ns, breakdown_fallbacks, clip_events;
+} ref_step_stats;
+
+// run_simulation (simulate.cpp:72-178) on generate_mechanism(species,
+// reactions, seed).  states: cells*species, in: initial, out: final.
+// Returns -9 with *abort_step set on SolverAbort.
+int ref_run_simulation(int64_t species, int64_t reactions, uint64_t seed, int64_t cells, int mode,
+                       int64_t steps, double dt, double tol, int64_t max_iter, int strategy,
+                       int64_t k_request, int direct, double newton_rtol, int64_t max_newton,
+                       int64_t workers, double* states, ref_step_stats* stats, int64_t* abort_step) {
+    if (abort_step) *abort_step = -1;
+    try {
+        const MechanismSpec mech = generate_mechanism(static_cast<std::size_t>(species),
+                                                      static_cast<std::size_t>(reactions), seed);
+        SimulationConfig cfg;
+        cfg.cells = static_cast<std::size_t>(cells);
+        cfg.mode = mode == 0 ? ConditionMode::Ideal : ConditionMode::Realistic;
+        cfg.steps = static_cast<std::size_t>(steps);
+        cfg.dt_seconds = dt;
+        cfg.tol = tol;
+        cfg.max_iter = static_cast<std::size_t>(max_iter);
+        cfg.worker_count = static_cast<std::size_t>(workers);
+        cfg.solver.use_direct_reference = direct != 0;
+        cfg.solver.strategy.kind = strategy == 0 ? Strategy::OneCell
+                                   : strategy == 1 ? Strategy::MultiCells
+                                                   : Strategy::BlockCells;
+        if (k_request > 0) cfg.solver.strategy.cells_per_block = static_cast<std::size_t>(k_request);
+        cfg.newton_rtol = newton_rtol;
+        cfg.max_newton_iterations = static_cast<std::size_t>(max_newton);
+        std::vector<CellState> init(static_cast<std::size_t>(cells));
+        for (int64_t c = 0; c < cells; ++c)
+            init[c].concentrations.assign(states + c * species, states + (c + 1) * species);
+        const SimulationResult r = run_simulation(mech, cfg, init);
+        for (int64_t c = 0; c < cells; ++c)
+            std::memcpy(states + c * species, r.final_states[c].concentrations.data(), sizeof(double) * species);
+        for (std::size_t i = 0; i < r.per_step.size(); ++i) {
+            const StepStats& q = r.per_step[i];
+            stats[i] = ref_step_stats{static_cast<int64_t>(q.step), static_cast<int64_t>(q.newton_iterations),
+                                      static_cast<int64_t>(q.iterations_effective),
+                                      static_cast<int64_t>(q.iterations_sum), q.max_residual_rms,
+                                      q.wall_time_ns, static_cast<int64_t>(q.breakdown_fallbacks),
+                                      static_cast<int64_t>(q.clip_events)};
+        }
+        return 0;
+    } catch (const SolverAbort& a) {
+        if (abort_step) *abort_step = static_cast<int64_t>(a.step);
+        return -9;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
 }  // extern "C"

@@ -40,6 +40,29 @@ class Outcome(C.Structure):
                 ("converged", _i32), ("breakdown", _i32)]
 
 
+class SimParams(C.Structure):  # bc_sim_params (SimulationConfig)
+    _fields_ = [
+        ("cells", _i64), ("steps", _i64), ("dt_seconds", _f64), ("tol", _f64), ("max_iter", _i64),
+        ("strategy", _i32), ("algo", _i32), ("cells_per_block", _i64), ("max_threads_per_block", _i64),
+        ("use_direct_reference", _i32), ("reserved", _i32), ("newton_rtol", _f64),
+        ("max_newton_iterations", _i64), ("stream", _c_p),
+    ]
+
+
+class StepStatsC(C.Structure):  # bc_step_stats (StepStats)
+    _fields_ = [
+        ("step", _i64), ("newton_iterations", _i64), ("iterations_effective", _i64), ("iterations_sum", _i64),
+        ("max_residual_rms", _f64), ("wall_time_ns", _i64), ("breakdown_fallbacks", _i64),
+        ("clip_events", _i64),
+    ]
+
+
+class MechTables(C.Structure):  # bc_mechanism_tables
+    _fields_ = [("species", _i32), ("reactions", _i32), ("nnz", _i32), ("stamps", _i32)] + [
+        (n, _c_p) for n in ("row_ptr", "col_idx", "stamp_ptr", "stamp_slot", "stamp_other", "stamp_sign",
+                            "reactant_ptr", "reactants", "product_ptr", "products", "diag_slot")]
+
+
 def _load(path: str, what: str) -> C.CDLL:
     if not os.path.exists(path):
         raise RuntimeError(
@@ -73,6 +96,8 @@ def b200() -> C.CDLL:
         lib.bc_kernel_launches.restype = _i64
         lib.bc_newton_assemble.argtypes = [_c_p, _i64, _i32, _i32, _i32] + [_c_p] * 10 + [
             _f64, _c_p, _c_p, _c_p, _c_p, _c_p]
+        lib.bc_simulate.argtypes = [_c_p, C.POINTER(SimParams), C.POINTER(MechTables), _c_p, _c_p, _c_p,
+                                    C.POINTER(_i64)]
         _b200 = lib
     return _b200
 

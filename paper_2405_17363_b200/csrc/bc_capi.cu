@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -121,6 +122,8 @@ struct bc_ctx {
     std::vector<DevBuf> plan_bufs;
     DevBuf values, rhs, x, giters, grms, gflags, counters, lu_scratch, lu_entries, lu_status,
         f_scratch, lu_rms_scratch, t_values, t_work;
+    // device-resident simulation (bc_simulate)
+    DevBuf sim_tabs, sim_sign, sim_rates, sim_y, sim_prev, sim_values, sim_rhs, sim_dx, sim_red;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     // host-input pipeline: chunk copies + ready flags on copy_st, gated kernels on st
     cudaStream_t copy_st = nullptr;
@@ -756,7 +759,8 @@ void bc_ctx_destroy(bc_ctx* ctx) {
                       &ctx->grms, &ctx->gflags, &ctx->counters, &ctx->lu_scratch,
                       &ctx->lu_entries, &ctx->lu_status, &ctx->f_scratch, &ctx->lu_rms_scratch, &ctx->t_values,
                       &ctx->t_work, &ctx->m_trp, &ctx->m_trow, &ctx->m_tval, &ctx->m_diag, &ctx->m_ranges,
-                      &ctx->m_work, &ctx->m_part, &ctx->m_out})
+                      &ctx->m_work, &ctx->m_part, &ctx->m_out, &ctx->sim_tabs, &ctx->sim_sign, &ctx->sim_rates,
+                      &ctx->sim_y, &ctx->sim_prev, &ctx->sim_values, &ctx->sim_rhs, &ctx->sim_dx, &ctx->sim_red})
         b->release();
     for (DevBuf& b : ctx->plan_bufs) b.release();
     if (ctx->e0) cudaEventDestroy(ctx->e0);
@@ -1227,6 +1231,144 @@ int bc_newton_assemble(bc_ctx* ctx, int64_t count, int32_t species, int32_t reac
                                      static_cast<cudaStream_t>(stream)>>>(p);
         check_cuda(cudaGetLastError(), "newton_assemble_kernel launch");
         ctx->launches++;
+        return BC_OK;
+    });
+}
+
+int bc_simulate(bc_ctx* ctx, const bc_sim_params* prm, const bc_mechanism_tables* mt, const double* rates,
+                double* states, bc_step_stats* per_step, int64_t* abort_step) {
+    if (!ctx || !prm || !mt || !rates || !states) return BC_ERR_INVALID_ARGUMENT;
+    if (abort_step) *abort_step = -1;
+    return guarded(ctx, [&]() -> int {
+        // simulate.cpp:75-83
+        if (prm->cells < 1) fail(BC_ERR_INVALID_ARGUMENT, "run_simulation: cells must be >= 1");
+        if (!(prm->dt_seconds > 0.0)) fail(BC_ERR_INVALID_ARGUMENT, "run_simulation: dt must be positive");
+        if (mt->species < 1 || mt->reactions < 0 || mt->nnz < 1 || mt->stamps < 0)
+            fail(BC_ERR_INVALID_ARGUMENT, "run_simulation: bad mechanism tables");
+        if (prm->steps > 0 && !per_step) fail(BC_ERR_INVALID_ARGUMENT, "run_simulation: per_step is NULL");
+        const int64_t cells = prm->cells, s = mt->species, nnz = mt->nnz, R = mt->reactions;
+        cudaStream_t st = static_cast<cudaStream_t>(prm->stream);
+
+        // the pattern (kept when unchanged: plans and schedules survive)
+        const bc::Pattern want = make_pattern(static_cast<int32_t>(s), mt->row_ptr, mt->col_idx);
+        if (!ctx->has_pattern || ctx->pat.row_ptr != want.row_ptr || ctx->pat.col_idx != want.col_idx) {
+            const int stp = bc_set_pattern(ctx, static_cast<int32_t>(s), mt->row_ptr, mt->col_idx);
+            if (stp != BC_OK) throw Status(stp, ctx->err);
+        }
+        // evaluator tables -> device, one int32 buffer
+        const int32_t nre = mt->reactant_ptr[R], npr = mt->product_ptr[R];
+        std::vector<int32_t> tabs;
+        auto put = [&](const int32_t* p, int64_t n) {
+            const size_t at = tabs.size();
+            tabs.insert(tabs.end(), p, p + n);
+            return at;
+        };
+        const size_t o_sp = put(mt->stamp_ptr, R + 1), o_ss = put(mt->stamp_slot, mt->stamps),
+                     o_so = put(mt->stamp_other, mt->stamps), o_rp = put(mt->reactant_ptr, R + 1),
+                     o_re = put(mt->reactants, nre), o_pp = put(mt->product_ptr, R + 1),
+                     o_pr = put(mt->products, npr), o_dg = put(mt->diag_slot, s);
+        check_cuda(ctx->sim_tabs.ensure(sizeof(int32_t) * tabs.size()), "cudaMalloc");
+        check_cuda(ctx->sim_sign.ensure(sizeof(double) * std::max<int64_t>(mt->stamps, 1)), "cudaMalloc");
+        check_cuda(ctx->sim_rates.ensure(sizeof(double) * std::max<int64_t>(cells * R, 1)), "cudaMalloc");
+        const size_t yb = sizeof(double) * cells * s;
+        for (DevBuf* b : {&ctx->sim_y, &ctx->sim_prev, &ctx->sim_rhs, &ctx->sim_dx}) check_cuda(b->ensure(yb), "cudaMalloc");
+        check_cuda(ctx->sim_values.ensure(sizeof(double) * cells * nnz), "cudaMalloc");
+        check_cuda(ctx->sim_red.ensure(3 * sizeof(unsigned long long)), "cudaMalloc");
+        check_cuda(ctx->f_scratch.ensure(yb), "cudaMalloc");
+        check_cuda(cudaMemcpyAsync(ctx->sim_tabs.p, tabs.data(), sizeof(int32_t) * tabs.size(),
+                                   cudaMemcpyHostToDevice, st), "H2D tables");
+        if (mt->stamps > 0)
+            check_cuda(cudaMemcpyAsync(ctx->sim_sign.p, mt->stamp_sign, sizeof(double) * mt->stamps,
+                                       cudaMemcpyHostToDevice, st), "H2D signs");
+        if (R > 0)
+            check_cuda(cudaMemcpyAsync(ctx->sim_rates.p, rates, sizeof(double) * cells * R, cudaMemcpyDefault, st),
+                       "H2D rates");
+        double* y = ctx->sim_y.as<double>();
+        double* yprev = ctx->sim_prev.as<double>();
+        double* dx = ctx->sim_dx.as<double>();
+        check_cuda(cudaMemcpyAsync(y, states, yb, cudaMemcpyDefault, st), "H2D states");
+        const int32_t* tb = ctx->sim_tabs.as<int32_t>();
+        const bc::NewtonParams np{cells, static_cast<int>(s), static_cast<int>(R), static_cast<int>(nnz),
+                                  ctx->sim_rates.as<double>(), tb + o_sp, tb + o_ss, tb + o_so,
+                                  ctx->sim_sign.as<double>(), tb + o_rp, tb + o_re, tb + o_pp, tb + o_pr, tb + o_dg,
+                                  prm->dt_seconds, y, yprev, ctx->sim_values.as<double>(), ctx->sim_rhs.as<double>(),
+                                  ctx->f_scratch.as<double>()};
+        const unsigned asm_blocks = static_cast<unsigned>((cells + 127) / 128);
+        const int64_t ny = cells * s;
+        const unsigned ew_blocks = static_cast<unsigned>(std::min<int64_t>((ny + 255) / 256, 8 * ctx->sms));
+        unsigned long long* red = ctx->sim_red.as<unsigned long long>();
+
+        bc_solve_params sp{};
+        sp.strategy = prm->strategy;
+        sp.algo = prm->algo;
+        sp.cells_per_block = prm->cells_per_block;
+        sp.cells = cells;
+        sp.tol = prm->tol;
+        sp.max_iter = prm->max_iter;
+        sp.max_threads_per_block = prm->max_threads_per_block;
+        sp.stream = prm->stream;
+
+        using Clock = std::chrono::steady_clock;
+        for (int64_t step = 0; step < prm->steps; ++step) {  // simulate.cpp:103-176
+            check_cuda(cudaMemcpyAsync(yprev, y, yb, cudaMemcpyDeviceToDevice, st), "D2D prev");
+            bc_step_stats stats{};
+            stats.step = step;
+            for (int64_t newton = 1; newton <= prm->max_newton_iterations; ++newton) {
+                bc::newton_assemble_kernel<<<asm_blocks, 128, 0, st>>>(np);
+                check_cuda(cudaGetLastError(), "newton_assemble_kernel launch");
+                ctx->launches++;
+                if (prm->use_direct_reference) {  // lu_solve per cell (simulate.cpp:119-133)
+                    const auto t0 = Clock::now();
+                    std::vector<bc::LuEntry> ents(static_cast<size_t>(cells));
+                    for (int64_t c = 0; c < cells; ++c) ents[c] = {c, c, 1, 0};
+                    run_lu(ctx, ents, ctx->sim_values.as<double>(), ctx->sim_rhs.as<double>(), dx, nullptr,
+                           static_cast<int>(s), static_cast<int>(nnz), 0, st);
+                    stats.wall_time_ns +=
+                        std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count();
+                } else {  // run_strategy (simulate.cpp:134-147)
+                    bc_report rep{};
+                    const auto t0 = Clock::now();
+                    const int rc = bc_solve(ctx, &sp, ctx->sim_values.as<double>(), ctx->sim_rhs.as<double>(), dx,
+                                            nullptr, nullptr, nullptr, &rep);
+                    const int64_t wall =
+                        std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count();
+                    if (rc != BC_OK) throw Status(rc, ctx->err);
+                    stats.iterations_effective += rep.iterations_effective;
+                    stats.iterations_sum += rep.iterations_sum;
+                    stats.max_residual_rms = std::max(stats.max_residual_rms, rep.max_residual_rms);
+                    stats.wall_time_ns += wall;
+                    stats.breakdown_fallbacks += rep.breakdown_fallbacks;
+                }
+                // y += dy; |dy|_inf, |y|_inf, non-finite count (simulate.cpp:139-164)
+                check_cuda(cudaMemsetAsync(red, 0, 3 * sizeof(unsigned long long), st), "memset");
+                bc::newton_update_kernel<<<ew_blocks, 256, 0, st>>>(bc::UpdateParams{ny, y, dx, red});
+                check_cuda(cudaGetLastError(), "newton_update_kernel launch");
+                ctx->launches++;
+                unsigned long long h[3];
+                check_cuda(cudaMemcpyAsync(h, red, sizeof h, cudaMemcpyDeviceToHost, st), "D2H norms");
+                check_cuda(cudaStreamSynchronize(st), "newton update");
+                stats.newton_iterations = newton;
+                if (h[2]) {
+                    if (abort_step) *abort_step = step;
+                    fail(BC_ERR_SOLVER_ABORT, "non-finite concentration at step " + std::to_string(step));
+                }
+                double update_inf, state_inf;
+                std::memcpy(&update_inf, &h[0], 8);
+                std::memcpy(&state_inf, &h[1], 8);
+                if (update_inf < prm->newton_rtol * state_inf) break;
+            }
+            check_cuda(cudaMemsetAsync(red, 0, sizeof(unsigned long long), st), "memset");
+            bc::clip_kernel<<<ew_blocks, 256, 0, st>>>(ny, y, red);
+            check_cuda(cudaGetLastError(), "clip_kernel launch");
+            ctx->launches++;
+            unsigned long long clips = 0;
+            check_cuda(cudaMemcpyAsync(&clips, red, sizeof clips, cudaMemcpyDeviceToHost, st), "D2H clips");
+            check_cuda(cudaStreamSynchronize(st), "clip");
+            stats.clip_events = static_cast<int64_t>(clips);
+            per_step[step] = stats;
+        }
+        check_cuda(cudaMemcpyAsync(states, y, yb, cudaMemcpyDefault, st), "D2H states");
+        check_cuda(cudaStreamSynchronize(st), "states");
         return BC_OK;
     });
 }

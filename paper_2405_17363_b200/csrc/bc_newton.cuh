@@ -66,4 +66,79 @@ __global__ void __launch_bounds__(128) newton_assemble_kernel(const NewtonParams
     }
 }
 
+// Newton update of the device-resident simulation (simulate.cpp:139-165):
+// y += dy for every species of every cell, then max |dy| (update_inf) and
+// max |y| (state_inf) over the batch and a count of non-finite states.  The
+// host loop's `m = std::max(m, std::abs(v))` keeps m when v is NaN; the
+// `m < |v|` test below does the same.  max is exact and order-free, so the
+// block/atomic reduction is bit-equal to the host loop.  Non-negative
+// doubles order like their bit patterns: atomicMax on the 64-bit words.
+struct UpdateParams {
+    int64_t n;                // cells * species
+    double* y;
+    const double* dy;
+    unsigned long long* red;  // [0] update_inf bits, [1] state_inf bits, [2] non-finite count
+};
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, v, m);
+        if (v < o) v = o;
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(256) newton_update_kernel(const UpdateParams p) {
+    __shared__ double s_u[8], s_s[8];
+    __shared__ unsigned int s_bad;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    double mu = 0.0, ms = 0.0;
+    unsigned int bad = 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < p.n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double d = p.dy[i];
+        const double ad = fabs(d);
+        if (mu < ad) mu = ad;
+        const double v = __dadd_rn(p.y[i], d);
+        p.y[i] = v;
+        if (!isfinite(v)) ++bad;
+        const double av = fabs(v);
+        if (ms < av) ms = av;
+    }
+    mu = warp_max(mu);
+    ms = warp_max(ms);
+    if (bad) atomicAdd(&s_bad, bad);
+    const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+    if (l == 0) {
+        s_u[w] = mu;
+        s_s[w] = ms;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 1; q < static_cast<int>(blockDim.x / 32); ++q) {
+            if (mu < s_u[q]) mu = s_u[q];
+            if (ms < s_s[q]) ms = s_s[q];
+        }
+        atomicMax(&p.red[0], static_cast<unsigned long long>(__double_as_longlong(mu)));
+        atomicMax(&p.red[1], static_cast<unsigned long long>(__double_as_longlong(ms)));
+        if (s_bad) atomicAdd(&p.red[2], static_cast<unsigned long long>(s_bad));
+    }
+}
+
+// End-of-step clipping (simulate.cpp:168-174): v < 0 -> 0, counted.
+__global__ void __launch_bounds__(256) clip_kernel(int64_t n, double* y, unsigned long long* count) {
+    unsigned int c = 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        if (y[i] < 0.0) {
+            y[i] = 0.0;
+            ++c;
+        }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) c += __shfl_xor_sync(0xffffffffu, c, m);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, static_cast<unsigned long long>(c));
+}
+
 }  // namespace bc

@@ -83,6 +83,8 @@ def ref() -> C.CDLL:
         lib.ref_plan_reduce.argtypes = [_p, _i64, _p, _i64]
         lib.ref_mechanism_pattern.argtypes = [_i64, _i64, C.c_uint64, C.POINTER(_i64), _p, _p]
         lib.ref_newton_batch.argtypes = [_i64, _i64, C.c_uint64, _i64, _i64, _i64, C.c_int, _f64, _p, _p]
+        lib.ref_run_simulation.argtypes = [_i64, _i64, C.c_uint64, _i64, C.c_int, _i64, _f64, _f64, _i64, C.c_int,
+                                           _i64, C.c_int, _f64, _i64, _i64, _p, _p, C.POINTER(_i64)]
         _ref = lib
     return _ref
 
@@ -171,3 +173,79 @@ def lu_solve(which, row_ptr, col_idx, vals, b):
 
 def bits(a) -> np.ndarray:
     return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+# --- run_simulation (simulate.cpp:72-178) ------------------------------------
+
+STEP_FIELDS = ("step", "newton_iterations", "iterations_effective", "iterations_sum", "max_residual_rms",
+               "wall_time_ns", "breakdown_fallbacks", "clip_events")
+
+
+class RefStepStats(C.Structure):
+    _fields_ = [(f, _f64 if f == "max_residual_rms" else _i64) for f in STEP_FIELDS]
+
+
+class SimOut:
+    def __init__(self, states, per_step, abort_step):
+        self.states, self.per_step, self.abort_step = states, per_step, abort_step
+
+
+def ref_run_simulation(species, reactions, seed, cells, mode, steps, dt, tol, max_iter, strategy, k, direct,
+                       newton_rtol=1e-10, max_newton=10, states=None, workers=1):
+    """The reference's own run_simulation (oracle/_ref).  strategy: 0 one-cell,
+    1 multi-cells, 2 block-cells (k 0 = "N")."""
+    y = np.ones((cells, species)) if states is None else np.array(states, np.float64, order="C", copy=True)
+    stats = (RefStepStats * max(1, steps))()
+    ab = _i64(-1)
+    st = ref().ref_run_simulation(species, reactions, seed, cells, mode, steps, dt, tol, max_iter, strategy, k,
+                                  int(direct), newton_rtol, max_newton, workers, ptr(y), stats, C.byref(ab))
+    per_step = [{f: getattr(stats[i], f) for f in STEP_FIELDS} for i in range(steps)] if st == 0 else []
+    return st, SimOut(y, per_step, ab.value)
+
+
+def orc_run_simulation(mech, cells, mode, steps, dt, tol, max_iter, strategy, k, algo, direct, newton_rtol=1e-10,
+                       max_newton=10, states=None, workers=8):
+    """Restatement of run_simulation (simulate.cpp:72-178) over the checkers:
+    the workload generator's Newton systems (bcw_newton_batch: A = I - hJ(y),
+    b = -(y - y_prev - h f(y)), simulate.cpp:29-42) solved by the C oracle
+    (orc_solve_batch, any algorithm) or its dense LU (direct), then the
+    update, the max-norm Newton test, SolverAbort on a non-finite state and
+    end-of-step clipping, in the reference's order.  Returns (status, SimOut):
+    status -9 = SolverAbort (abort_step set)."""
+    y = np.ones((cells, mech.species)) if states is None else np.array(states, np.float64, order="C", copy=True)
+    per_step = []
+    for step in range(steps):
+        prev = y.copy()
+        rec = dict(step=step, newton_iterations=0, iterations_effective=0, iterations_sum=0, max_residual_rms=0.0,
+                   wall_time_ns=0, breakdown_fallbacks=0, clip_events=0)
+        for newton in range(1, max_newton + 1):
+            v, b = mech.newton_batch(0, cells, cells, dt, mode, y=y, y_prev=prev)
+            if direct:
+                dx = np.empty_like(y)
+                for c in range(cells):
+                    st, dx[c] = lu_solve("orc", mech.row_ptr, mech.col_idx, v[c], b[c])
+                    if st != 0:
+                        return st, SimOut(y, per_step, -1)
+            else:
+                st, res = orc_solve_batch(strategy, algo, k, mech.row_ptr, mech.col_idx, v, b, tol, max_iter,
+                                          workers=workers)
+                if st != 0:
+                    return st, SimOut(y, per_step, -1)
+                dx = res.x
+                rec["iterations_effective"] += res.report.iterations_effective
+                rec["iterations_sum"] += res.report.iterations_sum
+                rec["max_residual_rms"] = max(rec["max_residual_rms"], res.report.max_residual_rms)
+                rec["breakdown_fallbacks"] += res.report.breakdown_fallbacks
+            update_inf = float(np.fmax.reduce(np.abs(dx).ravel(), initial=0.0))  # std::max keeps a on NaN
+            y = y + dx
+            rec["newton_iterations"] = newton
+            if not np.isfinite(y).all():
+                return -9, SimOut(y, per_step, step)
+            state_inf = float(np.abs(y).max(initial=0.0))
+            if update_inf < newton_rtol * state_inf:
+                break
+        neg = y < 0.0
+        rec["clip_events"] = int(neg.sum())
+        y[neg] = 0.0
+        per_step.append(rec)
+    return 0, SimOut(y, per_step, -1)
