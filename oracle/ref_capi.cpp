@@ -5,7 +5,7 @@
 // reference arm / cpu_baseline leg.  No reference source is copied here; this
 // file only converts plain arrays to the reference's types and calls its
 // public API (strategies.hpp:60-82, bicg.hpp:42-48, dense_lu.hpp:28-33,
-// mechanism.hpp:45-125, simulate.hpp:29-32).
+// mechanism.hpp:45-125, simulate.hpp:29-32, bench.hpp:69-104, format.hpp).
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -13,7 +13,9 @@
 #include <stdexcept>
 #include <vector>
 
+#include "blockcells/bench.hpp"
 #include "blockcells/bicg.hpp"
+#include "blockcells/format.hpp"
 #include "blockcells/dense_lu.hpp"
 #include "blockcells/exec_model.hpp"
 #include "blockcells/mechanism.hpp"
@@ -274,5 +276,112 @@ int ref_run_simulation(int64_t species, int64_t reactions, uint64_t seed, int64_
         return map_exception();
     }
 }
+
+// format_double (format.cpp:9-14) into buf (>= 64 bytes).
+int ref_format_double(double v, char* buf) {
+    try {
+        const std::string t = format_double(v);
+        std::memcpy(buf, t.c_str(), t.size() + 1);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+namespace {
+std::string g_text;  // last text result of the bench wrappers
+}
+
+// bench::to_csv (bench.cpp:189-218) of n rows given column-wise; strategy
+// names are one NUL-separated block.  The text stays in ref_last_text().
+int ref_to_csv(int64_t n, const int64_t* step, const char* strategies, const int64_t* cells,
+               const int64_t* species, const double* cpb, const int64_t* it_eff, const int64_t* it_sum,
+               const int64_t* wall, const double* rms, const int64_t* fallbacks, const int64_t* clips) {
+    try {
+        std::vector<bench::StepRecord> raw(static_cast<std::size_t>(n));
+        const char* name = strategies;
+        for (int64_t i = 0; i < n; ++i) {
+            raw[i].step = static_cast<std::size_t>(step[i]);
+            raw[i].strategy = name;
+            name += raw[i].strategy.size() + 1;
+            raw[i].cells = static_cast<std::size_t>(cells[i]);
+            raw[i].species = static_cast<std::size_t>(species[i]);
+            raw[i].cells_per_block = cpb[i];
+            raw[i].iterations_effective = static_cast<std::size_t>(it_eff[i]);
+            raw[i].iterations_sum = static_cast<std::size_t>(it_sum[i]);
+            raw[i].wall_ns = wall[i];
+            raw[i].max_residual_rms = rms[i];
+            raw[i].breakdown_fallbacks = static_cast<std::size_t>(fallbacks[i]);
+            raw[i].clip_events = static_cast<std::size_t>(clips[i]);
+        }
+        g_text = bench::to_csv(raw);
+        if (bench::parse_csv(g_text) != raw) return -8;
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// The reference reads a summary.json back (summary_stats_from_json,
+// bench.cpp:332-357) and writes it again (summary_to_json) for the given
+// config: strategies as kind (0/1/2) + k (0 = "N").  Text in ref_last_text().
+int ref_summary_roundtrip(const char* json_in, int64_t cells, int64_t species, int64_t steps, double dt,
+                          int mode, int64_t n_strat, const int32_t* kinds, const int64_t* ks, double tol,
+                          int64_t max_iter, uint64_t seed, int64_t workers, const char* output_path) {
+    try {
+        bench::ExperimentConfig cfg;
+        cfg.cells = static_cast<std::size_t>(cells);
+        cfg.species = static_cast<std::size_t>(species);
+        cfg.steps = static_cast<std::size_t>(steps);
+        cfg.dt_seconds = dt;
+        cfg.mode = mode == 0 ? ConditionMode::Ideal : ConditionMode::Realistic;
+        for (int64_t i = 0; i < n_strat; ++i) {
+            StrategyConfig sc;
+            sc.kind = kinds[i] == 0 ? Strategy::OneCell : kinds[i] == 1 ? Strategy::MultiCells : Strategy::BlockCells;
+            if (ks[i] > 0) sc.cells_per_block = static_cast<std::size_t>(ks[i]);
+            cfg.strategies.push_back(sc);
+        }
+        cfg.tol = tol;
+        cfg.max_iter = static_cast<std::size_t>(max_iter);
+        cfg.seed = seed;
+        cfg.worker_count = static_cast<std::size_t>(workers);
+        cfg.output_path = output_path;
+        const bench::AggregateStats stats = bench::summary_stats_from_json(json_in);
+        g_text = bench::summary_to_json(cfg, stats);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// plan_kernel + occupancy_estimate + memory_estimate (exec_model.cpp:102-200)
+// as the summary's JSON fragments, text in ref_last_text().
+int ref_plan_json(int kind, int64_t cells, int64_t species, int64_t k, int64_t mtpb) {
+    try {
+        DeviceSpec dev;
+        dev.max_threads_per_block = static_cast<std::size_t>(mtpb);
+        if (dev.max_threads_per_sm < dev.max_threads_per_block) dev.max_threads_per_sm = dev.max_threads_per_block;
+        const Strategy st = kind == 0 ? Strategy::OneCell : kind == 1 ? Strategy::MultiCells : Strategy::BlockCells;
+        std::optional<std::size_t> req;
+        if (k > 0) req = static_cast<std::size_t>(k);
+        const KernelPlan plan = plan_kernel(st, static_cast<std::size_t>(cells), static_cast<std::size_t>(species),
+                                            dev, st == Strategy::BlockCells ? req : std::nullopt);
+        const OccupancyEstimate occ = occupancy_estimate(plan, dev);
+        const auto opt = st == Strategy::BlockCells ? req : std::nullopt;
+        g_text = kernel_plan_to_json(plan) + "\n" + format_double(occ.value) + " " +
+                 (occ.shared_mem_exceeded ? "1" : "0") + " " +
+                 std::to_string(memory_estimate(st, static_cast<std::size_t>(cells),
+                                                static_cast<std::size_t>(species), 9, dev, opt)) +
+                 " " +
+                 std::to_string(memory_estimate(st, static_cast<std::size_t>(cells),
+                                                static_cast<std::size_t>(species), BicgWorkspace::aux_array_count(),
+                                                dev, opt));
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+const char* ref_last_text() { return g_text.c_str(); }
 
 }  // extern "C"

@@ -83,6 +83,12 @@ def ref() -> C.CDLL:
         lib.ref_plan_reduce.argtypes = [_p, _i64, _p, _i64]
         lib.ref_mechanism_pattern.argtypes = [_i64, _i64, C.c_uint64, C.POINTER(_i64), _p, _p]
         lib.ref_newton_batch.argtypes = [_i64, _i64, C.c_uint64, _i64, _i64, _i64, C.c_int, _f64, _p, _p]
+        lib.ref_format_double.argtypes = [_f64, C.c_char_p]
+        lib.ref_to_csv.argtypes = [_i64, _p, C.c_char_p] + [_p] * 9
+        lib.ref_summary_roundtrip.argtypes = [C.c_char_p, _i64, _i64, _i64, _f64, C.c_int, _i64, _p, _p, _f64, _i64,
+                                              C.c_uint64, _i64, C.c_char_p]
+        lib.ref_plan_json.argtypes = [C.c_int, _i64, _i64, _i64, _i64]
+        lib.ref_last_text.restype = C.c_char_p
         lib.ref_run_simulation.argtypes = [_i64, _i64, C.c_uint64, _i64, C.c_int, _i64, _f64, _f64, _i64, C.c_int,
                                            _i64, C.c_int, _f64, _i64, _i64, _p, _p, C.POINTER(_i64)]
         _ref = lib
