@@ -287,25 +287,28 @@ int pipe_chunks() {  // BC_PIPE_CHUNKS overrides the default 32
 constexpr int64_t kPipeMinCells = 4096;
 
 struct TmemCfg {
-    int R, RV, warps, ST, CP;  // warps per CTA (= 4 * groups per lane quarter), row streams, gather copies
-    TmemFn fn;
+    int R, RV, warps, ST, CP, ALGO;  // warps per CTA (= 4 * groups per lane quarter), row streams,
+    TmemFn fn;                       // gather copies, bc::AlgoKind
 };
 
-// 16 warps/SM at <= 128 registers; 8 warps (<= 255 registers) for schedules
-// too long for 3 groups per quarter (the scaled mechanism: 312 species).
-// Each with one or two row streams and one or two gather-vector copies.
-#define BC_TMEM_CFG1(R, RV, W, ST, CP) \
-    { R, RV, W, ST, CP, &bc::block_cells_tmem_kernel<R, RV, 32 * W, ST, CP> }
-#define BC_TMEM_CFG(R, RV, W)                                                                  \
-    BC_TMEM_CFG1(R, RV, W, 1, 1), BC_TMEM_CFG1(R, RV, W, 1, 2), BC_TMEM_CFG1(R, RV, W, 2, 1), \
-        BC_TMEM_CFG1(R, RV, W, 2, 2)
+// Jacobi-BiCGSTAB: 16 warps/SM at <= 128 registers; 8 warps (<= 255
+// registers) for schedules too long for 3 groups per quarter (the scaled
+// mechanism: 312 species); one or two row streams, one or two gather copies.
+// BiCG: its pair schedule (A and A^T in one pass) is twice as long, so 8
+// warps/SM at M156 and 4 at M312; two streams.
+#define BC_TMEM_CFG1(R, RV, W, ST, CP, A) \
+    { R, RV, W, ST, CP, A, &bc::block_cells_tmem_kernel<R, RV, 32 * W, ST, CP, A> }
+#define BC_TMEM_CFG(R, RV, W)                                                                          \
+    BC_TMEM_CFG1(R, RV, W, 1, 1, bc::kBiCGStab), BC_TMEM_CFG1(R, RV, W, 1, 2, bc::kBiCGStab),           \
+        BC_TMEM_CFG1(R, RV, W, 2, 1, bc::kBiCGStab), BC_TMEM_CFG1(R, RV, W, 2, 2, bc::kBiCGStab)
+#define BC_TMEM_CFG_BICG(R, RV, W) \
+    BC_TMEM_CFG1(R, RV, W, 2, 1, bc::kBiCG), BC_TMEM_CFG1(R, RV, W, 2, 2, bc::kBiCG)
 const TmemCfg kTmemConfigs[] = {
-    BC_TMEM_CFG(8, 5, 16),
-    BC_TMEM_CFG(8, 8, 16),
-    BC_TMEM_CFG(4, 4, 16),
-    BC_TMEM_CFG(16, 10, 8),
+    BC_TMEM_CFG(8, 5, 16),       BC_TMEM_CFG(8, 8, 16),       BC_TMEM_CFG(4, 4, 16),      BC_TMEM_CFG(16, 10, 8),
+    BC_TMEM_CFG_BICG(8, 5, 8),   BC_TMEM_CFG_BICG(8, 8, 8),   BC_TMEM_CFG_BICG(4, 4, 8),  BC_TMEM_CFG_BICG(16, 10, 4),
 };
 #undef BC_TMEM_CFG
+#undef BC_TMEM_CFG_BICG
 #undef BC_TMEM_CFG1
 
 int tmem_warps_pref() {
@@ -318,7 +321,7 @@ bool tmem_disabled() {
     return e && std::string(e) == "v1";
 }
 
-// The TMEM kernel (bc_tmem.cuh): Jacobi-BiCGSTAB, one warp per group, schedule
+// The TMEM kernel (bc_tmem.cuh): BiCG or Jacobi-BiCGSTAB, one warp per group, schedule
 // words + per-group values resident in Tensor Memory.  Returns false when the
 // group does not qualify (the caller then uses the v1 kernel).
 // Largest sigma with sqrt(sigma / n) <= tol, both correctly rounded (x86-64
@@ -347,34 +350,39 @@ double sigma_threshold(double tol, int n) {
 // reduction tree is the full Q = P/32 slots per lane (Q <= 16 instantiated).
 bool tmem_fits(const bc::GroupPlan& gp) { return gp.geo.P >= 32 && gp.geo.Q <= 16; }
 
+// BiCG plans (built with the transpose) get the pair schedule: A p and A^T p~
+// in one pass.
 void ensure_tmem_schedule(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp) {
     if (gp.has_tm || tmem_disabled() || !tmem_fits(gp)) return;
-    gp.tm = bc::build_tmem_schedule(pat, gp.k);
+    gp.tm = bc::build_tmem_schedule(pat, gp.k, gp.at.steps > 0);
     gp.d_tm_words = upload(ctx, gp.tm.words);
     gp.d_tm_vidx = upload(ctx, gp.tm.vidx);
     gp.has_tm = true;
 }
 
 // Per-lane owner tables for a kernel instance with RV row slots: copy-0
-// gather slot | Y slot << 16, and copy 1's slots two row slots per word; rows
-// >= n go to the trash slot (after every copy) and read the zero Y slot.
+// gather slot | Y slot << 16, and copy 1's slots two row slots per word; for a
+// pair schedule the same again for p~ and the A^T outputs.  Rows >= n go to
+// the trash slot (after every copy) and read the zero Y slot.
 void ensure_tmem_lane_tables(bc_ctx* ctx, bc::GroupPlan& gp, int RV) {
     if (gp.tm_lane_rv == RV) return;
-    const int n = gp.geo.n, trash = gp.tm.xslots;
-    std::vector<uint32_t> xy(static_cast<size_t>(RV) * 32);
-    std::vector<uint32_t> x1(static_cast<size_t>((RV + 1) / 2) * 32, 0u);
-    for (int j = 0; j < RV; ++j)
-        for (int l = 0; l < 32; ++l) {
-            const int row = j * 32 + l;
-            const bool ok = row < n;
-            xy[j * 32 + l] = static_cast<uint32_t>(ok ? gp.tm.xpos[row] : trash) |
-                             (static_cast<uint32_t>(ok ? gp.tm.yslot[row] : gp.tm.yslots) << 16);
-            const uint32_t s1 =
-                static_cast<uint32_t>(ok && gp.tm.copies > 1 ? gp.tm.xpos[static_cast<size_t>(n) + row] : trash);
-            x1[(j / 2) * 32 + l] |= s1 << (16 * (j % 2));
-        }
-    gp.d_tm_lane_xy = upload(ctx, xy);
-    gp.d_tm_lane_x1 = upload(ctx, x1);
+    const int n = gp.geo.n, trash = gp.tm.xslots, nx = gp.tm.pair ? 2 * n : n;
+    for (int part = 0; part < (gp.tm.pair ? 2 : 1); ++part) {
+        std::vector<uint32_t> xy(static_cast<size_t>(RV) * 32);
+        std::vector<uint32_t> x1(static_cast<size_t>((RV + 1) / 2) * 32, 0u);
+        for (int j = 0; j < RV; ++j)
+            for (int l = 0; l < 32; ++l) {
+                const int row = j * 32 + l, col = part * n + row;
+                const bool ok = row < n;
+                xy[j * 32 + l] = static_cast<uint32_t>(ok ? gp.tm.xpos[col] : trash) |
+                                 (static_cast<uint32_t>(ok ? gp.tm.yslot[col] : gp.tm.yslots) << 16);
+                const uint32_t s1 =
+                    static_cast<uint32_t>(ok && gp.tm.copies > 1 ? gp.tm.xpos[static_cast<size_t>(nx) + col] : trash);
+                x1[(j / 2) * 32 + l] |= s1 << (16 * (j % 2));
+            }
+        (part ? gp.d_tm_lane_xyT : gp.d_tm_lane_xy) = upload(ctx, xy);
+        (part ? gp.d_tm_lane_x1T : gp.d_tm_lane_x1) = upload(ctx, x1);
+    }
     gp.tm_lane_rv = RV;
 }
 
@@ -385,13 +393,14 @@ int tmem_groups_per_quarter(int S) { return S > 0 ? std::min(4, (512 - S / 2) / 
 // Kernel instance for a plan: same tree width R, enough row slots, and the
 // most warps the schedule's TMEM footprint allows (capped by BC_TMEM_WARPS).
 const TmemCfg* pick_tmem_cfg(const bc::GroupPlan& gp) {
+    const int algo = gp.tm.pair ? bc::kBiCG : bc::kBiCGStab;
     const int cpq = tmem_groups_per_quarter(gp.tm.steps);
     if (cpq < 1) return nullptr;
     const int want = std::min(4 * cpq, tmem_warps_pref());
     const TmemCfg* cfg = nullptr;
     for (const TmemCfg& t : kTmemConfigs) {
         if (t.R != gp.geo.Q || t.RV < (gp.geo.n + 31) / 32 || t.warps < want || t.ST != gp.tm.streams ||
-            t.CP != gp.tm.copies)
+            t.CP != gp.tm.copies || t.ALGO != algo)
             continue;
         if (!cfg || t.warps < cfg->warps || (t.warps == cfg->warps && t.RV < cfg->RV)) cfg = &t;
     }
@@ -431,6 +440,8 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
     p.didx = gp.d_didx;
     p.lane_xy = gp.d_tm_lane_xy;
     p.lane_x1 = gp.d_tm_lane_x1;
+    p.lane_xyT = gp.d_tm_lane_xyT;
+    p.lane_x1T = gp.d_tm_lane_x1T;
     p.counter = counter;
     p.cell_offset = cell0;
     p.group_offset = gout0;
@@ -830,11 +841,12 @@ int bc_schedule_export(int32_t species, const int32_t* row_ptr, const int32_t* c
 }
 
 int bc_tmem_schedule_export(int32_t species, const int32_t* row_ptr, const int32_t* col_idx, int32_t k,
-                            int32_t* info, uint16_t* words, int32_t* vidx, int32_t* xpos, int32_t* yslot) {
+                            int32_t pair, int32_t* info, uint16_t* words, int32_t* vidx, int32_t* xpos,
+                            int32_t* yslot) {
     if (!info || k < 1) return BC_ERR_INVALID_ARGUMENT;
     return guarded(nullptr, [&] {
         const bc::Pattern pat = make_pattern(species, row_ptr, col_idx);
-        const bc::TmemSchedule ts = bc::build_tmem_schedule(pat, k);
+        const bc::TmemSchedule ts = bc::build_tmem_schedule(pat, k, pair != 0);
         const int v[9] = {ts.steps,  ts.xslots,      ts.zero_slot, ts.yslots, ts.conflict_cost,
                           ts.copies, ts.model_total, ts.streams,   ts.ystream};
         std::memcpy(info, v, sizeof v);
@@ -938,7 +950,7 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
         } else {
             for (const GroupSpan& sp : spans) {  // host-side planning before the timed region
                 bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);
-                if (!bicg) {
+                {
                     ensure_tmem_schedule(ctx, pat, gp);
                     if (gp.has_tm)
                         if (const TmemCfg* t = pick_tmem_cfg(gp)) ensure_tmem_lane_tables(ctx, gp, t->RV);
@@ -1026,7 +1038,7 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
             const GroupSpan& sp = spans[i];
             bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);
             unsigned int* counter = ctx->counters.as<unsigned int>() + slot++;
-            if (bicg || !launch_tmem(ctx, pat, gp, sp.cell0, sp.gout0, sp.count, d_values, d_rhs, d_x, prm->tol,
+            if (!launch_tmem(ctx, pat, gp, sp.cell0, sp.gout0, sp.count, d_values, d_rhs, d_x, prm->tol,
                                      prm->max_iter, counter, st, gates[i]))
                 launch_block(ctx, pat, gp, prm->algo, sp.cell0, sp.gout0, sp.count, d_values, d_rhs, nullptr, d_x,
                              prm->tol, prm->max_iter, counter, st, gates[i]);

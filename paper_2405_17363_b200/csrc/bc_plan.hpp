@@ -79,6 +79,8 @@ struct TmemSchedule {
     std::vector<int32_t> yslot;     // group row -> Y slot (stream*ystream + k*32 + lane)
     int yslots = 0;
     int streams = 1;                // interleaved row streams per lane (1 or 2)
+    int pair = 0;                   // BiCG: A rows on stream 0, A^T rows on stream 1 (xpos: [copy][2n],
+                                    // columns n + i gather p~; yslot: [2n], A^T output j at n + j)
     int ystream = 32;               // Y slots per stream
     int conflict_cost = 0;          // modelled gather wavefronts per pass
 };
@@ -108,9 +110,11 @@ struct GroupPlan {
     int tm_lane_rv = 0;               // RV the lane tables below were built for
     uint32_t* d_tm_lane_xy = nullptr;
     uint32_t* d_tm_lane_x1 = nullptr;
+    uint32_t* d_tm_lane_xyT = nullptr;  // pair schedules: p~ / A^T tables
+    uint32_t* d_tm_lane_x1T = nullptr;
 };
 
-TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize = true);
+TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair = false, bool optimize = true);
 
 Schedule build_schedule(const Pattern& pat, int k, int lanes, bool transpose, bool optimize = true);
 GroupPlan build_group_plan(const Pattern& pat, int k, bool with_transpose, bool optimize = true);

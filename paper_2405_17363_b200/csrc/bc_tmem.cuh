@@ -53,6 +53,8 @@ struct TmemParams {
     const int32_t* didx;    // n: group value index of the diagonal, -1 if none
     const uint32_t* lane_xy;  // RV * 32: copy-0 gather slot | Y slot << 16 per (slot j, lane)
     const uint32_t* lane_x1;  // ((RV+1)/2) * 32: copy-1 gather slots, two row slots per word
+    const uint32_t* lane_xyT; // BiCG pair schedules: the same two tables for p~ / A^T p~
+    const uint32_t* lane_x1T;
     unsigned int* counter;
     int64_t cell_offset, group_offset;
     int group_count;
@@ -125,6 +127,8 @@ struct TmemWarp {
     uint32_t xaddr;         // shared address of Xs (aligned, see gaddr_lo)
     uint32_t xy[RV];        // copy-0 gather slot | Y slot << 16 of row slot j
     uint32_t x1[(RV + 1) / 2];  // copy-1 gather slots (CP = 2), row slots 2i | 2i+1 << 16
+    uint32_t xyT[RV];       // BiCG pair: the same for p~ and the A^T outputs
+    uint32_t x1T[(RV + 1) / 2];
     int lane;
     uint32_t wcol, vcol;    // TMEM addresses: words, this warp's values
     int S;
@@ -182,17 +186,22 @@ __device__ __forceinline__ void tmem_chunk4(uint32_t xaddr, uint32_t w0, uint32_
     }
 }
 
-// y = A x: publish x into every copy of the gather vector, walk the
-// TMEM-resident schedule (8 steps per tcgen05.ld pair, then a 4-step tail;
-// other warps hide the latency), collect the row sums from Y.
-template <int ST, int CP, int RV>
-__device__ __forceinline__ void tmem_spmv(const TmemWarp<RV>& tw, const double (&x)[RV], double (&y)[RV]) {
+// Publish x into every copy of the gather vector: copy-0 slot in the low half
+// of xy[j], copy-1 slot in x1 (two row slots per word).
+template <int CP, int RV>
+__device__ __forceinline__ void tmem_publish(double* Xs, const uint32_t (&xy)[RV], const uint32_t (&x1)[(RV + 1) / 2],
+                                             const double (&x)[RV]) {
 #pragma unroll
     for (int j = 0; j < RV; ++j) {
-        tw.Xs[tw.xy[j] & 0xFFFFu] = x[j];
-        if constexpr (CP == 2) tw.Xs[(tw.x1[j >> 1] >> (16 * (j & 1))) & 0xFFFFu] = x[j];
+        Xs[xy[j] & 0xFFFFu] = x[j];
+        if constexpr (CP == 2) Xs[(x1[j >> 1] >> (16 * (j & 1))) & 0xFFFFu] = x[j];
     }
-    __syncwarp();
+}
+
+// Walk the TMEM-resident schedule (8 steps per tcgen05.ld pair, then a 4-step
+// tail; other warps hide the latency), row sums into Y.
+template <int ST, int RV>
+__device__ __forceinline__ void tmem_walk(const TmemWarp<RV>& tw) {
     double* yp[ST];
     double acc[ST];
 #pragma unroll
@@ -216,9 +225,35 @@ __device__ __forceinline__ void tmem_spmv(const TmemWarp<RV>& tw, const double (
         tm_wait_ld();
         tmem_chunk4<ST>(tw.xaddr, w[0], w[1], v, acc, yp);
     }
+}
+
+// y = A x (for a BiCG pair schedule the A^T stream runs on whatever p~ holds
+// and its outputs are ignored).
+template <int ST, int CP, int RV>
+__device__ __forceinline__ void tmem_spmv(const TmemWarp<RV>& tw, const double (&x)[RV], double (&y)[RV]) {
+    tmem_publish<CP>(tw.Xs, tw.xy, tw.x1, x);
+    __syncwarp();
+    tmem_walk<ST>(tw);
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < RV; ++j) y[j] = tw.Ys[tw.xy[j] >> 16];
+}
+
+// BiCG's two products in one pass of the pair schedule: A p on stream 0,
+// A^T p~ on stream 1 (bc_tmem_plan.cpp, pair mode).
+template <int CP, int RV>
+__device__ __forceinline__ void tmem_spmv_pair(const TmemWarp<RV>& tw, const double (&pv)[RV],
+                                               const double (&ps)[RV], double (&ap)[RV], double (&atps)[RV]) {
+    tmem_publish<CP>(tw.Xs, tw.xy, tw.x1, pv);
+    tmem_publish<CP>(tw.Xs, tw.xyT, tw.x1T, ps);
+    __syncwarp();
+    tmem_walk<2>(tw);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < RV; ++j) {
+        ap[j] = tw.Ys[tw.xy[j] >> 16];
+        atps[j] = tw.Ys[tw.xyT[j] >> 16];
+    }
 }
 
 // Reduce NV values over the group: team_reduce<W = 1> with its
@@ -262,7 +297,7 @@ __device__ __forceinline__ double tmem_fresh_rms(const Ctx<1, R, RV>& c, const T
     return __dsqrt_rn(ddiv(out[0], static_cast<double>(c.n)));
 }
 
-template <int R, int RV, int NT, int ST, int CP>
+template <int R, int RV, int NT, int ST, int CP, int ALGO>
 __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t s_taddr;
@@ -321,6 +356,10 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
     for (int j = 0; j < RV; ++j) tw.xy[j] = p.lane_xy[j * 32 + lane];
 #pragma unroll
     for (int i = 0; i < (RV + 1) / 2; ++i) tw.x1[i] = CP == 2 ? p.lane_x1[i * 32 + lane] : 0u;
+#pragma unroll
+    for (int j = 0; j < RV; ++j) tw.xyT[j] = ALGO == kBiCG ? p.lane_xyT[j * 32 + lane] : 0u;
+#pragma unroll
+    for (int i = 0; i < (RV + 1) / 2; ++i) tw.x1T[i] = (ALGO == kBiCG && CP == 2) ? p.lane_x1T[i * 32 + lane] : 0u;
     for (int i = lane; i < p.xslots; i += 32) tw.Xs[i] = 0.0;  // zero slots stay +0.0
     for (int i = lane; i < p.yslots; i += 32) tw.Ys[i] = 0.0;
     __syncwarp();
@@ -355,124 +394,220 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
         tm_wait_st();
         __syncwarp();
 
-        double x[RV], dinv[RV];
+        double x[RV];
 #pragma unroll
-        for (int j = 0; j < RV; ++j) {
-            x[j] = 0.0;
-            const int di = c.valid(j) ? p.didx[c.row(j)] : -1;
-            const double d = di >= 0 ? __ldg(src + di) : 0.0;
-            dinv[j] = c.valid(j) ? (d != 0.0 ? ddiv(1.0, d) : 1.0) : 0.0;
-        }
+        for (int j = 0; j < RV; ++j) x[j] = 0.0;
         int iters = 0;
         bool conv = false, brk = false;
         double fres = 0.0;
-        double r[RV], rh[RV], pv[RV], v[RV];
-        {
-            double ax[RV];
-            tmem_spmv<ST, CP>(tw, x, ax);
+        if constexpr (ALGO == kBiCGStab) {
+            double dinv[RV];
 #pragma unroll
             for (int j = 0; j < RV; ++j) {
-                const double bj = c.valid(j) ? __ldcs(bsrc + c.row(j)) : 0.0;
-                r[j] = dadd(bj, -ax[j]);  // 1*b + (-1)*Ax; rows >= n: 0 + -0 = +0
-                rh[j] = r[j];
-                pv[j] = 0.0;
-                v[j] = 0.0;
+                const int di = c.valid(j) ? p.didx[c.row(j)] : -1;
+                const double d = di >= 0 ? __ldg(src + di) : 0.0;
+                dinv[j] = c.valid(j) ? (d != 0.0 ? ddiv(1.0, d) : 1.0) : 0.0;
             }
-        }
-        double sigma, rho_next;
-        {
-            double q[2][RV], o[2];
-#pragma unroll
-            for (int j = 0; j < RV; ++j) {
-                q[0][j] = dmul(r[j], r[j]);
-                q[1][j] = dmul(rh[j], r[j]);
+            double r[RV], rh[RV], pv[RV], v[RV];
+            {
+                double ax[RV];
+                tmem_spmv<ST, CP>(tw, x, ax);
+    #pragma unroll
+                for (int j = 0; j < RV; ++j) {
+                    const double bj = c.valid(j) ? __ldcs(bsrc + c.row(j)) : 0.0;
+                    r[j] = dadd(bj, -ax[j]);  // 1*b + (-1)*Ax; rows >= n: 0 + -0 = +0
+                    rh[j] = r[j];
+                    pv[j] = 0.0;
+                    v[j] = 0.0;
+                }
             }
-            tmem_reduce<2, R, RV>(q, o);
-            sigma = o[0];
-            rho_next = o[1];
-        }
-        if (sigma <= smax) {
-            fres = tmem_fresh_rms<ST, CP>(c, tw, x, bsrc);
-            conv = fres <= p.tol;
-        }
-        if (!conv) {
-            double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
-            for (int it = 1; it <= p.max_iter; ++it) {
-                const double rho = rho_next;
-                if (scalar_breaks(rho)) { brk = true; break; }
-                const double beta = dmul(ddiv(rho, rho_prev), ddiv(alpha, omega));
-                double y[RV];
-#pragma unroll
+            double sigma, rho_next;
+            {
+                double q[2][RV], o[2];
+    #pragma unroll
                 for (int j = 0; j < RV; ++j) {
-                    pv[j] = dadd(r[j], dmul(beta, dsub(pv[j], dmul(omega, v[j]))));
-                    y[j] = dmul(dinv[j], pv[j]);
+                    q[0][j] = dmul(r[j], r[j]);
+                    q[1][j] = dmul(rh[j], r[j]);
                 }
-                tmem_spmv<ST, CP>(tw, y, v);
-                double den;
-                {
-                    double q[1][RV], o[1];
-#pragma unroll
-                    for (int j = 0; j < RV; ++j) q[0][j] = dmul(rh[j], v[j]);
-                    tmem_reduce<1, R, RV>(q, o);
-                    den = o[0];
-                }
-                if (scalar_breaks(den)) { brk = true; break; }
-                alpha = ddiv(rho, den);
-                double z[RV];
-#pragma unroll
-                for (int j = 0; j < RV; ++j) {
-                    r[j] = dsub(r[j], dmul(alpha, v[j]));                 // r now holds s
-                    z[j] = dmul(dinv[j], r[j]);
-                    x[j] = dadd(x[j], dmul(alpha, dmul(dinv[j], pv[j])));  // y = dinv*p recomputed
-                }
-                double t[RV];
-                tmem_spmv<ST, CP>(tw, z, t);
-                double tt, ts;
-                {
-                    double q[2][RV], o[2];
-#pragma unroll
-                    for (int j = 0; j < RV; ++j) {
-                        q[0][j] = dmul(t[j], t[j]);
-                        q[1][j] = dmul(t[j], r[j]);
-                    }
-                    tmem_reduce<2, R, RV>(q, o);
-                    tt = o[0];
-                    ts = o[1];
-                }
-                if (tt != 0.0 && scalar_breaks(tt)) { brk = true; break; }
-                omega = tt == 0.0 ? 0.0 : ddiv(ts, tt);
-#pragma unroll
-                for (int j = 0; j < RV; ++j) {
-                    x[j] = dadd(x[j], dmul(omega, dmul(dinv[j], r[j])));  // z = dinv*s recomputed
-                    r[j] = dsub(r[j], dmul(omega, t[j]));
-                }
-                rho_prev = rho;
-                iters = it;
-                {
-                    double q[2][RV], o[2];
-#pragma unroll
-                    for (int j = 0; j < RV; ++j) {
-                        q[0][j] = dmul(r[j], r[j]);
-                        q[1][j] = dmul(rh[j], r[j]);
-                    }
-                    tmem_reduce<2, R, RV>(q, o);
-                    sigma = o[0];
-                    rho_next = o[1];
-                }
-                if (!isfinite(sigma)) { brk = true; break; }
-                if (sigma <= smax) {
-                    const double f = tmem_fresh_rms<ST, CP>(c, tw, x, bsrc);
-                    if (f <= p.tol) {
-                        fres = f;
-                        conv = true;
-                        break;
-                    }
-                }
-                if (scalar_breaks(omega)) { brk = true; break; }
+                tmem_reduce<2, R, RV>(q, o);
+                sigma = o[0];
+                rho_next = o[1];
+            }
+            if (sigma <= smax) {
+                fres = tmem_fresh_rms<ST, CP>(c, tw, x, bsrc);
+                conv = fres <= p.tol;
             }
             if (!conv) {
+                double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
+                for (int it = 1; it <= p.max_iter; ++it) {
+                    const double rho = rho_next;
+                    if (scalar_breaks(rho)) { brk = true; break; }
+                    const double beta = dmul(ddiv(rho, rho_prev), ddiv(alpha, omega));
+                    double y[RV];
+    #pragma unroll
+                    for (int j = 0; j < RV; ++j) {
+                        pv[j] = dadd(r[j], dmul(beta, dsub(pv[j], dmul(omega, v[j]))));
+                        y[j] = dmul(dinv[j], pv[j]);
+                    }
+                    tmem_spmv<ST, CP>(tw, y, v);
+                    double den;
+                    {
+                        double q[1][RV], o[1];
+    #pragma unroll
+                        for (int j = 0; j < RV; ++j) q[0][j] = dmul(rh[j], v[j]);
+                        tmem_reduce<1, R, RV>(q, o);
+                        den = o[0];
+                    }
+                    if (scalar_breaks(den)) { brk = true; break; }
+                    alpha = ddiv(rho, den);
+                    double z[RV];
+    #pragma unroll
+                    for (int j = 0; j < RV; ++j) {
+                        r[j] = dsub(r[j], dmul(alpha, v[j]));                 // r now holds s
+                        z[j] = dmul(dinv[j], r[j]);
+                        x[j] = dadd(x[j], dmul(alpha, dmul(dinv[j], pv[j])));  // y = dinv*p recomputed
+                    }
+                    double t[RV];
+                    tmem_spmv<ST, CP>(tw, z, t);
+                    double tt, ts;
+                    {
+                        double q[2][RV], o[2];
+    #pragma unroll
+                        for (int j = 0; j < RV; ++j) {
+                            q[0][j] = dmul(t[j], t[j]);
+                            q[1][j] = dmul(t[j], r[j]);
+                        }
+                        tmem_reduce<2, R, RV>(q, o);
+                        tt = o[0];
+                        ts = o[1];
+                    }
+                    if (tt != 0.0 && scalar_breaks(tt)) { brk = true; break; }
+                    omega = tt == 0.0 ? 0.0 : ddiv(ts, tt);
+    #pragma unroll
+                    for (int j = 0; j < RV; ++j) {
+                        x[j] = dadd(x[j], dmul(omega, dmul(dinv[j], r[j])));  // z = dinv*s recomputed
+                        r[j] = dsub(r[j], dmul(omega, t[j]));
+                    }
+                    rho_prev = rho;
+                    iters = it;
+                    {
+                        double q[2][RV], o[2];
+    #pragma unroll
+                        for (int j = 0; j < RV; ++j) {
+                            q[0][j] = dmul(r[j], r[j]);
+                            q[1][j] = dmul(rh[j], r[j]);
+                        }
+                        tmem_reduce<2, R, RV>(q, o);
+                        sigma = o[0];
+                        rho_next = o[1];
+                    }
+                    if (!isfinite(sigma)) { brk = true; break; }
+                    if (sigma <= smax) {
+                        const double f = tmem_fresh_rms<ST, CP>(c, tw, x, bsrc);
+                        if (f <= p.tol) {
+                            fres = f;
+                            conv = true;
+                            break;
+                        }
+                    }
+                    if (scalar_breaks(omega)) { brk = true; break; }
+                }
+                if (!conv) {
+                    fres = tmem_fresh_rms<ST, CP>(c, tw, x, bsrc);
+                    conv = !brk && fres <= p.tol;
+                }
+            }
+        } else {
+            // BiCG, bicg.cpp:42-142 operation for operation (as block_cells_kernel's
+            // kBiCG branch), A p and A^T p~ in one pass of the pair schedule
+            double r[RV], rs[RV], pv[RV], ps[RV];
+            {
+                double ax[RV];
+                tmem_spmv<ST, CP>(tw, x, ax);
+#pragma unroll
+                for (int j = 0; j < RV; ++j) {
+                    const double bj = c.valid(j) ? __ldcs(bsrc + c.row(j)) : 0.0;
+                    r[j] = dadd(bj, -ax[j]);  // 1*b + (-1)*Ax; rows >= n: 0 + -0 = +0
+                    rs[j] = r[j];
+                    pv[j] = r[j];
+                    ps[j] = r[j];
+                }
+            }
+            double sigma, rho_next;
+            {
+                double q[2][RV], o[2];
+#pragma unroll
+                for (int j = 0; j < RV; ++j) {
+                    q[0][j] = dmul(r[j], r[j]);
+                    q[1][j] = dmul(rs[j], r[j]);
+                }
+                tmem_reduce<2, R, RV>(q, o);
+                sigma = o[0];
+                rho_next = o[1];
+            }
+            if (sigma <= smax) {
                 fres = tmem_fresh_rms<ST, CP>(c, tw, x, bsrc);
-                conv = !brk && fres <= p.tol;
+                conv = fres <= p.tol;
+            }
+            if (!conv) {
+                double rho_prev = 0.0;
+                for (int it = 1; it <= p.max_iter; ++it) {
+                    const double rho = rho_next;
+                    if (scalar_breaks(rho)) { brk = true; break; }
+                    if (it > 1) {
+                        const double beta = ddiv(rho, rho_prev);
+#pragma unroll
+                        for (int j = 0; j < RV; ++j) {
+                            pv[j] = dadd(r[j], dmul(beta, pv[j]));
+                            ps[j] = dadd(rs[j], dmul(beta, ps[j]));
+                        }
+                    }
+                    double ap[RV], atps[RV];
+                    tmem_spmv_pair<CP>(tw, pv, ps, ap, atps);
+                    double den;
+                    {
+                        double q[1][RV], o[1];
+#pragma unroll
+                        for (int j = 0; j < RV; ++j) q[0][j] = dmul(ps[j], ap[j]);
+                        tmem_reduce<1, R, RV>(q, o);
+                        den = o[0];
+                    }
+                    if (scalar_breaks(den)) { brk = true; break; }
+                    const double alpha = ddiv(rho, den);
+                    const double nalpha = -alpha;
+#pragma unroll
+                    for (int j = 0; j < RV; ++j) {
+                        x[j] = dadd(x[j], dmul(alpha, pv[j]));
+                        r[j] = dadd(r[j], dmul(nalpha, ap[j]));
+                        rs[j] = dadd(rs[j], dmul(nalpha, atps[j]));
+                    }
+                    rho_prev = rho;
+                    iters = it;
+                    {
+                        double q[2][RV], o[2];
+#pragma unroll
+                        for (int j = 0; j < RV; ++j) {
+                            q[0][j] = dmul(r[j], r[j]);
+                            q[1][j] = dmul(rs[j], r[j]);
+                        }
+                        tmem_reduce<2, R, RV>(q, o);
+                        sigma = o[0];
+                        rho_next = o[1];
+                    }
+                    if (!isfinite(sigma)) { brk = true; break; }
+                    if (sigma <= smax) {
+                        const double f = tmem_fresh_rms<ST, CP>(c, tw, x, bsrc);
+                        if (f <= p.tol) {
+                            fres = f;
+                            conv = true;
+                            break;
+                        }
+                    }
+                }
+                if (!conv) {
+                    fres = tmem_fresh_rms<ST, CP>(c, tw, x, bsrc);
+                    conv = !brk && fres <= p.tol;
+                }
             }
         }
         double* xdst = p.x_out + cell0 * p.species;

@@ -29,6 +29,9 @@ constexpr int kLanes = 32;
 
 struct TmOpt {
     int S = 0, ncol = 0, nrow = 0, R = 1, NS = 16;
+    // pair: A rows on stream 0 and A^T rows (outputs nrow + j, gathering
+    // columns nrow + i) on stream 1, one pass for BiCG's two products
+    bool pair = false;
     // ST interleaved row streams per lane: virtual lane v = s*32 + L runs on
     // physical lane L, its virtual step u on physical step u*ST + s
     int ST = 1;
@@ -125,31 +128,33 @@ struct TmOpt {
         }
         load[v] = u;
     }
-    int publish_cost() const {  // R*RV STS.64 by the owner lanes (rows 32j+L)
+    int publish_cost() const {  // R*RV STS.64 by the owner lanes (rows 32j+L), twice for a pair
         int tot = 0;
-        for (int r = 0; r < R; ++r)
+        for (int part = 0; part < (pair ? 2 : 1); ++part)
+            for (int r = 0; r < R; ++r)
+                for (int j = 0; j * 32 < nrow; ++j)
+                    for (int h = 0; h < 2; ++h) {
+                        int cnt[16] = {0};
+                        for (int q = 0; q < 16; ++q) {
+                            const int row = 32 * j + 16 * h + q;
+                            if (row < nrow) cnt[bank(r, part * nrow + row)]++;
+                        }
+                        tot += *std::max_element(cnt, cnt + 16);
+                    }
+        return tot;
+    }
+    int yread_cost() const {  // RV LDS.64 of Y[..+k*32+lane(row)]: bank = lane(row) & 15
+        int tot = 0;
+        for (int part = 0; part < (pair ? 2 : 1); ++part)
             for (int j = 0; j * 32 < nrow; ++j)
                 for (int h = 0; h < 2; ++h) {
                     int cnt[16] = {0};
                     for (int q = 0; q < 16; ++q) {
                         const int row = 32 * j + 16 * h + q;
-                        if (row < nrow) cnt[bank(r, row)]++;
+                        if (row < nrow && row_lane[part * nrow + row] >= 0) cnt[row_lane[part * nrow + row] & 15]++;
                     }
                     tot += *std::max_element(cnt, cnt + 16);
                 }
-        return tot;
-    }
-    int yread_cost() const {  // RV LDS.64 of Y[k*32+lane(row)]: bank = lane(row) & 15
-        int tot = 0;
-        for (int j = 0; j * 32 < nrow; ++j)
-            for (int h = 0; h < 2; ++h) {
-                int cnt[16] = {0};
-                for (int q = 0; q < 16; ++q) {
-                    const int row = 32 * j + 16 * h + q;
-                    if (row < nrow && row_lane[row] >= 0) cnt[row_lane[row] & 15]++;
-                }
-                tot += *std::max_element(cnt, cnt + 16);
-            }
         return tot;
     }
     int ystore_cost() const {  // one STS.64 wavefront per half-warp with a row end
@@ -193,7 +198,7 @@ struct TmOpt {
 
 }  // namespace
 
-TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
+TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, bool optimize) {
     if (const char* e = std::getenv("BC_SCHED_OPT")) optimize = optimize && std::atoi(e) != 0;
     // two placements of the gather vector: 448k vs 409k cell-solves/s with one,
     // 413k with three (B200, 100k M156, P regime; BC_GATHER_COPIES=1 overrides)
@@ -205,8 +210,10 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
     constexpr int d = 2;
     int streams = 2;  // two interleaved accumulator chains per lane (BC_TMEM_STREAMS)
     if (const char* e = std::getenv("BC_TMEM_STREAMS")) streams = std::atoi(e) == 1 ? 1 : 2;
+    if (pair) streams = 2;  // A on stream 0, A^T on stream 1
     const int s = pat.species, nnz = pat.nnz, n = k * s;
-    const int zero_col = n;  // pseudo-row whose slots always hold +0.0
+    const int nx = pair ? 2 * n : n;  // gathered columns: p (and p~ at n + i)
+    const int zero_col = nx;          // pseudo-row whose slots always hold +0.0
     // rows as segments padded to a multiple of d (csr.cpp:90-101 order kept)
     std::vector<int> seg_row, seg_len;
     std::vector<std::vector<int>> seg_cols, seg_vals;
@@ -227,24 +234,50 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
             seg_cols.push_back(std::move(cols));
             seg_vals.push_back(std::move(vals));
         }
+    const int n_a_segs = static_cast<int>(seg_row.size());
+    if (pair) {  // A^T row j = column j of A in ascending source row i (csr.cpp:129-142)
+        for (int c = 0; c < k; ++c) {
+            std::vector<std::vector<int>> tcols(s), tvals(s);
+            for (int i = 0; i < s; ++i)
+                for (int e = pat.row_ptr[i]; e < pat.row_ptr[i + 1]; ++e) {
+                    tcols[pat.col_idx[e]].push_back(n + c * s + i);
+                    tvals[pat.col_idx[e]].push_back(c * nnz + e);
+                }
+            for (int j = 0; j < s; ++j) {
+                if (tcols[j].empty()) continue;
+                while (tcols[j].size() % d) {
+                    tcols[j].push_back(zero_col);
+                    tvals[j].push_back(-1);
+                }
+                seg_row.push_back(n + c * s + j);
+                seg_len.push_back(static_cast<int>(tcols[j].size()));
+                seg_cols.push_back(std::move(tcols[j]));
+                seg_vals.push_back(std::move(tvals[j]));
+            }
+        }
+    }
     TmOpt o;
     o.seg_len = &seg_len;
     o.seg_cols = &seg_cols;
     o.seg_row = &seg_row;
-    o.ncol = n + 1;
+    o.ncol = nx + 1;
     o.nrow = n;
     o.R = copies;
     o.ST = streams;
+    o.pair = pair;
     o.lane_segs.assign(o.VL(), {});
     o.load.assign(o.VL(), 0);
+    // lane groups a segment may use: everything, or (pair) stream 0 / stream 1
+    auto group_of_seg = [&](int sg) { return pair && sg >= n_a_segs ? 1 : 0; };
+    auto group_of_lane = [&](int v) { return pair && v >= kLanes ? 1 : 0; };
     {  // longest-processing-time start
         std::vector<int> order(seg_row.size());
         std::iota(order.begin(), order.end(), 0);
         std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return seg_len[a] > seg_len[b]; });
         for (int idx : order) {
-            int best = 0;
-            for (int L = 1; L < o.VL(); ++L)
-                if (o.load[L] < o.load[best]) best = L;
+            int best = -1;
+            for (int L = 0; L < o.VL(); ++L)
+                if (group_of_lane(L) == group_of_seg(idx) && (best < 0 || o.load[L] < o.load[best])) best = L;
             o.load[best] += seg_len[idx];
             o.lane_segs[best].push_back(idx);
         }
@@ -258,7 +291,7 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
                 for (size_t i = 0; i < o.lane_segs[b].size() && !moved; ++i) {
                     const int sa = o.lane_segs[b][i];
                     for (int c = 0; c < o.VL() && !moved; ++c) {
-                        if (c == b) continue;
+                        if (c == b || group_of_lane(c) != group_of_lane(b)) continue;
                         if (o.load[c] + seg_len[sa] < M) {
                             o.lane_segs[b].erase(o.lane_segs[b].begin() + i);
                             o.lane_segs[c].push_back(sa);
@@ -290,6 +323,11 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
         for (int l : seg_len) total += l;
         const int lpt_max = *std::max_element(o.load.begin(), o.load.end());
         int cap = std::max(order.empty() ? 0 : seg_len[order[0]], (total + o.VL() - 1) / o.VL());
+        if (pair) {  // each stream's lanes carry their own rows
+            int ta = 0;
+            for (int sg = 0; sg < n_a_segs; ++sg) ta += seg_len[sg];
+            cap = std::max({cap, (ta + kLanes - 1) / kLanes, (total - ta + kLanes - 1) / kLanes});
+        }
         cap = (cap + unit - 1) / unit * unit;
         for (; cap < lpt_max; cap += unit) {
             std::vector<std::vector<int>> segs(o.VL());
@@ -297,7 +335,7 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
             bool ok = true;
             for (int idx : order) {
                 int b = 0;
-                while (b < o.VL() && load[b] + seg_len[idx] > cap) ++b;
+                while (b < o.VL() && (group_of_lane(b) != group_of_seg(idx) || load[b] + seg_len[idx] > cap)) ++b;
                 if (b == o.VL()) {
                     ok = false;
                     break;
@@ -336,14 +374,15 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
     }
     o.col_at.assign(static_cast<size_t>(o.S) * kLanes, -1);
     o.end_at.assign(static_cast<size_t>(o.S) * kLanes, 0);
-    o.row_lane.assign(n, -1);
+    o.row_lane.assign(pair ? 2 * n : n, -1);
     o.gcost.assign(static_cast<size_t>(o.S) * 2, 0);
     for (int v = 0; v < o.VL(); ++v) o.lay_lane(v);
     o.full_eval();
 
     if (optimize) {
         auto urand = [&]() { return static_cast<double>(rnd() >> 11) * 0x1.0p-53; };
-        const long iters = std::max<long>(20000, std::min<long>(200000, 40000000L / (o.S * kLanes)));
+        long iters = std::max<long>(20000, std::min<long>(200000, 40000000L / (o.S * kLanes)));
+        if (const char* e = std::getenv("BC_ANNEAL_ITERS")) iters = std::atol(e);
         double T = 1.0;
         const double cool = std::pow(0.01 / T, 1.0 / static_cast<double>(iters));
         int cur = o.total(), best = cur;
@@ -390,7 +429,9 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
             } else {
                 // segment moves: reorder within a lane, move or exchange between lanes
                 const int A = static_cast<int>(rnd() % o.VL());
-                int B = kind == 2 ? A : static_cast<int>(rnd() % o.VL());
+                int B = kind == 2 ? A
+                        : pair    ? (A / kLanes) * kLanes + static_cast<int>(rnd() % kLanes)
+                                  : static_cast<int>(rnd() % o.VL());
                 if (o.lane_segs[A].empty()) continue;
                 const auto saveA = o.lane_segs[A], saveB = o.lane_segs[B];
                 if (kind == 2) {
@@ -452,12 +493,13 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool optimize) {
     ts.copies = o.R;
     ts.xslots = o.R * o.NS;
     ts.zero_slot = o.pos[zero_col];
-    ts.xpos.assign(static_cast<size_t>(o.R) * n, 0);
+    ts.pair = pair ? 1 : 0;
+    ts.xpos.assign(static_cast<size_t>(o.R) * nx, 0);
     for (int r = 0; r < o.R; ++r)
-        for (int i = 0; i < n; ++i) ts.xpos[static_cast<size_t>(r) * n + i] = r * o.NS + o.pos[r * o.ncol + i];
+        for (int i = 0; i < nx; ++i) ts.xpos[static_cast<size_t>(r) * nx + i] = r * o.NS + o.pos[r * o.ncol + i];
     ts.words.assign(static_cast<size_t>(o.S) * kLanes, 0);
     ts.vidx.assign(static_cast<size_t>(o.S) * kLanes, -1);
-    ts.yslot.assign(n, -1);
+    ts.yslot.assign(pair ? 2 * n : n, -1);
     std::vector<int> vals_at(static_cast<size_t>(o.S) * kLanes, -1);
     int kmax = 1;
     for (int v = 0; v < o.VL(); ++v) kmax = std::max(kmax, static_cast<int>(o.lane_segs[v].size()));

@@ -225,20 +225,21 @@ def test_reduction_geometry_reproduces_tree(n):
         assert of.bits(got) == of.bits(want)
 
 
-def export_tmem_schedule(rp, ci, k):
+def export_tmem_schedule(rp, ci, k, pair=0):
     species = len(rp) - 1
     rp = np.ascontiguousarray(rp, np.int32)
     ci = np.ascontiguousarray(ci, np.int32)
     info = np.zeros(9, np.int32)
     lib = _native.b200()
-    assert lib.bc_tmem_schedule_export(species, of.ptr(rp), of.ptr(ci), k, of.ptr(info), None, None, None,
+    assert lib.bc_tmem_schedule_export(species, of.ptr(rp), of.ptr(ci), k, pair, of.ptr(info), None, None, None,
                                        None) == 0
     S, copies = int(info[0]), int(info[5])
+    mult = 2 if pair else 1
     words = np.zeros(S * 32, np.uint16)
     vidx = np.zeros(S * 32, np.int32)
-    xpos = np.zeros(copies * k * species, np.int32)
-    yslot = np.zeros(k * species, np.int32)
-    assert lib.bc_tmem_schedule_export(species, of.ptr(rp), of.ptr(ci), k, of.ptr(info), of.ptr(words),
+    xpos = np.zeros(copies * k * species * mult, np.int32)
+    yslot = np.zeros(k * species * mult, np.int32)
+    assert lib.bc_tmem_schedule_export(species, of.ptr(rp), of.ptr(ci), k, pair, of.ptr(info), of.ptr(words),
                                        of.ptr(vidx), of.ptr(xpos), of.ptr(yslot)) == 0
     return dict(S=S, xslots=int(info[1]), zero_slot=int(info[2]), yslots=int(info[3]), cost=int(info[4]),
                 copies=copies, model=int(info[6]), streams=int(info[7]), ystream=int(info[8]), words=words,
@@ -275,9 +276,10 @@ def emulate_tmem_spmv(sc, vals, x):
     return Y[sc["yslot"]]
 
 
+@pytest.mark.parametrize("pair", [0, 1])
 @pytest.mark.parametrize("species,k,density,seed", [(9, 1, 0.4, 0), (40, 3, 0.2, 1), (156, 1, 0.0, 2),
                                                     (100, 2, 0.05, 3), (17, 15, 0.3, 4), (60, 1, 0.02, 5)])
-def test_tmem_schedule_reproduces_spmv_order(species, k, density, seed):
+def test_tmem_schedule_reproduces_spmv_order(species, k, density, seed, pair):
     rng = np.random.default_rng(seed)
     if density == 0.0:
         m = Mechanism(156, 468, 0)
@@ -294,13 +296,16 @@ def test_tmem_schedule_reproduces_spmv_order(species, k, density, seed):
             ci = ci[keep]
             rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
     nnz = int(rp[-1])
-    sc = export_tmem_schedule(rp, ci, k)
+    sc = export_tmem_schedule(rp, ci, k, pair)
     assert sc["S"] % 4 == 0
     vals = rng.uniform(-1, 1, k * nnz) * 10.0 ** rng.integers(-8, 8, k * nnz)
-    x = rng.uniform(-1, 1, k * species)
-    x[rng.random(k * species) < 0.05] = np.inf  # padding must never touch x (0*inf = NaN)
+    n = k * species
+    x = rng.uniform(-1, 1, n * (2 if pair else 1))
+    x[rng.random(len(x)) < 0.05] = np.inf  # padding must never touch x (0*inf = NaN)
     y = emulate_tmem_spmv(sc, vals, x)
     with np.errstate(invalid="ignore"):
-        np.testing.assert_array_equal(of.bits(y), of.bits(ref_spmv(rp, ci, vals, x, k, species, nnz)))
+        np.testing.assert_array_equal(of.bits(y[:n]), of.bits(ref_spmv(rp, ci, vals, x[:n], k, species, nnz)))
+        if pair:  # BiCG's A^T p~ in the same pass, ascending source rows (csr.cpp:129-142)
+            np.testing.assert_array_equal(of.bits(y[n:]), of.bits(ref_spmv_t(rp, ci, vals, x[n:], k, species, nnz)))
     used = sc["vidx"][sc["vidx"] >= 0]
-    assert sorted(used.tolist()) == list(range(k * nnz))
+    assert sorted(used.tolist()) == sorted(list(range(k * nnz)) * (2 if pair else 1))

@@ -87,6 +87,8 @@ def test_m156_bicg_bitwise_vs_reference(solver, m156, m156_batches, regime, kind
         assert st == 0
         assert_matches_reference(rep, rres, f"{regime} {kind} {k} vs reference")
     north_star_tolerances(rep, res)
+    if k == 1 or kind == Strategy.OneCell:  # one warp per cell: the TMEM kernel's pair schedule
+        assert rep.kernels & ~16 == KERNEL_TMEM, rep.kernels
 
 
 @pytest.mark.parametrize("regime", ["P", "C"])

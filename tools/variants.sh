@@ -1,7 +1,8 @@
-# GPU tests + e2e bench on the GPU box.
+# GPU tests + kernel timings on the GPU box.
 cd ${GRAFT_REPO_ROOT:-.}
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-timeout 300 python tools/e2e_probe.py
-for v in "" "BC_PIPE_CHUNKS=8" "BC_PIPE_CHUNKS=64"; do
-env $v timeout 400 python bench.py --no-cpu-baseline --steps 5 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v value',d['value'],'e2e',d['e2e']['value'], d['e2e']['ms_per_step'])"
+for v in "" "BC_KERNEL=v1"; do
+  echo "== M156 bicg $v"; env $v REPS=2 timeout 200 python tools/prof_block.py 100000 bicg 2>&1 | tail -1
+  echo "== M312 bicg $v"; env $v SPECIES=312 REPS=1 timeout 300 python tools/prof_block.py 100000 bicg 2>&1 | tail -1
 done
+echo "== M156 bicgstab"; REPS=2 timeout 200 python tools/prof_block.py 100000 2>&1 | tail -1
