@@ -130,12 +130,13 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_reference_rate(values, rhs, row_ptr, col_idx, reg, budget_s, algo_name="bicg"):
-    """The reference's run_strategy (Block-cells(1), all host threads) on a
-    bounded prefix sample of the workload.  Returns (rate, cores, sample, kind)."""
+def cpu_reference_rate(values, rhs, row_ptr, col_idx, reg, budget_s, algo_name="bicg", threads=None):
+    """The reference's run_strategy (Block-cells(1), all host threads unless
+    `threads`) on a bounded prefix sample of the workload.  Returns (rate,
+    cores, sample, kind)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_ffi as of
-    cores = os.cpu_count() or 1
+    cores = threads or os.cpu_count() or 1
     use_ref = of.have_ref() and algo_name == "bicg"
     kind = "reference" if use_ref else "port"
 
@@ -345,6 +346,10 @@ def main_b200(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, cores, sample, kind = cpu_reference_rate(h_values, h_rhs, m.row_ptr, m.col_idx, reg, args.cpu_seconds)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+        # BASELINE.json configs[1]: the reference on one host thread as well
+        rate1, _, sample1, kind1 = cpu_reference_rate(h_values, h_rhs, m.row_ptr, m.col_idx, reg,
+                                                      max(2.0, args.cpu_seconds / 3), threads=1)
+        cpu["single_thread"] = {"value": rate1, "unit": UNIT, "cores": 1, "kind": kind1, "sample": sample1}
 
     if rank == 0:
         out = {
