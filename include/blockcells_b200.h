@@ -149,11 +149,12 @@ int bc_schedule_export(int32_t species, const int32_t* row_ptr, const int32_t* c
  * wavefronts per pass, copies of the gather vector, modelled shared
  * wavefronts per SpMV, row streams per lane, Y slots per stream.  pair != 0:
  * BiCG's schedule, A rows on stream 0 and A^T rows on stream 1 (columns and
- * outputs doubled).  Arrays may be NULL to query sizes: words/vidx S*32, xpos
- * copies*k*species (x2 for a pair), yslot k*species (x2 for a pair). */
+ * outputs doubled).  team: warps per group (1, 2, 4).  Arrays may be NULL to
+ * query sizes: words/vidx S*32*team, xpos copies*k*species (x2 for a pair),
+ * yslot k*species (x2 for a pair). */
 int bc_tmem_schedule_export(int32_t species, const int32_t* row_ptr, const int32_t* col_idx, int32_t k,
-                            int32_t pair, int32_t* info, uint16_t* words, int32_t* vidx, int32_t* xpos,
-                            int32_t* yslot);
+                            int32_t pair, int32_t team, int32_t* info, uint16_t* words, int32_t* vidx,
+                            int32_t* xpos, int32_t* yslot);
 
 /*
  * Solve every cell's system A_c x_c = b_c (x0 = 0, as solve_group does).

@@ -87,7 +87,7 @@ def b200() -> C.CDLL:
         lib.bc_set_pattern.argtypes = [_c_p, _i32, _c_p, _c_p]
         lib.bc_plan.argtypes = [_i32, C.POINTER(SolveParams), C.POINTER(_i64), C.POINTER(_f64)]
         lib.bc_schedule_export.argtypes = [_i32, _c_p, _c_p, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]
-        lib.bc_tmem_schedule_export.argtypes = [_i32, _c_p, _c_p, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p]
+        lib.bc_tmem_schedule_export.argtypes = [_i32, _c_p, _c_p, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p]
         lib.bc_solve.argtypes = [_c_p, C.POINTER(SolveParams), _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                                  C.POINTER(Report)]
         lib.bc_bicg_solve.argtypes = [_c_p, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _f64, _i64,

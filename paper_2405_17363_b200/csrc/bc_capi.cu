@@ -287,29 +287,32 @@ int pipe_chunks() {  // BC_PIPE_CHUNKS overrides the default 32
 constexpr int64_t kPipeMinCells = 4096;
 
 struct TmemCfg {
-    int R, RV, warps, ST, CP, ALGO;  // warps per CTA (= 4 * groups per lane quarter), row streams,
-    TmemFn fn;                       // gather copies, bc::AlgoKind
+    int T, R, RV, warps, ST, CP, ALGO;  // team width (warps per group), tree slots, row slots, warps per CTA,
+    TmemFn fn;                          // row streams, gather copies, bc::AlgoKind
 };
 
-// Jacobi-BiCGSTAB: 16 warps/SM at <= 128 registers; 8 warps (<= 255
-// registers) for schedules too long for 3 groups per quarter (the scaled
-// mechanism: 312 species); one or two row streams, one or two gather copies.
-// BiCG: its pair schedule (A and A^T in one pass) is twice as long, so 8
-// warps/SM at M156 and 4 at M312; two streams.
-#define BC_TMEM_CFG1(R, RV, W, ST, CP, A) \
-    { R, RV, W, ST, CP, A, &bc::block_cells_tmem_kernel<R, RV, 32 * W, ST, CP, A> }
-#define BC_TMEM_CFG(R, RV, W)                                                                          \
-    BC_TMEM_CFG1(R, RV, W, 1, 1, bc::kBiCGStab), BC_TMEM_CFG1(R, RV, W, 1, 2, bc::kBiCGStab),           \
-        BC_TMEM_CFG1(R, RV, W, 2, 1, bc::kBiCGStab), BC_TMEM_CFG1(R, RV, W, 2, 2, bc::kBiCGStab)
-#define BC_TMEM_CFG_BICG(R, RV, W) \
-    BC_TMEM_CFG1(R, RV, W, 2, 1, bc::kBiCG), BC_TMEM_CFG1(R, RV, W, 2, 2, bc::kBiCG)
+// Jacobi-BiCGSTAB: one warp per cell at 16 warps/SM (<= 128 registers) or 8
+// (<= 255); two-warp teams for schedules too long for 4 cells per lane
+// quarter (the scaled mechanism, 312 species: 16 warps = 8 cells/SM instead
+// of 8 warps = 8 cells); four-warp teams for latency (BC_TMEM_TEAM=4).
+// BiCG runs its pair schedule (A and A^T in one pass, twice as long).
+#define BC_TMEM_CFG(T, R, RV, W, ST, CP, A) \
+    { T, R, RV, W, ST, CP, A, &bc::block_cells_tmem_kernel<T, R, RV, 32 * W, ST, CP, A> }
+constexpr int kS = bc::kBiCGStab, kB = bc::kBiCG;
 const TmemCfg kTmemConfigs[] = {
-    BC_TMEM_CFG(8, 5, 16),       BC_TMEM_CFG(8, 8, 16),       BC_TMEM_CFG(4, 4, 16),      BC_TMEM_CFG(16, 10, 8),
-    BC_TMEM_CFG_BICG(8, 5, 8),   BC_TMEM_CFG_BICG(8, 8, 8),   BC_TMEM_CFG_BICG(4, 4, 8),  BC_TMEM_CFG_BICG(16, 10, 4),
+    // BiCGSTAB, one warp per cell
+    BC_TMEM_CFG(1, 8, 5, 16, 2, 2, kS), BC_TMEM_CFG(1, 8, 5, 16, 2, 1, kS), BC_TMEM_CFG(1, 8, 5, 16, 1, 2, kS),
+    BC_TMEM_CFG(1, 8, 5, 16, 1, 1, kS), BC_TMEM_CFG(1, 8, 8, 16, 2, 2, kS), BC_TMEM_CFG(1, 4, 4, 16, 2, 2, kS),
+    BC_TMEM_CFG(1, 16, 10, 8, 2, 2, kS), BC_TMEM_CFG(1, 16, 10, 8, 2, 1, kS),
+    // BiCGSTAB, teams
+    BC_TMEM_CFG(2, 8, 5, 16, 2, 2, kS), BC_TMEM_CFG(2, 4, 3, 16, 2, 2, kS), BC_TMEM_CFG(4, 2, 2, 16, 1, 2, kS),
+    BC_TMEM_CFG(4, 4, 3, 16, 1, 2, kS),
+    // BiCG (pair schedules)
+    BC_TMEM_CFG(1, 8, 5, 8, 2, 2, kB), BC_TMEM_CFG(1, 8, 5, 8, 2, 1, kB), BC_TMEM_CFG(1, 8, 8, 8, 2, 2, kB),
+    BC_TMEM_CFG(1, 4, 4, 8, 2, 2, kB), BC_TMEM_CFG(1, 16, 10, 4, 2, 2, kB), BC_TMEM_CFG(2, 8, 5, 8, 2, 2, kB),
+    BC_TMEM_CFG(2, 4, 3, 16, 2, 2, kB),
 };
 #undef BC_TMEM_CFG
-#undef BC_TMEM_CFG_BICG
-#undef BC_TMEM_CFG1
 
 int tmem_warps_pref() {
     const char* e = std::getenv("BC_TMEM_WARPS");
@@ -346,15 +349,42 @@ double sigma_threshold(double tol, int n) {
     return r;
 }
 
-// The TMEM kernel runs a group on one warp whatever the v1 team width: its
-// reduction tree is the full Q = P/32 slots per lane (Q <= 16 instantiated).
+// The TMEM kernel runs a group on a team of 1, 2 or 4 warps whatever the v1
+// team width: its reduction tree is Q/team slots per lane (Q <= 16 here).
 bool tmem_fits(const bc::GroupPlan& gp) { return gp.geo.P >= 32 && gp.geo.Q <= 16; }
+
+int tmem_team_pref() {
+    const char* e = std::getenv("BC_TMEM_TEAM");
+    const int t = e ? std::atoi(e) : 0;
+    return t == 1 || t == 2 || t == 4 ? t : 0;
+}
+
+// Warps per TMEM lane quarter that fit 512 columns: S/2 word columns shared
+// by the quarter, 2S value columns per warp (one group, or one team member).
+int tmem_groups_per_quarter(int S) { return S > 0 ? std::min(4, (512 - S / 2) / (2 * S)) : 0; }
 
 // BiCG plans (built with the transpose) get the pair schedule: A p and A^T p~
 // in one pass.
 void ensure_tmem_schedule(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp) {
     if (gp.has_tm || tmem_disabled() || !tmem_fits(gp)) return;
-    gp.tm = bc::build_tmem_schedule(pat, gp.k, gp.at.steps > 0);
+    const bool pair = gp.at.steps > 0;
+    int team = tmem_team_pref();
+    if (team == 0 || gp.geo.Q % team) {
+        // One warp per cell while 2 cells fit a lane quarter (8 warps/SM), else
+        // two-warp teams.  B200, 100k cells, P regime: M312 BiCG pair schedule
+        // (S = 200, 4 warps/SM alone) 209k with teams vs 157k; where 2 cells fit,
+        // teams lose to their barriers (M312 BiCGSTAB 212k vs 221k, M156 BiCG
+        // 455k vs 476k, M156 BiCGSTAB 289k vs 502k).
+        gp.tm = bc::build_tmem_schedule(pat, gp.k, pair, 1);
+        team = (tmem_groups_per_quarter(gp.tm.steps) >= 2 || gp.geo.Q % 2) ? 1 : 2;
+        if (team == 1) {
+            gp.d_tm_words = upload(ctx, gp.tm.words);
+            gp.d_tm_vidx = upload(ctx, gp.tm.vidx);
+            gp.has_tm = true;
+            return;
+        }
+    }
+    gp.tm = bc::build_tmem_schedule(pat, gp.k, pair, team);
     gp.d_tm_words = upload(ctx, gp.tm.words);
     gp.d_tm_vidx = upload(ctx, gp.tm.vidx);
     gp.has_tm = true;
@@ -366,29 +396,28 @@ void ensure_tmem_schedule(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp
 // the trash slot (after every copy) and read the zero Y slot.
 void ensure_tmem_lane_tables(bc_ctx* ctx, bc::GroupPlan& gp, int RV) {
     if (gp.tm_lane_rv == RV) return;
-    const int n = gp.geo.n, trash = gp.tm.xslots, nx = gp.tm.pair ? 2 * n : n;
+    const int n = gp.geo.n, trash = gp.tm.xslots, nx = gp.tm.pair ? 2 * n : n, T = gp.tm.team;
     for (int part = 0; part < (gp.tm.pair ? 2 : 1); ++part) {
-        std::vector<uint32_t> xy(static_cast<size_t>(RV) * 32);
-        std::vector<uint32_t> x1(static_cast<size_t>((RV + 1) / 2) * 32, 0u);
+        // owner row of (slot j, warp w, lane l) is (j*T + w)*32 + l (team_reduce's layout)
+        std::vector<uint32_t> xy(static_cast<size_t>(RV) * T * 32);
+        std::vector<uint32_t> x1(static_cast<size_t>((RV + 1) / 2) * T * 32, 0u);
         for (int j = 0; j < RV; ++j)
-            for (int l = 0; l < 32; ++l) {
-                const int row = j * 32 + l, col = part * n + row;
-                const bool ok = row < n;
-                xy[j * 32 + l] = static_cast<uint32_t>(ok ? gp.tm.xpos[col] : trash) |
-                                 (static_cast<uint32_t>(ok ? gp.tm.yslot[col] : gp.tm.yslots) << 16);
-                const uint32_t s1 =
-                    static_cast<uint32_t>(ok && gp.tm.copies > 1 ? gp.tm.xpos[static_cast<size_t>(nx) + col] : trash);
-                x1[(j / 2) * 32 + l] |= s1 << (16 * (j % 2));
-            }
+            for (int w = 0; w < T; ++w)
+                for (int l = 0; l < 32; ++l) {
+                    const int row = (j * T + w) * 32 + l, col = part * n + row;
+                    const bool ok = row < n;
+                    xy[row] = static_cast<uint32_t>(ok ? gp.tm.xpos[col] : trash) |
+                              (static_cast<uint32_t>(ok ? gp.tm.yslot[col] : gp.tm.yslots) << 16);
+                    const uint32_t s1 = static_cast<uint32_t>(
+                        ok && gp.tm.copies > 1 ? gp.tm.xpos[static_cast<size_t>(nx) + col] : trash);
+                    x1[((j / 2) * T + w) * 32 + l] |= s1 << (16 * (j % 2));
+                }
         (part ? gp.d_tm_lane_xyT : gp.d_tm_lane_xy) = upload(ctx, xy);
         (part ? gp.d_tm_lane_x1T : gp.d_tm_lane_x1) = upload(ctx, x1);
     }
     gp.tm_lane_rv = RV;
 }
 
-// Groups per TMEM lane quarter that fit 512 columns: S/2 word columns shared
-// by the quarter, 2S value columns per group.
-int tmem_groups_per_quarter(int S) { return S > 0 ? std::min(4, (512 - S / 2) / (2 * S)) : 0; }
 
 // Kernel instance for a plan: same tree width R, enough row slots, and the
 // most warps the schedule's TMEM footprint allows (capped by BC_TMEM_WARPS).
@@ -399,8 +428,9 @@ const TmemCfg* pick_tmem_cfg(const bc::GroupPlan& gp) {
     const int want = std::min(4 * cpq, tmem_warps_pref());
     const TmemCfg* cfg = nullptr;
     for (const TmemCfg& t : kTmemConfigs) {
-        if (t.R != gp.geo.Q || t.RV < (gp.geo.n + 31) / 32 || t.warps < want || t.ST != gp.tm.streams ||
-            t.CP != gp.tm.copies || t.ALGO != algo)
+        const int T = gp.tm.team;
+        if (t.T != T || t.R * T != gp.geo.Q || t.RV * T < (gp.geo.n + 31) / 32 || t.warps < want ||
+            t.ST != gp.tm.streams || t.CP != gp.tm.copies || t.ALGO != algo)
             continue;
         if (!cfg || t.warps < cfg->warps || (t.warps == cfg->warps && t.RV < cfg->RV)) cfg = &t;
     }
@@ -417,11 +447,11 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
     ensure_tmem_lane_tables(ctx, gp, cfg->RV);
     const int S = gp.tm.steps;
     const int cpq = std::min(cfg->warps / 4, tmem_groups_per_quarter(S));
-    const int warps = 4 * cpq;
-    const int xslots = (gp.tm.xslots + 1 + 31) & ~31, yslots = gp.tm.yslots + 32;
+    const int warps = 4 * cpq, T = cfg->T, teams = warps / T;
+    const int xslots = (gp.tm.xslots + 1 + 31) & ~31, yslots = gp.tm.yslots + 32 * T;
     const int xalign = static_cast<int>(bc::padded_len(8 * xslots));
-    const size_t smem = sizeof(int32_t) * S * 32 + static_cast<size_t>(xalign) * (warps + 1) +
-                        sizeof(double) * warps * yslots;
+    const size_t smem = sizeof(int32_t) * S * 32 * T + static_cast<size_t>(xalign) * (teams + 1) +
+                        sizeof(double) * teams * yslots + (T > 1 ? sizeof(double) * teams * 2 * 4 * 32 * T : 0);
     if (smem > static_cast<size_t>(kMaxDynSmem - 1024)) return false;
     if (!ctx->smem_set[reinterpret_cast<BlockFn>(cfg->fn)]) {
         check_cuda(cudaFuncSetAttribute(cfg->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem - 1024),
@@ -461,7 +491,7 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
     p.tol = tol;
     p.max_iter = static_cast<int>(std::min<int64_t>(max_iter, 0x7FFFFFFF));
     p.gate = gate;
-    const int blocks = std::max(1, std::min(ctx->sms, (groups + warps - 1) / warps));
+    const int blocks = std::max(1, std::min(ctx->sms, (groups + teams - 1) / teams));
     check_cuda(cudaMemsetAsync(counter, 0, sizeof(unsigned int), st), "cudaMemsetAsync(counter)");
     cfg->fn<<<blocks, warps * 32, smem, st>>>(p);
     check_cuda(cudaGetLastError(), "block_cells_tmem_kernel launch");
@@ -841,12 +871,13 @@ int bc_schedule_export(int32_t species, const int32_t* row_ptr, const int32_t* c
 }
 
 int bc_tmem_schedule_export(int32_t species, const int32_t* row_ptr, const int32_t* col_idx, int32_t k,
-                            int32_t pair, int32_t* info, uint16_t* words, int32_t* vidx, int32_t* xpos,
-                            int32_t* yslot) {
+                            int32_t pair, int32_t team, int32_t* info, uint16_t* words, int32_t* vidx,
+                            int32_t* xpos, int32_t* yslot) {
     if (!info || k < 1) return BC_ERR_INVALID_ARGUMENT;
     return guarded(nullptr, [&] {
         const bc::Pattern pat = make_pattern(species, row_ptr, col_idx);
-        const bc::TmemSchedule ts = bc::build_tmem_schedule(pat, k, pair != 0);
+        if (team != 1 && team != 2 && team != 4) fail(BC_ERR_INVALID_ARGUMENT, "team must be 1, 2 or 4");
+        const bc::TmemSchedule ts = bc::build_tmem_schedule(pat, k, pair != 0, team);
         const int v[9] = {ts.steps,  ts.xslots,      ts.zero_slot, ts.yslots, ts.conflict_cost,
                           ts.copies, ts.model_total, ts.streams,   ts.ystream};
         std::memcpy(info, v, sizeof v);

@@ -69,8 +69,8 @@ struct Schedule {
 //  * the gather vector has `copies` independent placements (bc_tmem_plan.cpp).
 struct TmemSchedule {
     int steps = 0;                  // S, a multiple of 4
-    std::vector<uint16_t> words;    // S * 32
-    std::vector<int32_t> vidx;      // S * 32: group value index, -1 for padding (value 0.0)
+    std::vector<uint16_t> words;    // S * 32W
+    std::vector<int32_t> vidx;      // S * 32W: group value index, -1 for padding (value 0.0)
     int copies = 1;                 // independent copies of the gather vector
     int xslots = 0;                 // gather-vector slots, all copies, incl. zero slots
     int zero_slot = 0;
@@ -82,6 +82,7 @@ struct TmemSchedule {
     int pair = 0;                   // BiCG: A rows on stream 0, A^T rows on stream 1 (xpos: [copy][2n],
                                     // columns n + i gather p~; yslot: [2n], A^T output j at n + j)
     int ystream = 32;               // Y slots per stream
+    int team = 1;                   // warps per group W: words/vidx are [S][32W], Y lane-major over 32W lanes
     int conflict_cost = 0;          // modelled gather wavefronts per pass
 };
 
@@ -114,7 +115,8 @@ struct GroupPlan {
     uint32_t* d_tm_lane_x1T = nullptr;
 };
 
-TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair = false, bool optimize = true);
+TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair = false, int team = 1,
+                                  bool optimize = true);
 
 Schedule build_schedule(const Pattern& pat, int k, int lanes, bool transpose, bool optimize = true);
 GroupPlan build_group_plan(const Pattern& pat, int k, bool with_transpose, bool optimize = true);

@@ -130,6 +130,7 @@ struct TmemWarp {
     uint32_t xyT[RV];       // BiCG pair: the same for p~ and the A^T outputs
     uint32_t x1T[(RV + 1) / 2];
     int lane;
+    int ylane;              // this lane's column in the team's lane-major Y (32 * warp-in-team + lane)
     uint32_t wcol, vcol;    // TMEM addresses: words, this warp's values
     int S;
     int ystream;            // Y slots per row stream
@@ -142,7 +143,7 @@ struct TmemWarp {
 //   ST = 2: two rows at a time, stream 0 on steps 0 and 2, stream 1 on steps 1
 //           and 3 -- two independent DADD chains; stream 0 rows end on step 2
 //           (flag in w0), stream 1 rows on step 3 (flag in w1).
-template <int ST>
+template <int ST, int LW>
 __device__ __forceinline__ void tmem_chunk4(uint32_t xaddr, uint32_t w0, uint32_t w1, const uint32_t* v,
                                             double (&acc)[ST], double* (&yp)[ST]) {
     const double x0 = lds64(gaddr_lo(w0, xaddr));
@@ -158,14 +159,14 @@ __device__ __forceinline__ void tmem_chunk4(uint32_t xaddr, uint32_t w0, uint32_
         acc[0] = dadd(acc[0], dmul(a1, x1));
         if (w0 & 0x8000u) {
             *yp[0] = acc[0];
-            yp[0] += 32;
+            yp[0] += LW;
             acc[0] = 0.0;
         }
         acc[0] = dadd(acc[0], dmul(a2, x2));
         acc[0] = dadd(acc[0], dmul(a3, x3));
         if (w1 & 0x8000u) {
             *yp[0] = acc[0];
-            yp[0] += 32;
+            yp[0] += LW;
             acc[0] = 0.0;
         }
     } else {
@@ -174,13 +175,13 @@ __device__ __forceinline__ void tmem_chunk4(uint32_t xaddr, uint32_t w0, uint32_
         acc[0] = dadd(acc[0], dmul(a2, x2));
         if (w0 & 0x8000u) {
             *yp[0] = acc[0];
-            yp[0] += 32;
+            yp[0] += LW;
             acc[0] = 0.0;
         }
         acc[1] = dadd(acc[1], dmul(a3, x3));
         if (w1 & 0x8000u) {
             *yp[1] = acc[1];
-            yp[1] += 32;
+            yp[1] += LW;
             acc[1] = 0.0;
         }
     }
@@ -200,13 +201,13 @@ __device__ __forceinline__ void tmem_publish(double* Xs, const uint32_t (&xy)[RV
 
 // Walk the TMEM-resident schedule (8 steps per tcgen05.ld pair, then a 4-step
 // tail; other warps hide the latency), row sums into Y.
-template <int ST, int RV>
+template <int ST, int LW, int RV>
 __device__ __forceinline__ void tmem_walk(const TmemWarp<RV>& tw) {
     double* yp[ST];
     double acc[ST];
 #pragma unroll
     for (int s = 0; s < ST; ++s) {
-        yp[s] = tw.Ys + s * tw.ystream + tw.lane;
+        yp[s] = tw.Ys + s * tw.ystream + tw.ylane;
         acc[s] = 0.0;
     }
     int t0 = 0;
@@ -215,40 +216,41 @@ __device__ __forceinline__ void tmem_walk(const TmemWarp<RV>& tw) {
         tm_ld_x4(tw.wcol + (t0 >> 1), w);
         tm_ld_x16(tw.vcol + 2 * t0, v);
         tm_wait_ld();
-        tmem_chunk4<ST>(tw.xaddr, w[0], w[1], v, acc, yp);
-        tmem_chunk4<ST>(tw.xaddr, w[2], w[3], v + 8, acc, yp);
+        tmem_chunk4<ST, LW>(tw.xaddr, w[0], w[1], v, acc, yp);
+        tmem_chunk4<ST, LW>(tw.xaddr, w[2], w[3], v + 8, acc, yp);
     }
     if (t0 < tw.S) {
         uint32_t w[2], v[8];
         tm_ld_x2(tw.wcol + (t0 >> 1), w);
         tm_ld_x8(tw.vcol + 2 * t0, v);
         tm_wait_ld();
-        tmem_chunk4<ST>(tw.xaddr, w[0], w[1], v, acc, yp);
+        tmem_chunk4<ST, LW>(tw.xaddr, w[0], w[1], v, acc, yp);
     }
 }
 
 // y = A x (for a BiCG pair schedule the A^T stream runs on whatever p~ holds
 // and its outputs are ignored).
-template <int ST, int CP, int RV>
-__device__ __forceinline__ void tmem_spmv(const TmemWarp<RV>& tw, const double (&x)[RV], double (&y)[RV]) {
+template <int ST, int CP, int W, int RV>
+__device__ __forceinline__ void tmem_spmv(const TmemWarp<RV>& tw, const Team<W>& tm, const double (&x)[RV],
+                                          double (&y)[RV]) {
     tmem_publish<CP>(tw.Xs, tw.xy, tw.x1, x);
-    __syncwarp();
-    tmem_walk<ST>(tw);
-    __syncwarp();
+    tm.sync();
+    tmem_walk<ST, 32 * W>(tw);
+    tm.sync();
 #pragma unroll
     for (int j = 0; j < RV; ++j) y[j] = tw.Ys[tw.xy[j] >> 16];
 }
 
 // BiCG's two products in one pass of the pair schedule: A p on stream 0,
 // A^T p~ on stream 1 (bc_tmem_plan.cpp, pair mode).
-template <int CP, int RV>
-__device__ __forceinline__ void tmem_spmv_pair(const TmemWarp<RV>& tw, const double (&pv)[RV],
+template <int CP, int W, int RV>
+__device__ __forceinline__ void tmem_spmv_pair(const TmemWarp<RV>& tw, const Team<W>& tm, const double (&pv)[RV],
                                                const double (&ps)[RV], double (&ap)[RV], double (&atps)[RV]) {
     tmem_publish<CP>(tw.Xs, tw.xy, tw.x1, pv);
     tmem_publish<CP>(tw.Xs, tw.xyT, tw.x1T, ps);
-    __syncwarp();
-    tmem_walk<2>(tw);
-    __syncwarp();
+    tm.sync();
+    tmem_walk<2, 32 * W>(tw);
+    tm.sync();
 #pragma unroll
     for (int j = 0; j < RV; ++j) {
         ap[j] = tw.Ys[tw.xy[j] >> 16];
@@ -280,11 +282,21 @@ __device__ __forceinline__ void tmem_reduce(const double (&vals)[NV][RV], double
         for (int v = 0; v < NV; ++v) out[v] = dadd(out[v], __shfl_xor_sync(0xffffffffu, out[v], mask));
 }
 
-template <int ST, int CP, int R, int RV>
-__device__ __forceinline__ double tmem_fresh_rms(const Ctx<1, R, RV>& c, const TmemWarp<RV>& tw,
+// W > 1: team_reduce (per-lane tree, one cross-warp step through shared
+// memory, xor butterfly -- the same tree order for any team width).
+template <int NV, int W, int R, int RV>
+__device__ __forceinline__ void tmem_reduce(Ctx<W, R, RV>& c, const double (&vals)[NV][RV], double (&out)[NV]) {
+    if constexpr (W == 1)
+        tmem_reduce<NV, R, RV>(vals, out);
+    else
+        team_reduce<NV>(c, vals, out);
+}
+
+template <int ST, int CP, int W, int R, int RV>
+__device__ __forceinline__ double tmem_fresh_rms(Ctx<W, R, RV>& c, const TmemWarp<RV>& tw,
                                                  const double (&x)[RV], const double* bsrc) {
     double ax[RV];
-    tmem_spmv<ST, CP>(tw, x, ax);
+    tmem_spmv<ST, CP>(tw, c.tm, x, ax);
     double sq[1][RV];
 #pragma unroll
     for (int j = 0; j < RV; ++j) {
@@ -293,25 +305,30 @@ __device__ __forceinline__ double tmem_fresh_rms(const Ctx<1, R, RV>& c, const T
         sq[0][j] = dmul(ri, ri);
     }
     double out[1];
-    tmem_reduce<1, R, RV>(sq, out);
+    tmem_reduce<1>(c, sq, out);
     return __dsqrt_rn(ddiv(out[0], static_cast<double>(c.n)));
 }
 
-template <int R, int RV, int NT, int ST, int CP, int ALGO>
+template <int W, int R, int RV, int NT, int ST, int CP, int ALGO>
 __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParams p) {
+    constexpr int LW = 32 * W;  // lanes per group (a team of W warps per cell)
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t s_taddr;
+    __shared__ int s_group[16];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int quarter = warp % 4, slot = warp / 4;
-    int32_t* s_vidx = reinterpret_cast<int32_t*>(smem);  // S*32
-    // X regions (one per warp, each aligned to xalign) then Y regions
+    const int team = warp / W, wr = warp % W;  // team = consecutive warps: quarter % W == wr
+    int32_t* s_vidx = reinterpret_cast<int32_t*>(smem);  // S*LW
+    // X regions (one per team, each aligned to xalign), then Y regions, then
+    // (W > 1) the cross-warp reduction buffers
     const uint32_t s_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-    const uint32_t x_area = (s_base + sizeof(int32_t) * p.S * 32 + p.xalign - 1) &
+    const uint32_t x_area = (s_base + sizeof(int32_t) * p.S * LW + p.xalign - 1) &
                             ~static_cast<uint32_t>(p.xalign - 1);
-    const int nwarps = blockDim.x / 32;
-    double* s_y = reinterpret_cast<double*>(smem + (x_area - s_base) + static_cast<size_t>(nwarps) * p.xalign);
+    const int nteams = blockDim.x / LW;
+    double* s_y = reinterpret_cast<double*>(smem + (x_area - s_base) + static_cast<size_t>(nteams) * p.xalign);
+    double* s_red = s_y + static_cast<size_t>(nteams) * p.yslots;
 
-    for (int i = threadIdx.x; i < p.S * 32; i += blockDim.x) s_vidx[i] = p.vidx[i];
+    for (int i = threadIdx.x; i < p.S * LW; i += blockDim.x) s_vidx[i] = p.vidx[i];
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          static_cast<uint32_t>(__cvta_generic_to_shared(&s_taddr))),
@@ -325,11 +342,12 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
     TmemWarp<RV> tw;
     tw.wcol = lane_base;  // words: columns [0, S/2)
     tw.vcol = lane_base + p.S / 2 + 2u * p.S * static_cast<uint32_t>(slot);
-    if (slot == 0) {  // words into TMEM once per lane quarter (same for every group)
+    if (slot == 0) {  // words of this quarter's team role into TMEM once (same for every group)
+        const uint16_t* wsrc = p.words + wr * 32 + lane;
         for (int t0 = 0; t0 < p.S; t0 += 4) {
             uint32_t w[2];
-            w[0] = p.words[t0 * 32 + lane] | (static_cast<uint32_t>(p.words[(t0 + 1) * 32 + lane]) << 16);
-            w[1] = p.words[(t0 + 2) * 32 + lane] | (static_cast<uint32_t>(p.words[(t0 + 3) * 32 + lane]) << 16);
+            w[0] = wsrc[t0 * LW] | (static_cast<uint32_t>(wsrc[(t0 + 1) * LW]) << 16);
+            w[1] = wsrc[(t0 + 2) * LW] | (static_cast<uint32_t>(wsrc[(t0 + 3) * LW]) << 16);
             tm_st_x2(tw.wcol + (t0 >> 1), w);
         }
         tm_wait_st();
@@ -339,41 +357,52 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
     asm volatile("tcgen05.fence::after_thread_sync;");
 
     const bool active = slot < p.cells_per_quarter;
-    Ctx<1, R, RV> c;
-    c.tm.id = warp;
-    c.tm.tid = lane;
-    c.tm.w = 0;
+    Ctx<W, R, RV> c;
+    c.tm.id = team;
+    c.tm.w = wr;
     c.tm.lane = lane;
+    c.tm.tid = wr * 32 + lane;
     c.n = p.n;
     c.P = p.P;
-    tw.xaddr = x_area + static_cast<uint32_t>(warp * p.xalign);
+    c.red = s_red + static_cast<size_t>(team) * (2 * 4 * LW);
+    c.red_buf = 0;
+    tw.xaddr = x_area + static_cast<uint32_t>(team * p.xalign);
     tw.Xs = reinterpret_cast<double*>(smem + (tw.xaddr - s_base));
-    tw.Ys = s_y + static_cast<size_t>(warp) * p.yslots;
+    tw.Ys = s_y + static_cast<size_t>(team) * p.yslots;
     tw.lane = lane;
+    tw.ylane = wr * 32 + lane;
     tw.S = p.S;
     tw.ystream = p.ystream;
 #pragma unroll
-    for (int j = 0; j < RV; ++j) tw.xy[j] = p.lane_xy[j * 32 + lane];
+    for (int j = 0; j < RV; ++j) tw.xy[j] = p.lane_xy[c.row(j)];
 #pragma unroll
-    for (int i = 0; i < (RV + 1) / 2; ++i) tw.x1[i] = CP == 2 ? p.lane_x1[i * 32 + lane] : 0u;
+    for (int i = 0; i < (RV + 1) / 2; ++i) tw.x1[i] = CP == 2 ? p.lane_x1[(i * W + wr) * 32 + lane] : 0u;
 #pragma unroll
-    for (int j = 0; j < RV; ++j) tw.xyT[j] = ALGO == kBiCG ? p.lane_xyT[j * 32 + lane] : 0u;
+    for (int j = 0; j < RV; ++j) tw.xyT[j] = ALGO == kBiCG ? p.lane_xyT[c.row(j)] : 0u;
 #pragma unroll
-    for (int i = 0; i < (RV + 1) / 2; ++i) tw.x1T[i] = (ALGO == kBiCG && CP == 2) ? p.lane_x1T[i * 32 + lane] : 0u;
-    for (int i = lane; i < p.xslots; i += 32) tw.Xs[i] = 0.0;  // zero slots stay +0.0
-    for (int i = lane; i < p.yslots; i += 32) tw.Ys[i] = 0.0;
-    __syncwarp();
-    const double nd = static_cast<double>(p.n);
+    for (int i = 0; i < (RV + 1) / 2; ++i)
+        tw.x1T[i] = (ALGO == kBiCG && CP == 2) ? p.lane_x1T[(i * W + wr) * 32 + lane] : 0u;
+    for (int i = c.tm.tid; i < p.xslots; i += LW) tw.Xs[i] = 0.0;  // zero slots stay +0.0
+    for (int i = c.tm.tid; i < p.yslots; i += LW) tw.Ys[i] = 0.0;
+    if (active) c.tm.sync();
     const double smax = p.sigma_max;
 
     while (active) {
-        unsigned int gv = 0;
-        if (lane == 0) gv = atomicAdd(p.counter, 1u);
-        const int gl = static_cast<int>(__shfl_sync(0xffffffffu, gv, 0));
+        int gl;
+        if constexpr (W == 1) {
+            unsigned int gv = 0;
+            if (lane == 0) gv = atomicAdd(p.counter, 1u);
+            gl = static_cast<int>(__shfl_sync(0xffffffffu, gv, 0));
+        } else {
+            if (c.tm.tid == 0) s_group[team] = static_cast<int>(atomicAdd(p.counter, 1u));
+            c.tm.sync();
+            gl = s_group[team];
+            c.tm.sync();
+        }
         if (gl >= p.group_count) break;
         if (p.gate.ready) {
-            if (lane == 0) gate_wait(p.gate, gl);
-            __syncwarp();
+            if (c.tm.tid == 0) gate_wait(p.gate, gl);
+            c.tm.sync();
         }
         const int64_t cell0 = p.cell_offset + static_cast<int64_t>(gl) * p.kc;
         const double* src = p.values + cell0 * p.nnz;
@@ -384,7 +413,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
             uint32_t v[8];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int vi = s_vidx[(t0 + u) * 32 + lane];
+                const int vi = s_vidx[(t0 + u) * LW + c.tm.tid];
                 const double a = vi >= 0 ? __ldg(src + vi) : 0.0;
                 v[2 * u] = static_cast<uint32_t>(__double2loint(a));
                 v[2 * u + 1] = static_cast<uint32_t>(__double2hiint(a));
@@ -411,7 +440,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
             double r[RV], rh[RV], pv[RV], v[RV];
             {
                 double ax[RV];
-                tmem_spmv<ST, CP>(tw, x, ax);
+                tmem_spmv<ST, CP>(tw, c.tm, x, ax);
     #pragma unroll
                 for (int j = 0; j < RV; ++j) {
                     const double bj = c.valid(j) ? __ldcs(bsrc + c.row(j)) : 0.0;
@@ -429,7 +458,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                     q[0][j] = dmul(r[j], r[j]);
                     q[1][j] = dmul(rh[j], r[j]);
                 }
-                tmem_reduce<2, R, RV>(q, o);
+                tmem_reduce<2>(c, q, o);
                 sigma = o[0];
                 rho_next = o[1];
             }
@@ -449,13 +478,13 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                         pv[j] = dadd(r[j], dmul(beta, dsub(pv[j], dmul(omega, v[j]))));
                         y[j] = dmul(dinv[j], pv[j]);
                     }
-                    tmem_spmv<ST, CP>(tw, y, v);
+                    tmem_spmv<ST, CP>(tw, c.tm, y, v);
                     double den;
                     {
                         double q[1][RV], o[1];
     #pragma unroll
                         for (int j = 0; j < RV; ++j) q[0][j] = dmul(rh[j], v[j]);
-                        tmem_reduce<1, R, RV>(q, o);
+                        tmem_reduce<1>(c, q, o);
                         den = o[0];
                     }
                     if (scalar_breaks(den)) { brk = true; break; }
@@ -468,7 +497,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                         x[j] = dadd(x[j], dmul(alpha, dmul(dinv[j], pv[j])));  // y = dinv*p recomputed
                     }
                     double t[RV];
-                    tmem_spmv<ST, CP>(tw, z, t);
+                    tmem_spmv<ST, CP>(tw, c.tm, z, t);
                     double tt, ts;
                     {
                         double q[2][RV], o[2];
@@ -477,7 +506,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                             q[0][j] = dmul(t[j], t[j]);
                             q[1][j] = dmul(t[j], r[j]);
                         }
-                        tmem_reduce<2, R, RV>(q, o);
+                        tmem_reduce<2>(c, q, o);
                         tt = o[0];
                         ts = o[1];
                     }
@@ -497,7 +526,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                             q[0][j] = dmul(r[j], r[j]);
                             q[1][j] = dmul(rh[j], r[j]);
                         }
-                        tmem_reduce<2, R, RV>(q, o);
+                        tmem_reduce<2>(c, q, o);
                         sigma = o[0];
                         rho_next = o[1];
                     }
@@ -523,7 +552,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
             double r[RV], rs[RV], pv[RV], ps[RV];
             {
                 double ax[RV];
-                tmem_spmv<ST, CP>(tw, x, ax);
+                tmem_spmv<ST, CP>(tw, c.tm, x, ax);
 #pragma unroll
                 for (int j = 0; j < RV; ++j) {
                     const double bj = c.valid(j) ? __ldcs(bsrc + c.row(j)) : 0.0;
@@ -541,7 +570,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                     q[0][j] = dmul(r[j], r[j]);
                     q[1][j] = dmul(rs[j], r[j]);
                 }
-                tmem_reduce<2, R, RV>(q, o);
+                tmem_reduce<2>(c, q, o);
                 sigma = o[0];
                 rho_next = o[1];
             }
@@ -563,13 +592,13 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                         }
                     }
                     double ap[RV], atps[RV];
-                    tmem_spmv_pair<CP>(tw, pv, ps, ap, atps);
+                    tmem_spmv_pair<CP>(tw, c.tm, pv, ps, ap, atps);
                     double den;
                     {
                         double q[1][RV], o[1];
 #pragma unroll
                         for (int j = 0; j < RV; ++j) q[0][j] = dmul(ps[j], ap[j]);
-                        tmem_reduce<1, R, RV>(q, o);
+                        tmem_reduce<1>(c, q, o);
                         den = o[0];
                     }
                     if (scalar_breaks(den)) { brk = true; break; }
@@ -590,7 +619,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                             q[0][j] = dmul(r[j], r[j]);
                             q[1][j] = dmul(rs[j], r[j]);
                         }
-                        tmem_reduce<2, R, RV>(q, o);
+                        tmem_reduce<2>(c, q, o);
                         sigma = o[0];
                         rho_next = o[1];
                     }
@@ -614,13 +643,13 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
 #pragma unroll
         for (int j = 0; j < RV; ++j)
             if (c.valid(j)) xdst[c.row(j)] = x[j];
-        if (lane == 0) {
+        if (c.tm.tid == 0) {
             const int64_t g = p.group_offset + gl;
             p.g_iters[g] = iters;
             p.g_rms[g] = fres;
             p.g_flags[g] = static_cast<uint8_t>((conv ? 1 : 0) | (brk ? 2 : 0));
         }
-        __syncwarp();
+        c.tm.sync();
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();

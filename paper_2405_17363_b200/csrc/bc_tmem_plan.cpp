@@ -35,7 +35,11 @@ struct TmOpt {
     // ST interleaved row streams per lane: virtual lane v = s*32 + L runs on
     // physical lane L, its virtual step u on physical step u*ST + s
     int ST = 1;
-    int VL() const { return kLanes * ST; }
+    // LW lanes per group: a team of LW/32 warps shares one cell (rows spread
+    // over all its lanes; half-warps are lanes [16h, 16h+16), H of them)
+    int LW = kLanes;
+    int H() const { return LW / 16; }
+    int VL() const { return LW * ST; }
     int cap() const { return S / ST; }
     const std::vector<int>* seg_len;
     const std::vector<std::vector<int>>* seg_cols;
@@ -47,7 +51,7 @@ struct TmOpt {
     std::vector<uint8_t> end_at;
     std::vector<int> row_lane;  // row -> lane computing it
     std::vector<int> load;
-    std::vector<int> gcost;  // [t * 2 + h]
+    std::vector<int> gcost;  // [t * H() + h]
     int gsum = 0, pub = 0, yrd = 0, yst = 0;
 
     int bank(int r, int c) const { return pos[r * ncol + c] & 15; }
@@ -100,7 +104,7 @@ struct TmOpt {
     int distinct(int t, int h, int* cols) const {
         int m = 0;
         for (int L = 16 * h; L < 16 * h + 16; ++L) {
-            const int c = col_at[t * kLanes + L];
+            const int c = col_at[t * LW + L];
             if (c < 0) continue;
             bool dup = false;
             for (int q = 0; q < m; ++q) dup |= cols[q] == c;
@@ -113,7 +117,7 @@ struct TmOpt {
         const int m = distinct(t, h, cols);
         return match_cost(cols, m, nullptr);
     }
-    int at(int v, int u) const { return (u * ST + v / kLanes) * kLanes + v % kLanes; }
+    int at(int v, int u) const { return (u * ST + v / LW) * LW + v % LW; }
     void lay_lane(int v) {
         for (int u = 0; u < cap(); ++u) {
             col_at[at(v, u)] = -1;
@@ -124,7 +128,7 @@ struct TmOpt {
             const auto& cols = (*seg_cols)[sg];
             for (size_t q = 0; q < cols.size(); ++q, ++u) col_at[at(v, u)] = cols[q];
             end_at[at(v, u - 1)] = 1;
-            row_lane[(*seg_row)[sg]] = v % kLanes;
+            row_lane[(*seg_row)[sg]] = v % LW;
         }
         load[v] = u;
     }
@@ -160,9 +164,9 @@ struct TmOpt {
     int ystore_cost() const {  // one STS.64 wavefront per half-warp with a row end
         int tot = 0;
         for (int t = 0; t < S; ++t)
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < H(); ++h) {
                 bool any = false;
-                for (int L = 16 * h; L < 16 * h + 16; ++L) any |= end_at[t * kLanes + L] != 0;
+                for (int L = 16 * h; L < 16 * h + 16; ++L) any |= end_at[t * LW + L] != 0;
                 tot += any;
             }
         return tot;
@@ -171,7 +175,7 @@ struct TmOpt {
     void full_eval() {
         gsum = 0;
         for (int t = 0; t < S; ++t)
-            for (int h = 0; h < 2; ++h) gsum += (gcost[t * 2 + h] = group_cost(t, h));
+            for (int h = 0; h < H(); ++h) gsum += (gcost[t * H() + h] = group_cost(t, h));
         pub = publish_cost();
         yrd = yread_cost();
         yst = ystore_cost();
@@ -179,14 +183,14 @@ struct TmOpt {
     // re-evaluate the gather groups of the halves holding lanes A and B
     int regather_lanes(int A, int B) {
         int g = gsum;
-        const int ha = (A % kLanes) / 16, hb = (B % kLanes) / 16;
+        const int ha = (A % LW) / 16, hb = (B % LW) / 16;
         for (int t = 0; t < S; ++t) {
-            const int id = t * 2 + ha;
+            const int id = t * H() + ha;
             const int c = group_cost(t, ha);
             g += c - gcost[id];
             gcost[id] = c;
             if (hb != ha) {
-                const int id2 = t * 2 + hb;
+                const int id2 = t * H() + hb;
                 const int c2 = group_cost(t, hb);
                 g += c2 - gcost[id2];
                 gcost[id2] = c2;
@@ -198,7 +202,7 @@ struct TmOpt {
 
 }  // namespace
 
-TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, bool optimize) {
+TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, int team, bool optimize) {
     if (const char* e = std::getenv("BC_SCHED_OPT")) optimize = optimize && std::atoi(e) != 0;
     // two placements of the gather vector: 448k vs 409k cell-solves/s with one,
     // 413k with three (B200, 100k M156, P regime; BC_GATHER_COPIES=1 overrides)
@@ -257,6 +261,7 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, bool opti
         }
     }
     TmOpt o;
+    o.LW = kLanes * std::max(1, team);
     o.seg_len = &seg_len;
     o.seg_cols = &seg_cols;
     o.seg_row = &seg_row;
@@ -269,7 +274,7 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, bool opti
     o.load.assign(o.VL(), 0);
     // lane groups a segment may use: everything, or (pair) stream 0 / stream 1
     auto group_of_seg = [&](int sg) { return pair && sg >= n_a_segs ? 1 : 0; };
-    auto group_of_lane = [&](int v) { return pair && v >= kLanes ? 1 : 0; };
+    auto group_of_lane = [&](int v) { return pair && v >= o.LW ? 1 : 0; };
     {  // longest-processing-time start
         std::vector<int> order(seg_row.size());
         std::iota(order.begin(), order.end(), 0);
@@ -326,7 +331,7 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, bool opti
         if (pair) {  // each stream's lanes carry their own rows
             int ta = 0;
             for (int sg = 0; sg < n_a_segs; ++sg) ta += seg_len[sg];
-            cap = std::max({cap, (ta + kLanes - 1) / kLanes, (total - ta + kLanes - 1) / kLanes});
+            cap = std::max({cap, (ta + o.LW - 1) / o.LW, (total - ta + o.LW - 1) / o.LW});
         }
         cap = (cap + unit - 1) / unit * unit;
         for (; cap < lpt_max; cap += unit) {
@@ -372,16 +377,16 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, bool opti
             o.owner[r * o.NS + perm[c]] = c;
         }
     }
-    o.col_at.assign(static_cast<size_t>(o.S) * kLanes, -1);
-    o.end_at.assign(static_cast<size_t>(o.S) * kLanes, 0);
+    o.col_at.assign(static_cast<size_t>(o.S) * o.LW, -1);
+    o.end_at.assign(static_cast<size_t>(o.S) * o.LW, 0);
     o.row_lane.assign(pair ? 2 * n : n, -1);
-    o.gcost.assign(static_cast<size_t>(o.S) * 2, 0);
+    o.gcost.assign(static_cast<size_t>(o.S) * o.H(), 0);
     for (int v = 0; v < o.VL(); ++v) o.lay_lane(v);
     o.full_eval();
 
     if (optimize) {
         auto urand = [&]() { return static_cast<double>(rnd() >> 11) * 0x1.0p-53; };
-        long iters = std::max<long>(20000, std::min<long>(200000, 40000000L / (o.S * kLanes)));
+        long iters = std::max<long>(20000, std::min<long>(200000, 40000000L / (o.S * o.LW)));
         if (const char* e = std::getenv("BC_ANNEAL_ITERS")) iters = std::atol(e);
         double T = 1.0;
         const double cool = std::pow(0.01 / T, 1.0 / static_cast<double>(iters));
@@ -407,13 +412,13 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, bool opti
                 touched.clear();
                 for (size_t q = 0; q < o.col_at.size(); ++q)
                     if (o.col_at[q] == c || (other >= 0 && o.col_at[q] == other))
-                        touched.push_back(static_cast<int>((q / kLanes) * 2 + (q % kLanes) / 16));
+                        touched.push_back(static_cast<int>((q / o.LW) * o.H() + (q % o.LW) / 16));
                 std::sort(touched.begin(), touched.end());
                 touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
                 int g = o.gsum;
                 std::vector<int> nc(touched.size());
                 for (size_t q = 0; q < touched.size(); ++q) {
-                    nc[q] = o.group_cost(touched[q] / 2, touched[q] % 2);
+                    nc[q] = o.group_cost(touched[q] / o.H(), touched[q] % o.H());
                     g += nc[q] - o.gcost[touched[q]];
                 }
                 const int npub = o.publish_cost();
@@ -430,7 +435,7 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, bool opti
                 // segment moves: reorder within a lane, move or exchange between lanes
                 const int A = static_cast<int>(rnd() % o.VL());
                 int B = kind == 2 ? A
-                        : pair    ? (A / kLanes) * kLanes + static_cast<int>(rnd() % kLanes)
+                        : pair    ? (A / o.LW) * o.LW + static_cast<int>(rnd() % o.LW)
                                   : static_cast<int>(rnd() % o.VL());
                 if (o.lane_segs[A].empty()) continue;
                 const auto saveA = o.lane_segs[A], saveB = o.lane_segs[B];
@@ -497,10 +502,10 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, bool opti
     ts.xpos.assign(static_cast<size_t>(o.R) * nx, 0);
     for (int r = 0; r < o.R; ++r)
         for (int i = 0; i < nx; ++i) ts.xpos[static_cast<size_t>(r) * nx + i] = r * o.NS + o.pos[r * o.ncol + i];
-    ts.words.assign(static_cast<size_t>(o.S) * kLanes, 0);
-    ts.vidx.assign(static_cast<size_t>(o.S) * kLanes, -1);
+    ts.words.assign(static_cast<size_t>(o.S) * o.LW, 0);
+    ts.vidx.assign(static_cast<size_t>(o.S) * o.LW, -1);
     ts.yslot.assign(pair ? 2 * n : n, -1);
-    std::vector<int> vals_at(static_cast<size_t>(o.S) * kLanes, -1);
+    std::vector<int> vals_at(static_cast<size_t>(o.S) * o.LW, -1);
     int kmax = 1;
     for (int v = 0; v < o.VL(); ++v) kmax = std::max(kmax, static_cast<int>(o.lane_segs[v].size()));
     // stream s's k-th row of lane L -> Y[s*kmax*32 + k*32 + L] (lane-major per stream)
@@ -508,23 +513,24 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, bool opti
         int u = 0, kk = 0;
         for (int sg : o.lane_segs[v]) {
             for (size_t q = 0; q < seg_cols[sg].size(); ++q, ++u) vals_at[o.at(v, u)] = seg_vals[sg][q];
-            ts.yslot[seg_row[sg]] = (v / kLanes) * kmax * kLanes + kk * kLanes + v % kLanes;
+            ts.yslot[seg_row[sg]] = (v / o.LW) * kmax * o.LW + kk * o.LW + v % o.LW;
             ++kk;
         }
     }
     ts.streams = o.ST;
-    ts.ystream = kmax * kLanes;
-    ts.yslots = o.ST * kmax * kLanes;
+    ts.ystream = kmax * o.LW;
+    ts.yslots = o.ST * kmax * o.LW;
+    ts.team = o.LW / kLanes;
     for (int& y : ts.yslot)
         if (y < 0) y = ts.yslots;  // empty rows read the zero slot after the last row slot
     int cost = 0;
     for (int t = 0; t < o.S; ++t)
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < o.H(); ++h) {
             int cols[16], choice[16];
             const int m = o.distinct(t, h, cols);
             cost += o.match_cost(cols, m, choice);
             for (int L = 16 * h; L < 16 * h + 16; ++L) {
-                const int id = t * kLanes + L;
+                const int id = t * o.LW + L;
                 int c = o.col_at[id], r = 0;
                 if (c < 0) {  // idle tail: broadcast a column the half already reads
                     c = m > 0 ? cols[0] : zero_col;
@@ -539,8 +545,8 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, bool opti
                 // step 4c+1 (one stream) or 4c+2 (two streams) on step 4c: the low
                 // halves of the chunk's two 32-bit TMEM words, masked off by the
                 // address LOP3
-                if ((t & 3) == 2 && o.end_at[id + kLanes]) w |= 0x8000u;
-                if ((t & 3) == 0 && o.end_at[id + (o.ST == 1 ? 1 : 2) * kLanes]) w |= 0x8000u;
+                if ((t & 3) == 2 && o.end_at[id + o.LW]) w |= 0x8000u;
+                if ((t & 3) == 0 && o.end_at[id + (o.ST == 1 ? 1 : 2) * o.LW]) w |= 0x8000u;
                 ts.words[id] = w;
                 ts.vidx[id] = vals_at[id];
             }

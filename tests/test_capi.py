@@ -225,24 +225,24 @@ def test_reduction_geometry_reproduces_tree(n):
         assert of.bits(got) == of.bits(want)
 
 
-def export_tmem_schedule(rp, ci, k, pair=0):
+def export_tmem_schedule(rp, ci, k, pair=0, team=1):
     species = len(rp) - 1
     rp = np.ascontiguousarray(rp, np.int32)
     ci = np.ascontiguousarray(ci, np.int32)
     info = np.zeros(9, np.int32)
     lib = _native.b200()
-    assert lib.bc_tmem_schedule_export(species, of.ptr(rp), of.ptr(ci), k, pair, of.ptr(info), None, None, None,
-                                       None) == 0
+    assert lib.bc_tmem_schedule_export(species, of.ptr(rp), of.ptr(ci), k, pair, team, of.ptr(info), None, None,
+                                       None, None) == 0
     S, copies = int(info[0]), int(info[5])
     mult = 2 if pair else 1
-    words = np.zeros(S * 32, np.uint16)
-    vidx = np.zeros(S * 32, np.int32)
+    words = np.zeros(S * 32 * team, np.uint16)
+    vidx = np.zeros(S * 32 * team, np.int32)
     xpos = np.zeros(copies * k * species * mult, np.int32)
     yslot = np.zeros(k * species * mult, np.int32)
-    assert lib.bc_tmem_schedule_export(species, of.ptr(rp), of.ptr(ci), k, pair, of.ptr(info), of.ptr(words),
+    assert lib.bc_tmem_schedule_export(species, of.ptr(rp), of.ptr(ci), k, pair, team, of.ptr(info), of.ptr(words),
                                        of.ptr(vidx), of.ptr(xpos), of.ptr(yslot)) == 0
     return dict(S=S, xslots=int(info[1]), zero_slot=int(info[2]), yslots=int(info[3]), cost=int(info[4]),
-                copies=copies, model=int(info[6]), streams=int(info[7]), ystream=int(info[8]), words=words,
+                copies=copies, model=int(info[6]), streams=int(info[7]), ystream=int(info[8]), team=team, words=words,
                 vidx=vidx, xpos=xpos.reshape(copies, -1), yslot=yslot)
 
 
@@ -252,17 +252,17 @@ def emulate_tmem_spmv(sc, vals, x):
     4c+2's word flags a row ending on step 4c+3, bit 15 of step 4c's a row
     ending on step 4c+1 with one stream or 4c+2 with two), stream s of lane
     L runs on steps s mod streams; its k-th row -> Y[s*ystream + k*32 + L]."""
-    S, ST = sc["S"], sc["streams"]
+    S, ST, LW = sc["S"], sc["streams"], 32 * sc["team"]
     X = np.zeros(sc["xslots"] + 1)
     for xp in sc["xpos"]:  # every copy of the gather vector
         X[xp] = x
-    Y = np.zeros(sc["yslots"] + 32)
-    words = sc["words"].reshape(S, 32)
-    for L in range(32):
+    Y = np.zeros(sc["yslots"] + LW)
+    words = sc["words"].reshape(S, LW)
+    for L in range(LW):
         acc, k = [0.0] * ST, [0] * ST
         for t in range(S):
             w = int(words[t, L])
-            vi = int(sc["vidx"][t * 32 + L])
+            vi = int(sc["vidx"][t * LW + L])
             a = float(vals[vi]) if vi >= 0 else 0.0
             s = t % ST
             acc[s] = acc[s] + a * float(X[(w & 0x7FFF) // 8])
@@ -270,16 +270,16 @@ def emulate_tmem_spmv(sc, vals, x):
                 raise AssertionError("end flag on an odd step")
             flag = t - 1 if (t & 3) == 3 else (t & ~3 if (t & 3) == ST else -1)
             if flag >= 0 and int(words[flag, L]) & 0x8000:
-                Y[s * sc["ystream"] + k[s] * 32 + L] = acc[s]
+                Y[s * sc["ystream"] + k[s] * LW + L] = acc[s]
                 k[s] += 1
                 acc[s] = 0.0
     return Y[sc["yslot"]]
 
 
-@pytest.mark.parametrize("pair", [0, 1])
+@pytest.mark.parametrize("pair,team", [(0, 1), (1, 1), (0, 2), (1, 2), (0, 4)])
 @pytest.mark.parametrize("species,k,density,seed", [(9, 1, 0.4, 0), (40, 3, 0.2, 1), (156, 1, 0.0, 2),
                                                     (100, 2, 0.05, 3), (17, 15, 0.3, 4), (60, 1, 0.02, 5)])
-def test_tmem_schedule_reproduces_spmv_order(species, k, density, seed, pair):
+def test_tmem_schedule_reproduces_spmv_order(species, k, density, seed, pair, team):
     rng = np.random.default_rng(seed)
     if density == 0.0:
         m = Mechanism(156, 468, 0)
@@ -296,7 +296,7 @@ def test_tmem_schedule_reproduces_spmv_order(species, k, density, seed, pair):
             ci = ci[keep]
             rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
     nnz = int(rp[-1])
-    sc = export_tmem_schedule(rp, ci, k, pair)
+    sc = export_tmem_schedule(rp, ci, k, pair, team)
     assert sc["S"] % 4 == 0
     vals = rng.uniform(-1, 1, k * nnz) * 10.0 ** rng.integers(-8, 8, k * nnz)
     n = k * species
