@@ -363,41 +363,80 @@ int tmem_team_pref() {
 // by the quarter, 2S value columns per warp (one group, or one team member).
 int tmem_groups_per_quarter(int S) { return S > 0 ? std::min(4, (512 - S / 2) / (2 * S)) : 0; }
 
+// The TMEM schedule of a plan for a team width, built and uploaded once.
 // BiCG plans (built with the transpose) get the pair schedule: A p and A^T p~
 // in one pass.
-void ensure_tmem_schedule(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp) {
-    if (gp.has_tm || tmem_disabled() || !tmem_fits(gp)) return;
-    const bool pair = gp.at.steps > 0;
-    int team = tmem_team_pref();
-    if (team == 0 || gp.geo.Q % team) {
-        // One warp per cell while 2 cells fit a lane quarter (8 warps/SM), else
-        // two-warp teams.  B200, 100k cells, P regime: M312 BiCG pair schedule
-        // (S = 200, 4 warps/SM alone) 209k with teams vs 157k; where 2 cells fit,
-        // teams lose to their barriers (M312 BiCGSTAB 212k vs 221k, M156 BiCG
-        // 455k vs 476k, M156 BiCGSTAB 289k vs 502k).
-        gp.tm = bc::build_tmem_schedule(pat, gp.k, pair, 1);
-        team = (tmem_groups_per_quarter(gp.tm.steps) >= 2 || gp.geo.Q % 2) ? 1 : 2;
-        if (team == 1) {
-            gp.d_tm_words = upload(ctx, gp.tm.words);
-            gp.d_tm_vidx = upload(ctx, gp.tm.vidx);
-            gp.has_tm = true;
-            return;
+bc::TmemPlan& tmem_schedule(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int team) {
+    auto it = gp.tmem.find(team);
+    if (it != gp.tmem.end()) return it->second;
+    bc::TmemPlan tp;
+    tp.tm = bc::build_tmem_schedule(pat, gp.k, gp.at.steps > 0, team);
+    tp.d_words = upload(ctx, tp.tm.words);
+    tp.d_vidx = upload(ctx, tp.tm.vidx);
+    return gp.tmem.emplace(team, std::move(tp)).first->second;
+}
+
+// Kernel instance for a schedule: same team and tree width, enough row
+// slots, and the most warps the schedule's TMEM footprint allows (capped by
+// BC_TMEM_WARPS).
+const TmemCfg* pick_tmem_cfg(const bc::GroupPlan& gp, const bc::TmemPlan& tp) {
+    const int algo = tp.tm.pair ? bc::kBiCG : bc::kBiCGStab;
+    const int cpq = tmem_groups_per_quarter(tp.tm.steps);
+    if (cpq < 1) return nullptr;
+    const int want = std::min(4 * cpq, tmem_warps_pref());
+    const int T = tp.tm.team;
+    const TmemCfg* cfg = nullptr;
+    for (const TmemCfg& t : kTmemConfigs) {
+        if (t.T != T || t.R * T != gp.geo.Q || t.RV * T < (gp.geo.n + 31) / 32 || t.warps < want ||
+            t.ST != tp.tm.streams || t.CP != tp.tm.copies || t.ALGO != algo)
+            continue;
+        if (!cfg || t.warps < cfg->warps || (t.warps == cfg->warps && t.RV < cfg->RV)) cfg = &t;
+    }
+    return cfg;
+}
+
+// Team width for a launch of `groups` groups (BC_TMEM_TEAM overrides):
+//   * batches that leave SMs idle trade cells in flight for latency: up to
+//     4 groups per SM run as four-warp teams, up to 8 as two-warp teams
+//     (B200, M156, P regime: 100 cells 30.5k cell-solves/s with four-warp
+//     teams vs 20.0k, 1000 cells 163k with two-warp teams vs 148k);
+//   * otherwise one warp per cell while 2 cells fit a lane quarter (8
+//     warps/SM), else two-warp teams: M312 BiCG's pair schedule (S = 200, 4
+//     warps/SM alone) 209k with teams vs 157k at 100k cells; where 2 cells fit,
+//     teams lose to their barriers (M312 BiCGSTAB 212k vs 221k, M156 BiCG
+//     455k vs 476k, M156 BiCGSTAB 289k vs 502k).
+// The first candidate with a kernel instance wins.
+bc::TmemPlan* tmem_plan(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int groups, const TmemCfg** cfg) {
+    if (tmem_disabled() || !tmem_fits(gp)) return nullptr;
+    int cand[3], nc = 0;
+    if (const int pref = tmem_team_pref()) cand[nc++] = pref;
+    if (groups <= 4 * ctx->sms) cand[nc++] = 4;
+    else if (groups <= 8 * ctx->sms) cand[nc++] = 2;
+    {
+        bc::TmemPlan& one = tmem_schedule(ctx, pat, gp, 1);
+        cand[nc++] = tmem_groups_per_quarter(one.tm.steps) >= 2 ? 1 : 2;
+    }
+    for (int i = 0; i < nc; ++i) {
+        const int team = cand[i];
+        if (gp.geo.Q % team) continue;
+        bc::TmemPlan& tp = tmem_schedule(ctx, pat, gp, team);
+        if (const TmemCfg* c = pick_tmem_cfg(gp, tp)) {
+            *cfg = c;
+            return &tp;
         }
     }
-    gp.tm = bc::build_tmem_schedule(pat, gp.k, pair, team);
-    gp.d_tm_words = upload(ctx, gp.tm.words);
-    gp.d_tm_vidx = upload(ctx, gp.tm.vidx);
-    gp.has_tm = true;
+    return nullptr;
 }
 
 // Per-lane owner tables for a kernel instance with RV row slots: copy-0
 // gather slot | Y slot << 16, and copy 1's slots two row slots per word; for a
 // pair schedule the same again for p~ and the A^T outputs.  Rows >= n go to
 // the trash slot (after every copy) and read the zero Y slot.
-void ensure_tmem_lane_tables(bc_ctx* ctx, bc::GroupPlan& gp, int RV) {
-    if (gp.tm_lane_rv == RV) return;
-    const int n = gp.geo.n, trash = gp.tm.xslots, nx = gp.tm.pair ? 2 * n : n, T = gp.tm.team;
-    for (int part = 0; part < (gp.tm.pair ? 2 : 1); ++part) {
+void ensure_tmem_lane_tables(bc_ctx* ctx, const bc::GroupPlan& gp, bc::TmemPlan& tp, int RV) {
+    if (tp.lane_rv == RV) return;
+    const bc::TmemSchedule& tm = tp.tm;
+    const int n = gp.geo.n, trash = tm.xslots, nx = tm.pair ? 2 * n : n, T = tm.team;
+    for (int part = 0; part < (tm.pair ? 2 : 1); ++part) {
         // owner row of (slot j, warp w, lane l) is (j*T + w)*32 + l (team_reduce's layout)
         std::vector<uint32_t> xy(static_cast<size_t>(RV) * T * 32);
         std::vector<uint32_t> x1(static_cast<size_t>((RV + 1) / 2) * T * 32, 0u);
@@ -406,49 +445,30 @@ void ensure_tmem_lane_tables(bc_ctx* ctx, bc::GroupPlan& gp, int RV) {
                 for (int l = 0; l < 32; ++l) {
                     const int row = (j * T + w) * 32 + l, col = part * n + row;
                     const bool ok = row < n;
-                    xy[row] = static_cast<uint32_t>(ok ? gp.tm.xpos[col] : trash) |
-                              (static_cast<uint32_t>(ok ? gp.tm.yslot[col] : gp.tm.yslots) << 16);
-                    const uint32_t s1 = static_cast<uint32_t>(
-                        ok && gp.tm.copies > 1 ? gp.tm.xpos[static_cast<size_t>(nx) + col] : trash);
+                    xy[row] = static_cast<uint32_t>(ok ? tm.xpos[col] : trash) |
+                              (static_cast<uint32_t>(ok ? tm.yslot[col] : tm.yslots) << 16);
+                    const uint32_t s1 =
+                        static_cast<uint32_t>(ok && tm.copies > 1 ? tm.xpos[static_cast<size_t>(nx) + col] : trash);
                     x1[((j / 2) * T + w) * 32 + l] |= s1 << (16 * (j % 2));
                 }
-        (part ? gp.d_tm_lane_xyT : gp.d_tm_lane_xy) = upload(ctx, xy);
-        (part ? gp.d_tm_lane_x1T : gp.d_tm_lane_x1) = upload(ctx, x1);
+        (part ? tp.d_xyT : tp.d_xy) = upload(ctx, xy);
+        (part ? tp.d_x1T : tp.d_x1) = upload(ctx, x1);
     }
-    gp.tm_lane_rv = RV;
-}
-
-
-// Kernel instance for a plan: same tree width R, enough row slots, and the
-// most warps the schedule's TMEM footprint allows (capped by BC_TMEM_WARPS).
-const TmemCfg* pick_tmem_cfg(const bc::GroupPlan& gp) {
-    const int algo = gp.tm.pair ? bc::kBiCG : bc::kBiCGStab;
-    const int cpq = tmem_groups_per_quarter(gp.tm.steps);
-    if (cpq < 1) return nullptr;
-    const int want = std::min(4 * cpq, tmem_warps_pref());
-    const TmemCfg* cfg = nullptr;
-    for (const TmemCfg& t : kTmemConfigs) {
-        const int T = gp.tm.team;
-        if (t.T != T || t.R * T != gp.geo.Q || t.RV * T < (gp.geo.n + 31) / 32 || t.warps < want ||
-            t.ST != gp.tm.streams || t.CP != gp.tm.copies || t.ALGO != algo)
-            continue;
-        if (!cfg || t.warps < cfg->warps || (t.warps == cfg->warps && t.RV < cfg->RV)) cfg = &t;
-    }
-    return cfg;
+    tp.lane_rv = RV;
 }
 
 bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t cell0, int64_t gout0,
                  int groups, const double* values, const double* rhs, double* x, double tol, int64_t max_iter,
                  unsigned int* counter, cudaStream_t st, const bc::InputGate& gate = bc::InputGate{}) {
-    if (tmem_disabled() || !tmem_fits(gp)) return false;
-    ensure_tmem_schedule(ctx, pat, gp);
-    const TmemCfg* cfg = pick_tmem_cfg(gp);
-    if (!cfg) return false;
-    ensure_tmem_lane_tables(ctx, gp, cfg->RV);
-    const int S = gp.tm.steps;
+    const TmemCfg* cfg = nullptr;
+    bc::TmemPlan* tpp = tmem_plan(ctx, pat, gp, groups, &cfg);
+    if (!tpp) return false;
+    bc::TmemPlan& tp = *tpp;
+    ensure_tmem_lane_tables(ctx, gp, tp, cfg->RV);
+    const int S = tp.tm.steps;
     const int cpq = std::min(cfg->warps / 4, tmem_groups_per_quarter(S));
     const int warps = 4 * cpq, T = cfg->T, teams = warps / T;
-    const int xslots = (gp.tm.xslots + 1 + 31) & ~31, yslots = gp.tm.yslots + 32 * T;
+    const int xslots = (tp.tm.xslots + 1 + 31) & ~31, yslots = tp.tm.yslots + 32 * T;
     const int xalign = static_cast<int>(bc::padded_len(8 * xslots));
     const size_t smem = sizeof(int32_t) * S * 32 * T + static_cast<size_t>(xalign) * (teams + 1) +
                         sizeof(double) * teams * yslots + (T > 1 ? sizeof(double) * teams * 2 * 4 * 32 * T : 0);
@@ -465,13 +485,13 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
     p.g_iters = ctx->giters.as<int32_t>();
     p.g_rms = ctx->grms.as<double>();
     p.g_flags = ctx->gflags.as<uint8_t>();
-    p.words = gp.d_tm_words;
-    p.vidx = gp.d_tm_vidx;
+    p.words = tp.d_words;
+    p.vidx = tp.d_vidx;
     p.didx = gp.d_didx;
-    p.lane_xy = gp.d_tm_lane_xy;
-    p.lane_x1 = gp.d_tm_lane_x1;
-    p.lane_xyT = gp.d_tm_lane_xyT;
-    p.lane_x1T = gp.d_tm_lane_x1T;
+    p.lane_xy = tp.d_xy;
+    p.lane_x1 = tp.d_x1;
+    p.lane_xyT = tp.d_xyT;
+    p.lane_x1T = tp.d_x1T;
     p.counter = counter;
     p.cell_offset = cell0;
     p.group_offset = gout0;
@@ -485,7 +505,7 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
     p.xslots = xslots;
     p.yslots = yslots;
     p.xalign = xalign;
-    p.ystream = gp.tm.ystream;
+    p.ystream = tp.tm.ystream;
     p.cells_per_quarter = cpq;
     p.sigma_max = sigma_threshold(tol, gp.geo.n);
     p.tol = tol;
@@ -981,11 +1001,9 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
         } else {
             for (const GroupSpan& sp : spans) {  // host-side planning before the timed region
                 bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);
-                {
-                    ensure_tmem_schedule(ctx, pat, gp);
-                    if (gp.has_tm)
-                        if (const TmemCfg* t = pick_tmem_cfg(gp)) ensure_tmem_lane_tables(ctx, gp, t->RV);
-                }
+                const TmemCfg* cfg = nullptr;
+                if (bc::TmemPlan* tp = tmem_plan(ctx, pat, gp, sp.count, &cfg))
+                    ensure_tmem_lane_tables(ctx, gp, *tp, cfg->RV);
             }
         }
         if (timing) check_cuda(cudaEventRecord(ctx->e0, st), "cudaEventRecord");

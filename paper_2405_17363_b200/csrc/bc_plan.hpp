@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <vector>
 
 namespace bc {
@@ -103,16 +104,19 @@ struct GroupPlan {
     int32_t* d_didx = nullptr;
     int32_t* d_xpos = nullptr;
     int32_t* d_txpos = nullptr;
-    // TMEM-kernel schedule (built on demand: BiCGSTAB, one-warp groups)
-    bool has_tm = false;
+    // TMEM-kernel schedules, built on demand per team width (1, 2, 4 warps per group)
+    std::map<int, struct TmemPlan> tmem;
+};
+
+struct TmemPlan {
     TmemSchedule tm;
-    uint16_t* d_tm_words = nullptr;
-    int32_t* d_tm_vidx = nullptr;
-    int tm_lane_rv = 0;               // RV the lane tables below were built for
-    uint32_t* d_tm_lane_xy = nullptr;
-    uint32_t* d_tm_lane_x1 = nullptr;
-    uint32_t* d_tm_lane_xyT = nullptr;  // pair schedules: p~ / A^T tables
-    uint32_t* d_tm_lane_x1T = nullptr;
+    uint16_t* d_words = nullptr;
+    int32_t* d_vidx = nullptr;
+    int lane_rv = 0;                  // RV the lane tables below were built for
+    uint32_t* d_xy = nullptr;
+    uint32_t* d_x1 = nullptr;
+    uint32_t* d_xyT = nullptr;        // pair schedules: p~ / A^T tables
+    uint32_t* d_x1T = nullptr;
 };
 
 TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair = false, int team = 1,

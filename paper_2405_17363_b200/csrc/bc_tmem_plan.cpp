@@ -212,7 +212,10 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, int team,
     // rows padded to an even number of (virtual) steps, so that rows end only
     // on steps 1, 3 (one stream) or 2, 3 (two streams) of a 4-step chunk
     constexpr int d = 2;
-    int streams = 2;  // two interleaved accumulator chains per lane (BC_TMEM_STREAMS)
+    // two interleaved accumulator chains per lane (BC_TMEM_STREAMS); four-warp
+    // teams use one, as their rows are already short (the longest row would
+    // set the step count)
+    int streams = team >= 4 ? 1 : 2;
     if (const char* e = std::getenv("BC_TMEM_STREAMS")) streams = std::atoi(e) == 1 ? 1 : 2;
     if (pair) streams = 2;  // A on stream 0, A^T on stream 1
     const int s = pat.species, nnz = pat.nnz, n = k * s;

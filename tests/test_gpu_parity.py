@@ -353,3 +353,28 @@ def test_multi_cells_random_and_breakdown(solver):
     st, res = of.orc_solve_batch(1, 0, 0, rp2, ci2, v2, b2, 1e-13, 100)
     assert st == 0
     assert_matches_oracle(rep, res, "multi breakdown")
+
+
+@pytest.mark.parametrize("team", [1, 2, 4])
+def test_tmem_teams_bitwise(m156, team, monkeypatch):
+    """Forced team widths (BC_TMEM_TEAM; by default small batches run four- or
+    two-warp teams and large ones one warp per cell): team_reduce's tree,
+    named barriers, team X/Y -- still bit-identical to the oracle."""
+    from paper_2405_17363_b200 import Solver
+    monkeypatch.setenv("BC_TMEM_TEAM", str(team))
+    s = Solver(0)
+    try:
+        for reg in (REGIME_C, REGIME_P):
+            v, b = m156.newton_batch(0, 40, 40, reg.h)
+            sysm = system_of(m156.row_ptr, m156.col_idx, v, b)
+            for algo in (Algo.BICGSTAB_JACOBI, Algo.BICG):
+                if algo == Algo.BICG and team == 4:
+                    continue  # no four-warp BiCG instance
+                rep = run_gpu(s, sysm, Strategy.BlockCells, 1, algo, reg.tol, reg.max_iter)
+                st, res = of.orc_solve_batch(2, int(algo), 1, m156.row_ptr, m156.col_idx, v, b, reg.tol,
+                                             reg.max_iter, workers=8)
+                assert st == 0
+                assert_matches_oracle(rep, res, f"team {team} {algo} {reg.name}")
+                assert rep.kernels & KERNEL_TMEM, rep.kernels
+    finally:
+        s.close()
