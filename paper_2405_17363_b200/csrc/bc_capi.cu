@@ -412,12 +412,13 @@ bc::TmemPlan* tmem_plan(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, 
     if (const int pref = tmem_team_pref()) cand[nc++] = pref;
     if (groups <= 4 * ctx->sms) cand[nc++] = 4;
     else if (groups <= 8 * ctx->sms) cand[nc++] = 2;
-    {
-        bc::TmemPlan& one = tmem_schedule(ctx, pat, gp, 1);
-        cand[nc++] = tmem_groups_per_quarter(one.tm.steps) >= 2 ? 1 : 2;
-    }
+    cand[nc++] = 0;  // the default, decided from the one-warp schedule below
     for (int i = 0; i < nc; ++i) {
-        const int team = cand[i];
+        int team = cand[i];
+        if (team == 0) {
+            bc::TmemPlan& one = tmem_schedule(ctx, pat, gp, 1);
+            team = tmem_groups_per_quarter(one.tm.steps) >= 2 ? 1 : 2;
+        }
         if (gp.geo.Q % team) continue;
         bc::TmemPlan& tp = tmem_schedule(ctx, pat, gp, team);
         if (const TmemCfg* c = pick_tmem_cfg(gp, tp)) {

@@ -17,6 +17,9 @@
 #include <cmath>
 #include <cstdlib>
 #include <numeric>
+#include <string>
+#include <mutex>
+#include <map>
 #include <stdexcept>
 
 #include "bc_plan.hpp"
@@ -202,7 +205,9 @@ struct TmOpt {
 
 }  // namespace
 
-TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, int team, bool optimize) {
+namespace {
+
+TmemSchedule build_uncached(const Pattern& pat, int k, bool pair, int team, bool optimize) {
     if (const char* e = std::getenv("BC_SCHED_OPT")) optimize = optimize && std::atoi(e) != 0;
     // two placements of the gather vector: 448k vs 409k cell-solves/s with one,
     // 413k with three (B200, 100k M156, P regime; BC_GATHER_COPIES=1 overrides)
@@ -389,7 +394,13 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, int team,
 
     if (optimize) {
         auto urand = [&]() { return static_cast<double>(rnd() >> 11) * 0x1.0p-53; };
-        long iters = std::max<long>(20000, std::min<long>(200000, 40000000L / (o.S * o.LW)));
+        // ~128 moves per scheduled entry, 20k..200k: at M156 (200k) 511k vs
+        // 503k cell-solves/s with 24k (B200, 100k cells), a few seconds once
+        // per pattern (schedules are cached per process); small patterns stay
+        // cheap
+        long entries = 0;
+        for (int l : seg_len) entries += l;
+        long iters = std::max<long>(20000, std::min<long>(200000, 128 * entries));
         if (const char* e = std::getenv("BC_ANNEAL_ITERS")) iters = std::atol(e);
         double T = 1.0;
         const double cool = std::pow(0.01 / T, 1.0 / static_cast<double>(iters));
@@ -558,6 +569,34 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, int team,
     ts.model_total = o.total();
     if (ts.xslots * 8 > 0x7FFF) throw std::invalid_argument("TMEM schedule: gather vector too large");
     return ts;
+}
+
+}  // namespace
+
+// Schedules are deterministic functions of (pattern, k, pair, team) and the
+// tuning knobs, and cost seconds of annealing: built once per process.
+TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, int team, bool optimize) {
+    static std::mutex mu;
+    static std::map<std::string, TmemSchedule> cache;
+    std::string key;
+    auto put = [&](const void* p, size_t n) { key.append(static_cast<const char*>(p), n); };
+    const int head[5] = {pat.species, k, pair ? 1 : 0, team, optimize ? 1 : 0};
+    put(head, sizeof head);
+    for (const char* env : {"BC_SCHED_OPT", "BC_GATHER_COPIES", "BC_TMEM_STREAMS", "BC_ANNEAL_ITERS"}) {
+        const char* e = std::getenv(env);
+        key += e ? e : "-";
+        key += '|';
+    }
+    put(pat.row_ptr.data(), sizeof(int32_t) * pat.row_ptr.size());
+    put(pat.col_idx.data(), sizeof(int32_t) * pat.col_idx.size());
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    TmemSchedule ts = build_uncached(pat, k, pair, team, optimize);
+    std::lock_guard<std::mutex> lock(mu);
+    return cache.emplace(key, std::move(ts)).first->second;
 }
 
 }  // namespace bc
