@@ -2,7 +2,8 @@
 //
 // One CTA per broken-down group: densify the group's block-diagonal matrix
 // (dense_lu.cpp:8-16), LU with partial pivoting -- max magnitude, ties to the
-// lowest row, rows addressed through perm[] (dense_lu.cpp:18-63) -- forward
+// lowest row, rows physically swapped (dense_lu.cpp:18-63 addresses them
+// through perm[]; the values are the same), blocked in column panels -- forward
 // and backward substitution in the reference's summation order, then the
 // fallback residual through the group's reduction plan (one interval, or
 // block_width-wide intervals + sequential combine for Multi-cells).
@@ -43,6 +44,16 @@ __device__ __forceinline__ void lu_argmax_combine(double& m, int& i, double m2, 
     }
 }
 
+// Right-looking LU in panels of kLuPanel columns on physically swapped rows:
+// every element still receives its updates a_ij -= l_ik * u_kj one k at a
+// time in ascending k, each product and difference rounded separately, with
+// the operands the reference's unblocked loop uses -- so the factors are bit-
+// identical -- but the trailing matrix is read and written once per panel
+// instead of once per k (K-fold less L2/HBM traffic), in 32x32 tiles whose
+// L and U panels are staged in shared memory.
+constexpr int kLuPanel = 16;
+constexpr int kLuTile = 32;
+
 __global__ void __launch_bounds__(256) lu_fallback_kernel(const LuParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const LuEntry ent = p.entries[blockIdx.x];
@@ -55,75 +66,116 @@ __global__ void __launch_bounds__(256) lu_fallback_kernel(const LuParams p) {
     __shared__ double red_m[8];
     __shared__ int red_i[8];
     __shared__ int s_pivot, s_singular;
+    __shared__ double s_lt[kLuTile][kLuPanel + 1];  // L21 tile (rows x panel)
+    __shared__ double s_ut[kLuPanel][kLuTile];      // U12 tile (panel x cols)
     const int tid = threadIdx.x, nt = blockDim.x;
     const double* vals = p.values + ent.cell0 * p.nnz;
     const double* b = p.rhs + ent.cell0 * s;
+    auto A = [&](int i, int j) -> double& { return lu[static_cast<int64_t>(i) * n + j]; };
 
+    // dense_lu.cpp:8-16 densify
     for (int64_t idx = tid; idx < static_cast<int64_t>(n) * n; idx += nt) lu[idx] = 0.0;
     __syncthreads();
     for (int i = tid; i < n; i += nt) {
         const int c = i / s, r = i % s;
-        for (int e = p.row_ptr[r]; e < p.row_ptr[r + 1]; ++e)
-            lu[static_cast<int64_t>(i) * n + c * s + p.col_idx[e]] = vals[c * p.nnz + e];
+        for (int e = p.row_ptr[r]; e < p.row_ptr[r + 1]; ++e) A(i, c * s + p.col_idx[e]) = vals[c * p.nnz + e];
         perm[i] = i;
     }
     if (tid == 0) s_singular = 0;
     __syncthreads();
 
-    for (int k = 0; k < n; ++k) {
-        const double a0 = fabs(lu[static_cast<int64_t>(perm[k]) * n + k]);
-        double bm = -1.0;
-        int bi = n;
-        if (isnan(a0)) {
-            bm = a0;  // every later comparison with NaN fails: pivot stays k
-            bi = k;
-        } else {
-            for (int i = k + tid; i < n; i += nt) {
-                const double mag = fabs(lu[static_cast<int64_t>(perm[i]) * n + k]);
-                if (!isnan(mag)) lu_argmax_combine(bm, bi, mag, i);
+    for (int k0 = 0; k0 < n; k0 += kLuPanel) {
+        const int k1 = min(n, k0 + kLuPanel);
+        // panel factorization: columns [k0, k1), rows [k0, n)
+        for (int k = k0; k < k1; ++k) {
+            // dense_lu.cpp:32-41: largest magnitude in column k, ties to the lowest row
+            const double a0 = fabs(A(k, k));
+            double bm = -1.0;
+            int bi = n;
+            if (isnan(a0)) {
+                bm = a0;  // every later comparison with NaN fails: pivot stays k
+                bi = k;
+            } else {
+                for (int i = k + tid; i < n; i += nt) {
+                    const double mag = fabs(A(i, k));
+                    if (!isnan(mag)) lu_argmax_combine(bm, bi, mag, i);
+                }
+                for (int off = 16; off >= 1; off >>= 1) {
+                    const double m2 = __shfl_down_sync(0xffffffffu, bm, off);
+                    const int i2 = __shfl_down_sync(0xffffffffu, bi, off);
+                    lu_argmax_combine(bm, bi, m2, i2);
+                }
+                if ((tid & 31) == 0) {
+                    red_m[tid >> 5] = bm;
+                    red_i[tid >> 5] = bi;
+                }
             }
-            for (int off = 16; off >= 1; off >>= 1) {
-                const double m2 = __shfl_down_sync(0xffffffffu, bm, off);
-                const int i2 = __shfl_down_sync(0xffffffffu, bi, off);
-                lu_argmax_combine(bm, bi, m2, i2);
+            __syncthreads();
+            if (tid == 0) {
+                if (!isnan(a0)) {
+                    bm = red_m[0];
+                    bi = red_i[0];
+                    for (int w = 1; w < nt / 32; ++w) lu_argmax_combine(bm, bi, red_m[w], red_i[w]);
+                }
+                if (bm == 0.0) s_singular = 1;  // dense_lu.cpp:35
+                s_pivot = bi;
+                const int t = perm[k];
+                perm[k] = perm[bi];
+                perm[bi] = t;
             }
-            if ((tid & 31) == 0) {
-                red_m[tid >> 5] = bm;
-                red_i[tid >> 5] = bi;
+            __syncthreads();
+            if (s_singular) {
+                if (tid == 0) p.status[blockIdx.x] = 1;
+                return;
+            }
+            const int piv = s_pivot;
+            if (piv != k)  // the whole row moves (its trailing part is as stale as row k's)
+                for (int c = tid; c < n; c += nt) {
+                    const double t = A(k, c);
+                    A(k, c) = A(piv, c);
+                    A(piv, c) = t;
+                }
+            __syncthreads();
+            const double pv = A(k, k);
+            for (int i = k + 1 + tid; i < n; i += nt) A(i, k) = __ddiv_rn(A(i, k), pv);
+            __syncthreads();
+            const int w = k1 - k - 1;  // the rest of the panel
+            if (w > 0) {
+                for (int64_t idx = tid; idx < static_cast<int64_t>(n - k - 1) * w; idx += nt) {
+                    const int i = k + 1 + static_cast<int>(idx / w), j = k + 1 + static_cast<int>(idx % w);
+                    A(i, j) = __dsub_rn(A(i, j), __dmul_rn(A(i, k), A(k, j)));
+                }
+                __syncthreads();
             }
         }
-        __syncthreads();
-        if (tid == 0) {
-            if (!isnan(a0)) {
-                bm = red_m[0];
-                bi = red_i[0];
-                for (int w = 1; w < nt / 32; ++w) lu_argmax_combine(bm, bi, red_m[w], red_i[w]);
+        if (k1 == n) break;
+        // U12: rows [k0, k1), columns [k1, n): a_ij -= l_ik u_kj for k = k0 .. i-1
+        for (int j = k1 + tid; j < n; j += nt)
+            for (int k = k0; k < k1; ++k) {
+                const double ukj = A(k, j);
+                for (int i = k + 1; i < k1; ++i) A(i, j) = __dsub_rn(A(i, j), __dmul_rn(A(i, k), ukj));
             }
-            if (bm == 0.0) s_singular = 1;  // dense_lu.cpp:35
-            s_pivot = bi;
-            const int t = perm[k];
-            perm[k] = perm[bi];
-            perm[bi] = t;
-        }
         __syncthreads();
-        if (s_singular) {
-            if (tid == 0) p.status[blockIdx.x] = 1;
-            return;
+        // A22: rows and columns [k1, n), the panel's updates in ascending k per element
+        const int K = k1 - k0, m = n - k1, tiles = (m + kLuTile - 1) / kLuTile;
+        for (int t = 0; t < tiles * tiles; ++t) {
+            const int i0 = k1 + (t / tiles) * kLuTile, j0 = k1 + (t % tiles) * kLuTile;
+            for (int q = tid; q < kLuTile * kLuPanel; q += nt) {
+                const int r = q / kLuPanel, kk = q % kLuPanel;
+                s_lt[r][kk] = (i0 + r < n && kk < K) ? A(i0 + r, k0 + kk) : 0.0;
+                const int kr = q / kLuTile, c = q % kLuTile;
+                s_ut[kr][c] = (j0 + c < n && kr < K) ? A(k0 + kr, j0 + c) : 0.0;
+            }
+            __syncthreads();
+            const int c = tid % kLuTile;
+            if (j0 + c < n)
+                for (int r = tid / kLuTile; r < kLuTile && i0 + r < n; r += nt / kLuTile) {
+                    double a = A(i0 + r, j0 + c);
+                    for (int kk = 0; kk < K; ++kk) a = __dsub_rn(a, __dmul_rn(s_lt[r][kk], s_ut[kk][c]));
+                    A(i0 + r, j0 + c) = a;
+                }
+            __syncthreads();
         }
-        const int64_t pk = static_cast<int64_t>(perm[k]) * n;
-        const double pv = lu[pk + k];
-        for (int i = k + 1 + tid; i < n; i += nt) {
-            double* lik = &lu[static_cast<int64_t>(perm[i]) * n + k];
-            *lik = __ddiv_rn(*lik, pv);
-        }
-        __syncthreads();
-        const int m = n - k - 1;
-        for (int64_t idx = tid; idx < static_cast<int64_t>(m) * m; idx += nt) {
-            const int i = k + 1 + static_cast<int>(idx / m), j = k + 1 + static_cast<int>(idx % m);
-            const int64_t pi = static_cast<int64_t>(perm[i]) * n;
-            lu[pi + j] = __dsub_rn(lu[pi + j], __dmul_rn(lu[pi + k], lu[pk + j]));
-        }
-        __syncthreads();
     }
 
     // forward: L y = P b, row i subtracts j = 0..i-1 in order (wavefront)
@@ -131,19 +183,17 @@ __global__ void __launch_bounds__(256) lu_fallback_kernel(const LuParams p) {
     for (int j = 0; j < n; ++j) {
         __syncthreads();
         const double xj = sum[j];
-        for (int i = j + 1 + tid; i < n; i += nt)
-            sum[i] = __dsub_rn(sum[i], __dmul_rn(lu[static_cast<int64_t>(perm[i]) * n + j], xj));
+        for (int i = j + 1 + tid; i < n; i += nt) sum[i] = __dsub_rn(sum[i], __dmul_rn(A(i, j), xj));
     }
     __syncthreads();
     // backward: U x = y, row ii subtracts j = ii+1..n-1 in order
     for (int ii = n - 1; ii >= 0; --ii) {
-        const int64_t pr = static_cast<int64_t>(perm[ii]) * n;
-        for (int j = ii + 1 + tid; j < n; j += nt) slots[j] = __dmul_rn(lu[pr + j], sum[j]);
+        for (int j = ii + 1 + tid; j < n; j += nt) slots[j] = __dmul_rn(A(ii, j), sum[j]);
         __syncthreads();
         if (tid == 0) {
             double acc = sum[ii];
             for (int j = ii + 1; j < n; ++j) acc = __dsub_rn(acc, slots[j]);
-            sum[ii] = __ddiv_rn(acc, lu[pr + ii]);
+            sum[ii] = __ddiv_rn(acc, A(ii, ii));
         }
         __syncthreads();
     }
