@@ -401,6 +401,7 @@ TmemSchedule build_uncached(const Pattern& pat, int k, bool pair, int team, bool
         long entries = 0;
         for (int l : seg_len) entries += l;
         long iters = std::max<long>(20000, std::min<long>(200000, 128 * entries));
+        if (o.LW > kLanes) iters = std::min<long>(iters, 50000);  // teams: latency-bound small batches
         if (const char* e = std::getenv("BC_ANNEAL_ITERS")) iters = std::atol(e);
         double T = 1.0;
         const double cool = std::pow(0.01 / T, 1.0 / static_cast<double>(iters));
