@@ -394,13 +394,13 @@ TmemSchedule build_uncached(const Pattern& pat, int k, bool pair, int team, bool
 
     if (optimize) {
         auto urand = [&]() { return static_cast<double>(rnd() >> 11) * 0x1.0p-53; };
-        // ~128 moves per scheduled entry, 20k..200k: at M156 (200k) 511k vs
+        // ~128 moves per scheduled entry, 2k..200k: at M156 (200k) 511k vs
         // 503k cell-solves/s with 24k (B200, 100k cells), a few seconds once
         // per pattern (schedules are cached per process); small patterns stay
         // cheap
         long entries = 0;
         for (int l : seg_len) entries += l;
-        long iters = std::max<long>(20000, std::min<long>(200000, 128 * entries));
+        long iters = std::max<long>(2000, std::min<long>(200000, 128 * entries));
         if (o.LW > kLanes) iters = std::min<long>(iters, 50000);  // teams: latency-bound small batches
         if (const char* e = std::getenv("BC_ANNEAL_ITERS")) iters = std::atol(e);
         double T = 1.0;
