@@ -174,7 +174,27 @@ struct TmOpt {
             }
         return tot;
     }
-    int total() const { return gsum + pub + yrd + yst; }
+    // weights of the wavefront kinds in the annealing objective (BC_PUB_WEIGHT,
+    // BC_YST_WEIGHT): the model counts wavefronts, weights bias the search
+    // (B200, 100k M156: Y stores weighted 2 -> BiCG 507k vs 501k cell-solves/s)
+    int wpub = 1, wyst = 2, wyrd = 1;
+    bool copy0_fixed = false;
+    // copy1_shift (default): copy 0 keeps the identity placement and copy 1
+    // rotates each 16-column group by a shift (bank = (column + shift[group])
+    // mod 16), so the owners' publishes are conflict-free in both copies (20
+    // wavefronts per M156 SpMV, the floor, vs 37) while the shifts still give
+    // every column a second bank for the gathers (111 vs 104 wavefronts):
+    // 538k vs 515k cell-solves/s (B200, 100k M156, BiCGSTAB)
+    bool copy1_shift = true;
+    std::vector<int> shift1;
+    void place_group1(int g) {
+        for (int c = 16 * g; c < std::min(ncol, 16 * g + 16); ++c) {
+            const int slot = 16 * g + ((c % 16 + shift1[g]) % 16);
+            pos[ncol + c] = slot;
+            owner[NS + slot] = c;
+        }
+    }
+    int total() const { return gsum + wpub * pub + wyrd * yrd + wyst * yst; }
     void full_eval() {
         gsum = 0;
         for (int t = 0; t < S; ++t)
@@ -270,6 +290,13 @@ TmemSchedule build_uncached(const Pattern& pat, int k, bool pair, int team, bool
     }
     TmOpt o;
     o.LW = kLanes * std::max(1, team);
+    if (const char* e = std::getenv("BC_PUB_WEIGHT")) o.wpub = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("BC_YST_WEIGHT")) o.wyst = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("BC_YRD_WEIGHT")) o.wyrd = std::max(1, std::atoi(e));
+    if (!optimize) o.copy1_shift = false;
+    if (const char* e = std::getenv("BC_COPY0_FIXED")) o.copy0_fixed = std::atoi(e) != 0;
+    if (const char* e = std::getenv("BC_COPY1_SHIFT")) o.copy1_shift = std::atoi(e) != 0;
+    if (o.copy1_shift && copies == 2) o.copy0_fixed = true;
     o.seg_len = &seg_len;
     o.seg_cols = &seg_cols;
     o.seg_row = &seg_row;
@@ -385,6 +412,14 @@ TmemSchedule build_uncached(const Pattern& pat, int k, bool pair, int team, bool
             o.owner[r * o.NS + perm[c]] = c;
         }
     }
+    if (o.copy1_shift && o.R == 2) {
+        std::fill(o.owner.begin() + o.NS, o.owner.begin() + 2 * o.NS, -1);
+        o.shift1.assign((o.ncol + 15) / 16, 0);
+        for (size_t g = 0; g < o.shift1.size(); ++g) {
+            o.shift1[g] = static_cast<int>(rnd() % 16);
+            o.place_group1(static_cast<int>(g));
+        }
+    }
     o.col_at.assign(static_cast<size_t>(o.S) * o.LW, -1);
     o.end_at.assign(static_cast<size_t>(o.S) * o.LW, 0);
     o.row_lane.assign(pair ? 2 * n : n, -1);
@@ -411,7 +446,39 @@ TmemSchedule build_uncached(const Pattern& pat, int k, bool pair, int team, bool
         for (long it = 0; it < iters; ++it, T *= cool) {
             const int kind = static_cast<int>(rnd() % 4);
             if (kind <= 1) {  // move one column's slot within one copy
-                const int r = static_cast<int>(rnd() % o.R);
+                // copy0_fixed: copy 0 keeps the identity placement (bank = column mod 16,
+                // so the owners' publishes into it are conflict-free); copy 1 moves
+                const int r = o.copy0_fixed && o.R > 1 ? 1 + static_cast<int>(rnd() % (o.R - 1))
+                                                       : static_cast<int>(rnd() % o.R);
+                if (o.copy1_shift && r == 1) {  // re-rotate one 16-column group of copy 1
+                    const int gi = static_cast<int>(rnd() % o.shift1.size());
+                    const int old_sh = o.shift1[gi];
+                    o.shift1[gi] = static_cast<int>(rnd() % 16);
+                    if (o.shift1[gi] == old_sh) continue;
+                    o.place_group1(gi);
+                    touched.clear();
+                    for (size_t q = 0; q < o.col_at.size(); ++q)
+                        if (o.col_at[q] >= 16 * gi && o.col_at[q] < 16 * gi + 16)
+                            touched.push_back(static_cast<int>((q / o.LW) * o.H() + (q % o.LW) / 16));
+                    std::sort(touched.begin(), touched.end());
+                    touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
+                    int g = o.gsum;
+                    std::vector<int> nc(touched.size());
+                    for (size_t q = 0; q < touched.size(); ++q) {
+                        nc[q] = o.group_cost(touched[q] / o.H(), touched[q] % o.H());
+                        g += nc[q] - o.gcost[touched[q]];
+                    }
+                    const int nt = g + o.wpub * o.pub + o.wyrd * o.yrd + o.wyst * o.yst;
+                    if (nt - cur <= 0 || urand() < std::exp(-(nt - cur) / T)) {
+                        for (size_t q = 0; q < touched.size(); ++q) o.gcost[touched[q]] = nc[q];
+                        o.gsum = g;
+                        cur = nt;
+                    } else {
+                        o.shift1[gi] = old_sh;
+                        o.place_group1(gi);
+                    }
+                    continue;
+                }
                 const int c = static_cast<int>(rnd() % o.ncol);
                 const int slot = static_cast<int>(rnd() % o.NS);
                 const int other = o.owner[r * o.NS + slot];
@@ -437,7 +504,7 @@ TmemSchedule build_uncached(const Pattern& pat, int k, bool pair, int team, bool
                     g += nc[q] - o.gcost[touched[q]];
                 }
                 const int npub = o.publish_cost();
-                const int nt = g + npub + o.yrd + o.yst;
+                const int nt = g + o.wpub * npub + o.wyrd * o.yrd + o.wyst * o.yst;
                 if (nt - cur <= 0 || urand() < std::exp(-(nt - cur) / T)) {
                     for (size_t q = 0; q < touched.size(); ++q) o.gcost[touched[q]] = nc[q];
                     o.gsum = g;
@@ -583,7 +650,8 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, int team,
     auto put = [&](const void* p, size_t n) { key.append(static_cast<const char*>(p), n); };
     const int head[5] = {pat.species, k, pair ? 1 : 0, team, optimize ? 1 : 0};
     put(head, sizeof head);
-    for (const char* env : {"BC_SCHED_OPT", "BC_GATHER_COPIES", "BC_TMEM_STREAMS", "BC_ANNEAL_ITERS"}) {
+    for (const char* env : {"BC_SCHED_OPT", "BC_GATHER_COPIES", "BC_TMEM_STREAMS", "BC_ANNEAL_ITERS", "BC_PUB_WEIGHT",
+                            "BC_YST_WEIGHT", "BC_YRD_WEIGHT", "BC_COPY0_FIXED", "BC_COPY1_SHIFT"}) {
         const char* e = std::getenv(env);
         key += e ? e : "-";
         key += '|';
