@@ -366,14 +366,17 @@ int tmem_groups_per_quarter(int S) { return S > 0 ? std::min(4, (512 - S / 2) / 
 // The TMEM schedule of a plan for a team width, built and uploaded once.
 // BiCG plans (built with the transpose) get the pair schedule: A p and A^T p~
 // in one pass.
-bc::TmemPlan& tmem_schedule(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int team) {
-    auto it = gp.tmem.find(team);
+// quick: fewer annealing moves, for batches too small to be bound by the
+// shared-memory pipe.
+bc::TmemPlan& tmem_schedule(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int team, bool quick) {
+    const int key = team + (quick ? 8 : 0);
+    auto it = gp.tmem.find(key);
     if (it != gp.tmem.end()) return it->second;
     bc::TmemPlan tp;
-    tp.tm = bc::build_tmem_schedule(pat, gp.k, gp.at.steps > 0, team);
+    tp.tm = bc::build_tmem_schedule(pat, gp.k, gp.at.steps > 0, team, true, quick);
     tp.d_words = upload(ctx, tp.tm.words);
     tp.d_vidx = upload(ctx, tp.tm.vidx);
-    return gp.tmem.emplace(team, std::move(tp)).first->second;
+    return gp.tmem.emplace(key, std::move(tp)).first->second;
 }
 
 // Kernel instance for a schedule: same team and tree width, enough row
@@ -413,14 +416,15 @@ bc::TmemPlan* tmem_plan(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, 
     if (groups <= 4 * ctx->sms) cand[nc++] = 4;
     else if (groups <= 8 * ctx->sms) cand[nc++] = 2;
     cand[nc++] = 0;  // the default, decided from the one-warp schedule below
+    const bool quick = groups <= 8 * ctx->sms;
     for (int i = 0; i < nc; ++i) {
         int team = cand[i];
         if (team == 0) {
-            bc::TmemPlan& one = tmem_schedule(ctx, pat, gp, 1);
+            bc::TmemPlan& one = tmem_schedule(ctx, pat, gp, 1, quick);
             team = tmem_groups_per_quarter(one.tm.steps) >= 2 ? 1 : 2;
         }
         if (gp.geo.Q % team) continue;
-        bc::TmemPlan& tp = tmem_schedule(ctx, pat, gp, team);
+        bc::TmemPlan& tp = tmem_schedule(ctx, pat, gp, team, quick);
         if (const TmemCfg* c = pick_tmem_cfg(gp, tp)) {
             *cfg = c;
             return &tp;

@@ -120,7 +120,7 @@ struct TmemPlan {
 };
 
 TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair = false, int team = 1,
-                                  bool optimize = true);
+                                  bool optimize = true, bool quick = false);
 
 Schedule build_schedule(const Pattern& pat, int k, int lanes, bool transpose, bool optimize = true);
 GroupPlan build_group_plan(const Pattern& pat, int k, bool with_transpose, bool optimize = true);

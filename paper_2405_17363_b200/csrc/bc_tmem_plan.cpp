@@ -227,7 +227,7 @@ struct TmOpt {
 
 namespace {
 
-TmemSchedule build_uncached(const Pattern& pat, int k, bool pair, int team, bool optimize) {
+TmemSchedule build_uncached(const Pattern& pat, int k, bool pair, int team, bool optimize, bool quick) {
     if (const char* e = std::getenv("BC_SCHED_OPT")) optimize = optimize && std::atoi(e) != 0;
     // two placements of the gather vector: 448k vs 409k cell-solves/s with one,
     // 413k with three (B200, 100k M156, P regime; BC_GATHER_COPIES=1 overrides)
@@ -436,6 +436,7 @@ TmemSchedule build_uncached(const Pattern& pat, int k, bool pair, int team, bool
         long entries = 0;
         for (int l : seg_len) entries += l;
         long iters = std::max<long>(2000, std::min<long>(200000, 128 * entries));
+        if (quick) iters = std::min<long>(iters, 10000);  // small batches: latency-bound, placement matters less
         if (o.LW > kLanes) iters = std::min<long>(iters, 50000);  // teams: latency-bound small batches
         if (const char* e = std::getenv("BC_ANNEAL_ITERS")) iters = std::atol(e);
         double T = 1.0;
@@ -643,12 +644,12 @@ TmemSchedule build_uncached(const Pattern& pat, int k, bool pair, int team, bool
 
 // Schedules are deterministic functions of (pattern, k, pair, team) and the
 // tuning knobs, and cost seconds of annealing: built once per process.
-TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, int team, bool optimize) {
+TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, int team, bool optimize, bool quick) {
     static std::mutex mu;
     static std::map<std::string, TmemSchedule> cache;
     std::string key;
     auto put = [&](const void* p, size_t n) { key.append(static_cast<const char*>(p), n); };
-    const int head[5] = {pat.species, k, pair ? 1 : 0, team, optimize ? 1 : 0};
+    const int head[6] = {pat.species, k, pair ? 1 : 0, team, optimize ? 1 : 0, quick ? 1 : 0};
     put(head, sizeof head);
     for (const char* env : {"BC_SCHED_OPT", "BC_GATHER_COPIES", "BC_TMEM_STREAMS", "BC_ANNEAL_ITERS", "BC_PUB_WEIGHT",
                             "BC_YST_WEIGHT", "BC_YRD_WEIGHT", "BC_COPY0_FIXED", "BC_COPY1_SHIFT"}) {
@@ -663,7 +664,7 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, int team,
         auto it = cache.find(key);
         if (it != cache.end()) return it->second;
     }
-    TmemSchedule ts = build_uncached(pat, k, pair, team, optimize);
+    TmemSchedule ts = build_uncached(pat, k, pair, team, optimize, quick);
     std::lock_guard<std::mutex> lock(mu);
     return cache.emplace(key, std::move(ts)).first->second;
 }
