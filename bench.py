@@ -380,7 +380,13 @@ def main_b200(args):
                          "peak_kind": peak_kind,
                          "compulsory_bytes": compulsory,
                          "compulsory_frac": compulsory / (kmean / 1e3) / 1e9 / peak,
-                         "fp64_tflops": fp64},
+                         "fp64_tflops": fp64,
+                         # what actually binds the kernel (ncu --set full of the same workload, profiles/):
+                         # the per-iteration bytes never leave the SM, so HBM is not it
+                         "measured_bound": None if not tr else {
+                             "resource": "shared-memory pipe (LSU wavefronts)", "frac": tr.get("shared_pipe_frac"),
+                             "issue_active_frac": tr.get("issue_active_frac"),
+                             "fp64_pipe_frac": tr.get("fp64_pipe_frac"), "source": f"ncu tag {tr.get('tag')}"}},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -83,10 +83,15 @@ def main(tag):
             metrics["dram__bytes_read.sum"][0]] + float(metrics["dram__bytes_write.sum"][1]) * {
             "Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[metrics["dram__bytes_write.sum"][0]]
         with open(os.path.join(PROF, "ncu_block_cells_traffic.json"), "w") as f:
+            pct = lambda k: float(metrics[k][1]) / 100.0 if k in metrics else None  # noqa: E731
             json.dump({"kernel": "block_cells_tmem_kernel", "cells": 100000, "tag": tag,
                        "dram_bytes_per_launch_scaled": traffic,
+                       "shared_pipe_frac": pct("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+                       "issue_active_frac": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                       "fp64_pipe_frac": pct("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
                        "note": "dram__bytes_read.sum + dram__bytes_write.sum of one launch on the bench workload "
-                               "(100k M156 cells, P regime); compulsory bytes are 1.496e9"}, f, indent=1)
+                               "(100k M156 cells, P regime); compulsory bytes are 1.496e9; the *_frac are the same "
+                               "capture's shared-memory pipe, issue and FP64 utilisation"}, f, indent=1)
     with open(os.path.join(PROF, f"{tag}_ncu_block_cells_tmem.txt"), "w") as f:
         f.write("\n".join(lines) + "\n")
     for name in (f"launches_{tag}.csv", f"bench_{tag}.json", "microbench_b200.json"):
