@@ -361,7 +361,10 @@ int tmem_team_pref() {
 
 // Warps per TMEM lane quarter that fit 512 columns: S/2 word columns shared
 // by the quarter, 2S value columns per warp (one group, or one team member).
-int tmem_groups_per_quarter(int S) { return S > 0 ? std::min(4, (512 - S / 2) / (2 * S)) : 0; }
+// extra: further columns per warp (BiCGSTAB keeps D^-1 there: 2 per row slot).
+int tmem_groups_per_quarter(int S, int extra = 0) {
+    return S > 0 ? std::min(4, (512 - S / 2) / (2 * S + extra)) : 0;
+}
 
 // The TMEM schedule of a plan for a team width, built and uploaded once.
 // BiCG plans (built with the transpose) get the pair schedule: A p and A^T p~
@@ -384,10 +387,11 @@ bc::TmemPlan& tmem_schedule(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& 
 // BC_TMEM_WARPS).
 const TmemCfg* pick_tmem_cfg(const bc::GroupPlan& gp, const bc::TmemPlan& tp) {
     const int algo = tp.tm.pair ? bc::kBiCG : bc::kBiCGStab;
-    const int cpq = tmem_groups_per_quarter(tp.tm.steps);
+    const int T = tp.tm.team;
+    const int rv_min = ((gp.geo.n + 31) / 32 + T - 1) / T;
+    const int cpq = tmem_groups_per_quarter(tp.tm.steps, algo == bc::kBiCGStab ? 2 * rv_min : 0);
     if (cpq < 1) return nullptr;
     const int want = std::min(4 * cpq, tmem_warps_pref());
-    const int T = tp.tm.team;
     const TmemCfg* cfg = nullptr;
     for (const TmemCfg& t : kTmemConfigs) {
         if (t.T != T || t.R * T != gp.geo.Q || t.RV * T < (gp.geo.n + 31) / 32 || t.warps < want ||
@@ -471,7 +475,9 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
     bc::TmemPlan& tp = *tpp;
     ensure_tmem_lane_tables(ctx, gp, tp, cfg->RV);
     const int S = tp.tm.steps;
-    const int cpq = std::min(cfg->warps / 4, tmem_groups_per_quarter(S));
+    const int cpq =
+        std::min(cfg->warps / 4, tmem_groups_per_quarter(S, cfg->ALGO == bc::kBiCGStab ? 2 * cfg->RV : 0));
+    if (cpq < 1) return false;
     const int warps = 4 * cpq, T = cfg->T, teams = warps / T;
     const int xslots = (tp.tm.xslots + 1 + 31) & ~31, yslots = tp.tm.yslots + 32 * T;
     const int xalign = static_cast<int>(bc::padded_len(8 * xslots));

@@ -103,6 +103,27 @@ __device__ __forceinline__ void tm_ld_x16(uint32_t addr, uint32_t (&r)[16]) {
         : "r"(addr));
 }
 
+// A per-lane vector of RV doubles in TMEM (two 32-bit columns each): the
+// Jacobi scaling D^-1 lives there rather than in registers.
+template <int RV>
+__device__ __forceinline__ void tm_store_vec(uint32_t col, const double (&v)[RV]) {
+#pragma unroll
+    for (int j = 0; j < RV; ++j) {
+        const uint32_t w[2] = {static_cast<uint32_t>(__double2loint(v[j])), static_cast<uint32_t>(__double2hiint(v[j]))};
+        tm_st_x2(col + 2 * j, w);
+    }
+    tm_wait_st();
+}
+template <int RV>
+__device__ __forceinline__ void tm_load_vec(uint32_t col, double (&v)[RV]) {
+    uint32_t w[RV][2];
+#pragma unroll
+    for (int j = 0; j < RV; ++j) tm_ld_x2(col + 2 * j, w[j]);
+    tm_wait_ld();
+#pragma unroll
+    for (int j = 0; j < RV; ++j) v[j] = __hiloint2double(static_cast<int>(w[j][1]), static_cast<int>(w[j][0]));
+}
+
 // Gather from the warp's X region: `xaddr` is its 32-bit shared address,
 // aligned to a power of two above every offset, so the low step's address is
 // one LOP3 ((w & 0x7FFF) | xaddr, which also drops the end flag) and the high
@@ -132,6 +153,7 @@ struct TmemWarp {
     int lane;
     int ylane;              // this lane's column in the team's lane-major Y (32 * warp-in-team + lane)
     uint32_t wcol, vcol;    // TMEM addresses: words, this warp's values
+    uint32_t dcol;          // BiCGSTAB: D^-1 (2*RV columns after the values)
     int S;
     int ystream;            // Y slots per row stream
 };
@@ -341,7 +363,10 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
     const uint32_t lane_base = s_taddr + (static_cast<uint32_t>(32 * quarter) << 16);
     TmemWarp<RV> tw;
     tw.wcol = lane_base;  // words: columns [0, S/2)
-    tw.vcol = lane_base + p.S / 2 + 2u * p.S * static_cast<uint32_t>(slot);
+    // per warp: 2S value columns (+ 2*RV for BiCGSTAB's D^-1)
+    const uint32_t warp_cols = 2u * p.S + (ALGO == kBiCGStab ? 2u * RV : 0u);
+    tw.vcol = lane_base + p.S / 2 + warp_cols * static_cast<uint32_t>(slot);
+    tw.dcol = tw.vcol + 2u * p.S;
     if (slot == 0) {  // words of this quarter's team role into TMEM once (same for every group)
         const uint16_t* wsrc = p.words + wr * 32 + lane;
         for (int t0 = 0; t0 < p.S; t0 += 4) {
@@ -430,12 +455,15 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
         bool conv = false, brk = false;
         double fres = 0.0;
         if constexpr (ALGO == kBiCGStab) {
-            double dinv[RV];
+            {  // D^-1 into TMEM (read back where used: frees 2*RV registers)
+                double dinv[RV];
 #pragma unroll
-            for (int j = 0; j < RV; ++j) {
-                const int di = c.valid(j) ? p.didx[c.row(j)] : -1;
-                const double d = di >= 0 ? __ldg(src + di) : 0.0;
-                dinv[j] = c.valid(j) ? (d != 0.0 ? ddiv(1.0, d) : 1.0) : 0.0;
+                for (int j = 0; j < RV; ++j) {
+                    const int di = c.valid(j) ? p.didx[c.row(j)] : -1;
+                    const double d = di >= 0 ? __ldg(src + di) : 0.0;
+                    dinv[j] = c.valid(j) ? (d != 0.0 ? ddiv(1.0, d) : 1.0) : 0.0;
+                }
+                tm_store_vec(tw.dcol, dinv);
             }
             double r[RV], rh[RV], pv[RV], v[RV];
             {
@@ -472,7 +500,8 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                     const double rho = rho_next;
                     if (scalar_breaks(rho)) { brk = true; break; }
                     const double beta = dmul(ddiv(rho, rho_prev), ddiv(alpha, omega));
-                    double y[RV];
+                    double y[RV], dinv[RV];
+                    tm_load_vec(tw.dcol, dinv);
     #pragma unroll
                     for (int j = 0; j < RV; ++j) {
                         pv[j] = dadd(r[j], dmul(beta, dsub(pv[j], dmul(omega, v[j]))));
@@ -489,12 +518,13 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                     }
                     if (scalar_breaks(den)) { brk = true; break; }
                     alpha = ddiv(rho, den);
-                    double z[RV];
+                    double z[RV], dinv2[RV];
+                    tm_load_vec(tw.dcol, dinv2);
     #pragma unroll
                     for (int j = 0; j < RV; ++j) {
-                        r[j] = dsub(r[j], dmul(alpha, v[j]));                 // r now holds s
-                        z[j] = dmul(dinv[j], r[j]);
-                        x[j] = dadd(x[j], dmul(alpha, dmul(dinv[j], pv[j])));  // y = dinv*p recomputed
+                        r[j] = dsub(r[j], dmul(alpha, v[j]));                  // r now holds s
+                        z[j] = dmul(dinv2[j], r[j]);
+                        x[j] = dadd(x[j], dmul(alpha, dmul(dinv2[j], pv[j])));  // y = dinv*p recomputed
                     }
                     double t[RV];
                     tmem_spmv<ST, CP>(tw, c.tm, z, t);
@@ -512,9 +542,11 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                     }
                     if (tt != 0.0 && scalar_breaks(tt)) { brk = true; break; }
                     omega = tt == 0.0 ? 0.0 : ddiv(ts, tt);
+                    double dinv3[RV];
+                    tm_load_vec(tw.dcol, dinv3);
     #pragma unroll
                     for (int j = 0; j < RV; ++j) {
-                        x[j] = dadd(x[j], dmul(omega, dmul(dinv[j], r[j])));  // z = dinv*s recomputed
+                        x[j] = dadd(x[j], dmul(omega, dmul(dinv3[j], r[j])));  // z = dinv*s recomputed
                         r[j] = dsub(r[j], dmul(omega, t[j]));
                     }
                     rho_prev = rho;
