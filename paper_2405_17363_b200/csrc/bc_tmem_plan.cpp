@@ -41,6 +41,10 @@ struct TmOpt {
     // LW lanes per group: a team of LW/32 warps shares one cell (rows spread
     // over all its lanes; half-warps are lanes [16h, 16h+16), H of them)
     int LW = kLanes;
+    // stream s's Y region starts s * ybank_shift banks further round (ystream
+    // = 8 mod 16 for two streams), so owner reads of rows computed on
+    // different streams by lanes L and L+16 no longer collide
+    int ybank_shift = 0;
     int H() const { return LW / 16; }
     int VL() const { return LW * ST; }
     int cap() const { return S / ST; }
@@ -131,7 +135,7 @@ struct TmOpt {
             const auto& cols = (*seg_cols)[sg];
             for (size_t q = 0; q < cols.size(); ++q, ++u) col_at[at(v, u)] = cols[q];
             end_at[at(v, u - 1)] = 1;
-            row_lane[(*seg_row)[sg]] = v % LW;
+            row_lane[(*seg_row)[sg]] = v % LW + (v / LW) * ybank_shift;  // the row's Y bank (mod 16)
         }
         load[v] = u;
     }
@@ -304,6 +308,8 @@ TmemSchedule build_uncached(const Pattern& pat, int k, bool pair, int team, bool
     o.nrow = n;
     o.R = copies;
     o.ST = streams;
+    o.ybank_shift = o.ST == 2 ? 8 : 0;
+    if (const char* e = std::getenv("BC_YBANK_SHIFT")) o.ybank_shift = std::atoi(e) ? o.ybank_shift : 0;
     o.pair = pair;
     o.lane_segs.assign(o.VL(), {});
     o.load.assign(o.VL(), 0);
@@ -596,13 +602,13 @@ TmemSchedule build_uncached(const Pattern& pat, int k, bool pair, int team, bool
         int u = 0, kk = 0;
         for (int sg : o.lane_segs[v]) {
             for (size_t q = 0; q < seg_cols[sg].size(); ++q, ++u) vals_at[o.at(v, u)] = seg_vals[sg][q];
-            ts.yslot[seg_row[sg]] = (v / o.LW) * kmax * o.LW + kk * o.LW + v % o.LW;
+            ts.yslot[seg_row[sg]] = (v / o.LW) * (kmax * o.LW + o.ybank_shift) + kk * o.LW + v % o.LW;
             ++kk;
         }
     }
     ts.streams = o.ST;
-    ts.ystream = kmax * o.LW;
-    ts.yslots = o.ST * kmax * o.LW;
+    ts.ystream = kmax * o.LW + o.ybank_shift;
+    ts.yslots = o.ST * ts.ystream;
     ts.team = o.LW / kLanes;
     for (int& y : ts.yslot)
         if (y < 0) y = ts.yslots;  // empty rows read the zero slot after the last row slot
@@ -652,7 +658,8 @@ TmemSchedule build_tmem_schedule(const Pattern& pat, int k, bool pair, int team,
     const int head[6] = {pat.species, k, pair ? 1 : 0, team, optimize ? 1 : 0, quick ? 1 : 0};
     put(head, sizeof head);
     for (const char* env : {"BC_SCHED_OPT", "BC_GATHER_COPIES", "BC_TMEM_STREAMS", "BC_ANNEAL_ITERS", "BC_PUB_WEIGHT",
-                            "BC_YST_WEIGHT", "BC_YRD_WEIGHT", "BC_COPY0_FIXED", "BC_COPY1_SHIFT"}) {
+                            "BC_YST_WEIGHT", "BC_YRD_WEIGHT", "BC_COPY0_FIXED", "BC_COPY1_SHIFT",
+                            "BC_YBANK_SHIFT"}) {
         const char* e = std::getenv(env);
         key += e ? e : "-";
         key += '|';

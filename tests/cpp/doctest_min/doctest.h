@@ -92,6 +92,16 @@ class Approx {
         }                                                                                     \
         doctest::report(doctest_ok_, #expr " throws " #__VA_ARGS__, __FILE__, __LINE__, false); \
     } while (0)
+#define CHECK_THROWS(expr)                                                             \
+    do {                                                                               \
+        bool doctest_ok_ = false;                                                      \
+        try {                                                                          \
+            (void)(expr);                                                              \
+        } catch (...) {                                                                \
+            doctest_ok_ = true;                                                        \
+        }                                                                              \
+        doctest::report(doctest_ok_, #expr " throws", __FILE__, __LINE__, false);       \
+    } while (0)
 #define CHECK_NOTHROW(expr)                                                              \
     do {                                                                                 \
         bool doctest_ok_ = true;                                                         \
