@@ -10,6 +10,7 @@
 #include <cstddef>
 
 #include "blockcells/bicg.hpp"
+#include "blockcells/simulate.hpp"
 #include "blockcells/strategies.hpp"
 
 namespace blockcells::b200 {
@@ -28,5 +29,14 @@ Algorithm default_algorithm();
 // bicg_solve's shape (bicg.hpp:42-44) for Jacobi-BiCGSTAB.
 SolveOutcome bicgstab_solve(const CsrMatrix& a, const DenseVector& b, const DenseVector& x0, double tol,
                             std::size_t max_iter, const ReductionPlan& reduction);
+
+// run_simulation's shape (simulate.hpp:76-78) with the whole Newton loop on
+// the GPU (bc_simulate): Newton systems assembled in HBM,
+// solved by the configured strategy with the default algorithm, updated and
+// tested on the device.  Same results, errors and SolverAbort as the
+// reference's (which, linked with this shim, also solves on the GPU but
+// copies every Newton system across PCIe).  Needs libbc_workload.so.
+SimulationResult run_simulation(const MechanismSpec& mech, const SimulationConfig& config,
+                                const std::vector<CellState>& initial_states);
 
 }  // namespace blockcells::b200

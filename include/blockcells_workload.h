@@ -29,6 +29,13 @@ enum { BCW_MODE_IDEAL = 0, BCW_MODE_REALISTIC = 1 };
 
 /* generate_mechanism(species, reactions, seed) + its evaluator tables. */
 int bcw_mechanism_create(int64_t species, int64_t reactions, uint64_t seed, bcw_mechanism** out);
+/* Any mechanism (MechanismSpec, mechanism.hpp:30-40, as flat arrays: kind 0
+ * emission / 1 unimolecular / 2 bimolecular, reactants and products in CSR
+ * form) with the same evaluator tables. */
+int bcw_mechanism_from_reactions(int64_t species, int64_t reactions, const int32_t* kind,
+                                 const int32_t* reactant_ptr, const int32_t* reactants,
+                                 const int32_t* product_ptr, const int32_t* products, const double* rate_coeff,
+                                 const double* temp_exponent, bcw_mechanism** out);
 void bcw_mechanism_destroy(bcw_mechanism* m);
 int64_t bcw_species(const bcw_mechanism* m);
 int64_t bcw_reactions(const bcw_mechanism* m);

@@ -199,6 +199,43 @@ int bcw_mechanism_create(int64_t species, int64_t reactions, uint64_t seed, bcw_
     return 0;
 }
 
+// An arbitrary mechanism (a MechanismSpec given as flat arrays) with the same
+// evaluator tables (mechanism.cpp:172-219).  kind: 0 emission, 1 unimolecular,
+// 2 bimolecular.
+int bcw_mechanism_from_reactions(int64_t species, int64_t reactions, const int32_t* kind,
+                                 const int32_t* reactant_ptr, const int32_t* reactants,
+                                 const int32_t* product_ptr, const int32_t* products, const double* rate_coeff,
+                                 const double* temp_exponent, bcw_mechanism** out) {
+    if (!out || species < 1 || reactions < 0 || (reactions > 0 && (!kind || !reactant_ptr || !product_ptr ||
+                                                                   !rate_coeff || !temp_exponent)))
+        return -1;
+    bcw_mechanism* m = new (std::nothrow) bcw_mechanism;
+    if (!m) return -7;
+    m->species = species;
+    for (int64_t j = 0; j < reactions; ++j) {
+        Reaction r;
+        r.kind = kind[j] == 0 ? Emission : kind[j] == 1 ? Unimolecular : Bimolecular;
+        for (int32_t q = reactant_ptr[j]; q < reactant_ptr[j + 1]; ++q) r.reactants.push_back(reactants[q]);
+        for (int32_t q = product_ptr[j]; q < product_ptr[j + 1]; ++q) r.products.push_back(products[q]);
+        for (int64_t sp : r.reactants)
+            if (sp < 0 || sp >= species) {
+                delete m;
+                return -1;
+            }
+        for (int64_t sp : r.products)
+            if (sp < 0 || sp >= species) {
+                delete m;
+                return -1;
+            }
+        r.rate_coeff = rate_coeff[j];
+        r.temp_exponent = temp_exponent[j];
+        m->reactions.push_back(std::move(r));
+    }
+    build_tables(*m);
+    *out = m;
+    return 0;
+}
+
 void bcw_mechanism_destroy(bcw_mechanism* m) { delete m; }
 int64_t bcw_species(const bcw_mechanism* m) { return m->species; }
 int64_t bcw_reactions(const bcw_mechanism* m) { return static_cast<int64_t>(m->reactions.size()); }

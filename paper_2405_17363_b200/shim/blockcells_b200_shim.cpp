@@ -35,6 +35,7 @@
 
 #include "blockcells/dense_lu.hpp"
 #include "blockcells_b200.h"
+#include "blockcells_workload.h"
 
 namespace blockcells {
 
@@ -186,6 +187,115 @@ Algorithm default_algorithm() { return env_algorithm(); }
 SolveOutcome bicgstab_solve(const CsrMatrix& a, const DenseVector& b, const DenseVector& x0, double tol,
                             std::size_t max_iter, const ReductionPlan& reduction) {
     return single_system(Algorithm::JacobiBiCGStab, a, b, x0, tol, max_iter, reduction);
+}
+
+// simulate.cpp:72-178 with every per-cell array in HBM (bc_simulate).
+SimulationResult run_simulation(const MechanismSpec& mech, const SimulationConfig& config,
+                                const std::vector<CellState>& initial_states) {
+    if (config.cells == 0) throw std::invalid_argument("run_simulation: cells must be >= 1");
+    if (!(config.dt_seconds > 0.0)) throw std::invalid_argument("run_simulation: dt must be positive");
+    if (initial_states.size() != config.cells)
+        throw std::invalid_argument("run_simulation: one initial state per cell");
+    for (const CellState& st : initial_states)
+        if (st.concentrations.size() != mech.n_species)
+            throw std::invalid_argument("run_simulation: state dimension mismatch");
+    mech.check_invariants();  // as MechanismEvaluator's construction does
+
+    // the mechanism as flat arrays -> the evaluator tables (blockcells_workload.h)
+    const std::size_t R = mech.reactions.size(), S = mech.n_species, C = config.cells;
+    std::vector<int32_t> kind(R), rptr(R + 1, 0), rlist, pptr(R + 1, 0), plist;
+    std::vector<double> coeff(R), texp(R);
+    for (std::size_t j = 0; j < R; ++j) {
+        const Reaction& r = mech.reactions[j];
+        kind[j] = r.kind == ReactionKind::Emission ? 0 : r.kind == ReactionKind::Unimolecular ? 1 : 2;
+        for (std::size_t x : r.reactants) rlist.push_back(static_cast<int32_t>(x));
+        for (std::size_t x : r.products) plist.push_back(static_cast<int32_t>(x));
+        rptr[j + 1] = static_cast<int32_t>(rlist.size());
+        pptr[j + 1] = static_cast<int32_t>(plist.size());
+        coeff[j] = r.rate_coeff;
+        texp[j] = r.temp_exponent;
+    }
+    bcw_mechanism* m = nullptr;
+    if (bcw_mechanism_from_reactions(static_cast<int64_t>(S), static_cast<int64_t>(R), kind.data(), rptr.data(),
+                                     rlist.data(), pptr.data(), plist.data(), coeff.data(), texp.data(), &m) != 0)
+        throw std::invalid_argument("run_simulation: bad mechanism");
+    std::unique_ptr<bcw_mechanism, void (*)(bcw_mechanism*)> hold(m, bcw_mechanism_destroy);
+    const int64_t nnz = bcw_nnz(m), nstamps = bcw_stamp_count(m);
+    std::vector<int32_t> row_ptr(S + 1), col_idx(static_cast<size_t>(nnz));
+    bcw_pattern(m, row_ptr.data(), col_idx.data());
+    std::vector<int32_t> sptr(R + 1), sslot(std::max<int64_t>(nstamps, 1)), sother(std::max<int64_t>(nstamps, 1)),
+        rp2(R + 1), re2(2 * R + 1), pp2(R + 1), pr2(2 * R + 1), diag(S);
+    std::vector<double> ssign(std::max<int64_t>(nstamps, 1));
+    bcw_stamp_program(m, sptr.data(), sslot.data(), ssign.data(), sother.data(), rp2.data(), re2.data(), pp2.data(),
+                      pr2.data(), diag.data());
+    std::vector<double> rates(C * R);
+    const int mode = config.mode == ConditionMode::Ideal ? BCW_MODE_IDEAL : BCW_MODE_REALISTIC;
+    if (R > 0) bcw_rate_constants(m, 0, static_cast<int64_t>(C), static_cast<int64_t>(C), mode, rates.data(), 0);
+
+    bc_mechanism_tables t{};
+    t.species = static_cast<int32_t>(S);
+    t.reactions = static_cast<int32_t>(R);
+    t.nnz = static_cast<int32_t>(nnz);
+    t.stamps = static_cast<int32_t>(nstamps);
+    t.row_ptr = row_ptr.data();
+    t.col_idx = col_idx.data();
+    t.stamp_ptr = sptr.data();
+    t.stamp_slot = sslot.data();
+    t.stamp_other = sother.data();
+    t.stamp_sign = ssign.data();
+    t.reactant_ptr = rp2.data();
+    t.reactants = re2.data();
+    t.product_ptr = pp2.data();
+    t.products = pr2.data();
+    t.diag_slot = diag.data();
+
+    bc_sim_params prm{};
+    prm.cells = static_cast<int64_t>(C);
+    prm.steps = static_cast<int64_t>(config.steps);
+    prm.dt_seconds = config.dt_seconds;
+    prm.tol = config.tol;
+    prm.max_iter = static_cast<int64_t>(config.max_iter);
+    const Strategy kd = config.solver.strategy.kind;
+    prm.strategy = kd == Strategy::OneCell     ? BC_STRATEGY_ONE_CELL
+                   : kd == Strategy::MultiCells ? BC_STRATEGY_MULTI_CELLS
+                                                : BC_STRATEGY_BLOCK_CELLS;
+    prm.algo = env_algorithm() == Algorithm::JacobiBiCGStab ? BC_ALGO_BICGSTAB_JACOBI : BC_ALGO_BICG;
+    prm.cells_per_block = config.solver.strategy.cells_per_block
+                              ? static_cast<int64_t>(*config.solver.strategy.cells_per_block)
+                              : 0;
+    prm.max_threads_per_block = static_cast<int64_t>(config.device.max_threads_per_block);
+    prm.use_direct_reference = config.solver.use_direct_reference ? 1 : 0;
+    prm.newton_rtol = config.newton_rtol;
+    prm.max_newton_iterations = static_cast<int64_t>(config.max_newton_iterations);
+
+    std::vector<double> y(C * S);
+    for (std::size_t c = 0; c < C; ++c)
+        std::copy(initial_states[c].concentrations.begin(), initial_states[c].concentrations.end(), y.begin() + c * S);
+    std::vector<bc_step_stats> steps(std::max<std::size_t>(config.steps, 1));
+    int64_t abort_step = -1;
+    bc_ctx* ctx = context();
+    const int st = bc_simulate(ctx, &prm, &t, rates.data(), y.data(), steps.data(), &abort_step);
+    if (st == BC_ERR_SOLVER_ABORT)
+        throw SolverAbort(static_cast<std::size_t>(abort_step),
+                          "non-finite concentration at step " + std::to_string(abort_step));
+    if (st != BC_OK) raise_status(st, bc_last_error(ctx));
+
+    SimulationResult out;
+    out.final_states.resize(C);
+    for (std::size_t c = 0; c < C; ++c) out.final_states[c].concentrations.assign(y.begin() + c * S, y.begin() + (c + 1) * S);
+    for (std::size_t i = 0; i < config.steps; ++i) {
+        StepStats q;
+        q.step = static_cast<std::size_t>(steps[i].step);
+        q.newton_iterations = static_cast<std::size_t>(steps[i].newton_iterations);
+        q.iterations_effective = static_cast<std::size_t>(steps[i].iterations_effective);
+        q.iterations_sum = static_cast<std::size_t>(steps[i].iterations_sum);
+        q.max_residual_rms = steps[i].max_residual_rms;
+        q.wall_time_ns = steps[i].wall_time_ns;
+        q.breakdown_fallbacks = static_cast<std::size_t>(steps[i].breakdown_fallbacks);
+        q.clip_events = static_cast<std::size_t>(steps[i].clip_events);
+        out.per_step.push_back(q);
+    }
+    return out;
 }
 
 }  // namespace b200

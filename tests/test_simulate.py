@@ -131,3 +131,22 @@ def test_device_simulation_abort_and_trivial_cases(solver):
         np.testing.assert_array_equal(of.bits(r.final_states[c]), of.bits(r.final_states[0]))
     with pytest.raises(ValueError):
         run_device(mech, 5, REALISTIC, 1, 0.0, 1e-30, 100, Strategy.BlockCells, 1, Algo.BICG, False)
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_device_simulation_equals_reference_loop():
+    """tests/cpp/test_simulate_dropin.cpp: the shim's blockcells::b200::run_simulation
+    (bc_simulate) against the reference's run_simulation (simulate.cpp) over the
+    shim's GPU run_strategy, bit for bit, BiCG on every strategy and the LU path,
+    Jacobi-BiCGSTAB, and the same errors."""
+    import os
+    import re
+    import subprocess
+    binary = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "bin", "sim_dropin")
+    if not os.path.exists(binary):
+        pytest.skip("tests/cpp binaries not built (needs /root/reference at build time)")
+    r = subprocess.run([binary], capture_output=True, text=True, timeout=900)
+    m = re.search(r"test cases: (\d+) \| (\d+) passed \| (\d+) failed; checks: (\d+) passed \| (\d+) failed", r.stdout)
+    assert m, r.stdout[-2000:] + r.stderr[-2000:]
+    assert int(m.group(3)) == 0 and int(m.group(5)) == 0, r.stdout[-3000:]
+    assert int(m.group(1)) == 3
