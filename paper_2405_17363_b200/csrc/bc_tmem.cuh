@@ -1,5 +1,7 @@
-// bc_tmem.cuh -- Block-cells Jacobi-BiCGSTAB with the SpMV operands in Tensor
-// Memory: the B200 hot path (K1 v2).
+// bc_tmem.cuh -- the B200 hot path (K1 v3): Block-cells solves of one cell (or
+// any group whose reduction tree has <= 16 slots per lane) per warp or per
+// team of 2/4 warps, BiCG or Jacobi-BiCGSTAB, with the SpMV operands in
+// Tensor Memory.
 //
 // The v1 kernel (bc_block.cuh) is bound by shared-memory wavefronts: per SpMV
 // step a lane loads its schedule word (1 wavefront), its matrix value (2) and
@@ -8,20 +10,24 @@
 // with LDS traffic, tools/microbench.py) takes the first two off the shared-
 // memory pipe:
 //
-//   TMEM lane 32q+L, columns [0, S/2)        16-bit schedule words of lane L,
-//                                            two steps per column (one copy per
-//                                            lane quarter q, shared by its warps)
-//   TMEM lane 32q+L, columns [S/2 + 2S*s,..) fp64 values of lane L's steps for the
-//                                            group held by warp (q, s)
+//   TMEM lane 32q+L, columns [0, S/2)      16-bit schedule words of lane L
+//                                          (team role q % W), two steps per
+//                                          column, shared by the quarter's warps
+//   then per warp (q, s): 2S columns       fp64 values of lane L's steps for the
+//                                          group it holds; BiCGSTAB adds 2*RV
+//                                          columns of D^-1
 //
-// Every step's column address is warp-uniform -- exactly the tcgen05.ld.32x32b
-// shape (each thread reads its own lane).  A CTA is 4*cells_per_quarter warps,
-// owns all 512 columns and stays resident (one per SM); each warp solves one
-// group at a time, fetched from an atomic counter.  The schedule
-// (bc_plan.hpp TmemSchedule, bc_tmem_plan.cpp) pads rows to even length with
-// zero entries so the row-end test runs every other step, writes lane L's
-// k-th row to Y[k*32+L], and keeps `copies` placements of the gathered vector
-// so that almost every gather is bank-conflict free.
+// Every column address is warp-uniform -- exactly the tcgen05.ld.32x32b shape
+// (each thread reads its own lane).  A CTA owns all 512 columns and stays
+// resident (one per SM); each warp (team) solves one group at a time, fetched
+// from an atomic counter.  The schedule (bc_plan.hpp TmemSchedule,
+// bc_tmem_plan.cpp) pads rows to even length with zero entries and runs two
+// rows per lane at a time (stream 0 on even steps, stream 1 on odd), so row
+// ends are tested once per two steps with the flag riding in an address word;
+// lane L's k-th row of stream s goes to Y[s*ystream + k*32W + L]; the gathered
+// vector is kept in two placements (identity, and rotated per 16 columns) so
+// gathers almost never conflict and publishes never do.  BiCG's pair schedule
+// puts A's rows on stream 0 and A^T's on stream 1: both products in one pass.
 //
 // Rows beyond n (register slots of the padded reduction tree) carry exact
 // +0.0 through every update -- 0-(+-0) = +0, 0+(+-0) = +0, 0*0 = +0 -- so the

@@ -1,18 +1,22 @@
 // bc_tmem_plan.cpp -- schedule of the Tensor-Memory kernel (bc_tmem.cuh).
 //
 // The kernel's SpMV cost is shared-memory wavefronts (ncu: the LSU data pipe
-// is the bound).  Per SpMV a warp issues, besides the TMEM reads:
-//   * one LDS.64 gather per step          -- wavefronts = sum over the two
+// is the bound).  Per SpMV a warp (team) issues, besides the TMEM reads:
+//   * one LDS.64 gather per step          -- wavefronts = sum over the
 //     half-warps of the largest number of distinct 8-byte slots that fall in
 //     one of the 16 bank pairs (measured exactly, tools/bank_probe.py);
-//   * one STS.64 per odd step with row ends -- lane-major Y[k*32+L] makes each
-//     half-warp's stores conflict-free (1 wavefront per half with an end);
-//   * R*RV publishes of x into the gather vector(s) and RV reads of Y.
-// The gather vector is kept in R independent copies; every access picks the
-// copy whose bank is free (an exact small b-matching per half-warp).  A
-// simulated annealing over the copies' slot placements and over which lane
-// runs which (padded) row, in which order, minimises the total.  Row entries
-// keep their CSR order and rows their values, so this changes speed only.
+//   * one STS.64 per row-end position      -- lane-major Y makes each half-
+//     warp's stores conflict-free (1 wavefront per half with an end);
+//   * R*RV publishes of x into the gather vector copies and RV reads of Y.
+// The gather vector is kept in R (2) copies; every access picks the copy
+// whose bank is free (an exact small b-matching per half-warp).  Copy 0 is
+// the identity placement and copy 1 rotates each 16-column group, so the
+// owners' publishes are conflict-free.  Rows are packed into 32W lanes x ST
+// row streams (first-fit decreasing / LPT), then a simulated annealing over
+// copy 1's rotations and over which lane runs which (padded) row, in which
+// order, minimises the weighted total.  BiCG's pair schedule holds A's rows on
+// stream 0 and A^T's rows on stream 1.  Row entries keep their CSR order (A^T:
+// ascending source row) and rows their values, so this changes speed only.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
