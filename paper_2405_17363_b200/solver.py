@@ -104,7 +104,7 @@ class SolveReport:
     cells_per_block: float = 1.0
     iterations_effective: int = 0
     iterations_sum: int = 0
-    per_block_iterations: List[int] = field(default_factory=list)
+    per_block_iterations: object = None  # (groups,) int64 array: strategies.hpp:40's vector
     max_residual_rms: float = 0.0
     wall_time_ns: int = 0
     breakdown_fallbacks: int = 0
@@ -274,7 +274,7 @@ class Solver:
         return SolveReport(
             strategy=Strategy(config.kind), cells_per_block=float(rep.cells_per_block),
             iterations_effective=int(rep.iterations_effective), iterations_sum=int(rep.iterations_sum),
-            per_block_iterations=iters.astype(np.int64).tolist(), max_residual_rms=float(rep.max_residual_rms),
+            per_block_iterations=iters.astype(np.int64), max_residual_rms=float(rep.max_residual_rms),
             wall_time_ns=int(wall), breakdown_fallbacks=int(rep.breakdown_fallbacks), per_cell_x=x_out,
             per_block_residual_rms=rms, per_block_flags=flags, device_ms=float(rep.device_ms),
             kernel_launches=int(rep.kernel_launches), kernels=int(rep.kernels))

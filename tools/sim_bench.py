@@ -43,6 +43,7 @@ for algo in (Algo.BICGSTAB_JACOBI, Algo.BICG):
         continue
     el = time.perf_counter() - t0
     out[algo.name.lower()] = {"seconds": el, "cell_steps_per_s": cells * steps / el,
+                              "solve_seconds": sum(s.wall_time_ns for s in res.per_step) / 1e9,
                               "newton_iterations": [s.newton_iterations for s in res.per_step],
                               "iterations_sum": [s.iterations_sum for s in res.per_step],
                               "clip_events": [s.clip_events for s in res.per_step]}
