@@ -311,6 +311,10 @@ const TmemCfg kTmemConfigs[] = {
     BC_TMEM_CFG(1, 8, 5, 8, 2, 2, kB), BC_TMEM_CFG(1, 8, 5, 8, 2, 1, kB), BC_TMEM_CFG(1, 8, 8, 8, 2, 2, kB),
     BC_TMEM_CFG(1, 4, 4, 8, 2, 2, kB), BC_TMEM_CFG(1, 16, 10, 4, 2, 2, kB), BC_TMEM_CFG(2, 8, 5, 8, 2, 2, kB),
     BC_TMEM_CFG(2, 4, 3, 16, 2, 2, kB),
+    // four-warp teams for coupled Block-cells(k) groups of up to 1024 rows
+    // (Block-cells(N) at M156: 936 rows, 2 groups per SM)
+    BC_TMEM_CFG(4, 8, 5, 8, 1, 2, kS), BC_TMEM_CFG(4, 8, 8, 8, 1, 2, kS), BC_TMEM_CFG(4, 8, 5, 4, 2, 2, kB),
+    BC_TMEM_CFG(4, 8, 8, 4, 2, 2, kB),
 };
 #undef BC_TMEM_CFG
 
@@ -351,7 +355,7 @@ double sigma_threshold(double tol, int n) {
 
 // The TMEM kernel runs a group on a team of 1, 2 or 4 warps whatever the v1
 // team width: its reduction tree is Q/team slots per lane (Q <= 16 here).
-bool tmem_fits(const bc::GroupPlan& gp) { return gp.geo.P >= 32 && gp.geo.Q <= 16; }
+bool tmem_fits(const bc::GroupPlan& gp) { return gp.geo.P >= 32 && gp.geo.Q <= 32; }
 
 int tmem_team_pref() {
     const char* e = std::getenv("BC_TMEM_TEAM");
@@ -376,7 +380,11 @@ bc::TmemPlan& tmem_schedule(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& 
     auto it = gp.tmem.find(key);
     if (it != gp.tmem.end()) return it->second;
     bc::TmemPlan tp;
-    tp.tm = bc::build_tmem_schedule(pat, gp.k, gp.at.steps > 0, team, true, quick);
+    try {
+        tp.tm = bc::build_tmem_schedule(pat, gp.k, gp.at.steps > 0, team, true, quick);
+    } catch (const std::invalid_argument&) {  // e.g. a gather vector beyond 15-bit offsets
+        tp.tm.steps = 0;                       // no schedule: pick_tmem_cfg finds no instance
+    }
     tp.d_words = upload(ctx, tp.tm.words);
     tp.d_vidx = upload(ctx, tp.tm.vidx);
     return gp.tmem.emplace(key, std::move(tp)).first->second;
@@ -393,11 +401,19 @@ const TmemCfg* pick_tmem_cfg(const bc::GroupPlan& gp, const bc::TmemPlan& tp) {
     if (cpq < 1) return nullptr;
     const int want = std::min(4 * cpq, tmem_warps_pref());
     const TmemCfg* cfg = nullptr;
+    // among matching instances: the fewest warps >= want (most registers), else the most warps
+    auto better = [&](const TmemCfg& t, const TmemCfg* c) {
+        if (!c) return true;
+        const bool tf = t.warps >= want, cf = c->warps >= want;
+        if (tf != cf) return tf;
+        if (t.warps != c->warps) return tf ? t.warps < c->warps : t.warps > c->warps;
+        return t.RV < c->RV;
+    };
     for (const TmemCfg& t : kTmemConfigs) {
-        if (t.T != T || t.R * T != gp.geo.Q || t.RV * T < (gp.geo.n + 31) / 32 || t.warps < want ||
-            t.ST != tp.tm.streams || t.CP != tp.tm.copies || t.ALGO != algo)
+        if (t.T != T || t.R * T != gp.geo.Q || t.RV * T < (gp.geo.n + 31) / 32 || t.ST != tp.tm.streams ||
+            t.CP != tp.tm.copies || t.ALGO != algo)
             continue;
-        if (!cfg || t.warps < cfg->warps || (t.warps == cfg->warps && t.RV < cfg->RV)) cfg = &t;
+        if (better(t, cfg)) cfg = &t;
     }
     return cfg;
 }
@@ -415,15 +431,17 @@ const TmemCfg* pick_tmem_cfg(const bc::GroupPlan& gp, const bc::TmemPlan& tp) {
 // The first candidate with a kernel instance wins.
 bc::TmemPlan* tmem_plan(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int groups, const TmemCfg** cfg) {
     if (tmem_disabled() || !tmem_fits(gp)) return nullptr;
-    int cand[3], nc = 0;
+    int cand[4], nc = 0;
     if (const int pref = tmem_team_pref()) cand[nc++] = pref;
     if (groups <= 4 * ctx->sms) cand[nc++] = 4;
     else if (groups <= 8 * ctx->sms) cand[nc++] = 2;
     cand[nc++] = 0;  // the default, decided from the one-warp schedule below
+    cand[nc++] = 4;  // last resort: four-warp teams (coupled groups)
     const bool quick = groups <= 8 * ctx->sms;
     for (int i = 0; i < nc; ++i) {
         int team = cand[i];
         if (team == 0) {
+            if (gp.geo.Q > 16) continue;  // one- and two-warp trees stop at 16 slots per lane
             bc::TmemPlan& one = tmem_schedule(ctx, pat, gp, 1, quick);
             team = tmem_groups_per_quarter(one.tm.steps) >= 2 ? 1 : 2;
         }

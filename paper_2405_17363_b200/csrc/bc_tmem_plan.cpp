@@ -402,7 +402,9 @@ TmemSchedule build_uncached(const Pattern& pat, int k, bool pair, int team, bool
     }
     const int S0 = std::max(4, o.ST * *std::max_element(o.load.begin(), o.load.end()));
     o.S = (S0 + 3) & ~3;  // the kernel walks 8 steps per TMEM load pair, then a 4-step tail
-    o.NS = optimize ? ((o.ncol + o.ncol / 4 + 15) / 16) * 16 : ((o.ncol + 15) / 16) * 16;
+    // slots per copy: the rotated placements need no slack; free placement gets 25%
+    o.NS = optimize && !(o.copy1_shift && o.R == 2) ? ((o.ncol + o.ncol / 4 + 15) / 16) * 16
+                                                  : ((o.ncol + 15) / 16) * 16;
     o.pos.resize(static_cast<size_t>(o.R) * o.ncol);
     o.owner.assign(static_cast<size_t>(o.R) * o.NS, -1);
     uint64_t rng = 0x243F6A8885A308D3ull ^ static_cast<uint64_t>(n * 977 + nnz);

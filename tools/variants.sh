@@ -1,6 +1,5 @@
 cd ${GRAFT_REPO_ROOT:-.}
-for v in "" "BC_TMEM_TEAM=2"; do
-  echo "== M312 bicgstab $v"; env $v SPECIES=312 REPS=2 timeout 300 python tools/prof_block.py 100000 2>&1 | tail -1
-  echo "== M156 bicg $v"; env $v REPS=2 timeout 300 python tools/prof_block.py 100000 bicg 2>&1 | tail -1
-  echo "== M156 bicgstab 3000 $v"; env $v REPS=3 timeout 300 python tools/prof_block.py 3000 2>&1 | tail -1
-done
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | grep -v "^\.\|^$" | tail -8
+REPS=3 timeout 300 python tools/prof_block.py 100000 2>&1 | tail -1
+timeout 900 python tools/compare_strategies.py 100000 156 > /dev/null 2>&1; cp gpurun_out/strategies_m156.json gpurun_out/strategies_m156_v4.json
+timeout 900 python tools/compare_strategies.py 100000 312 > /dev/null 2>&1; cp gpurun_out/strategies_m312.json gpurun_out/strategies_m312_v4.json
