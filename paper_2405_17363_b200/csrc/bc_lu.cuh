@@ -52,7 +52,7 @@ __device__ __forceinline__ void lu_argmax_combine(double& m, int& i, double m2, 
 // instead of once per k (K-fold less L2/HBM traffic), in 32x32 tiles whose
 // L and U panels are staged in shared memory.
 constexpr int kLuPanel = 16;
-constexpr int kLuTile = 32;
+constexpr int kLuTile = 64;  // A22 tile edge: 256 threads x (4 x 4) register micro-tiles
 
 __global__ void __launch_bounds__(256) lu_fallback_kernel(const LuParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(256) lu_fallback_kernel(const LuParams p) {
     __shared__ int s_pivot, s_singular;
     __shared__ double s_lt[kLuTile][kLuPanel + 1];  // L21 tile (rows x panel)
     __shared__ double s_ut[kLuPanel][kLuTile];      // U12 tile (panel x cols)
+    static_assert(kLuTile == 64, "the A22 micro-tiling below assumes 256 threads on a 64 x 64 tile");
     const int tid = threadIdx.x, nt = blockDim.x;
     const double* vals = p.values + ent.cell0 * p.nnz;
     const double* b = p.rhs + ent.cell0 * s;
@@ -167,13 +168,37 @@ __global__ void __launch_bounds__(256) lu_fallback_kernel(const LuParams p) {
                 s_ut[kr][c] = (j0 + c < n && kr < K) ? A(k0 + kr, j0 + c) : 0.0;
             }
             __syncthreads();
-            const int c = tid % kLuTile;
-            if (j0 + c < n)
-                for (int r = tid / kLuTile; r < kLuTile && i0 + r < n; r += nt / kLuTile) {
-                    double a = A(i0 + r, j0 + c);
-                    for (int kk = 0; kk < K; ++kk) a = __dsub_rn(a, __dmul_rn(s_lt[r][kk], s_ut[kk][c]));
-                    A(i0 + r, j0 + c) = a;
+            // thread (tr, tc) owns rows 4tr..4tr+3 and columns tc + 16q of the tile; per
+            // element the panel's updates still run one k at a time in ascending order
+            const int tr = tid / 16, tc = tid % 16;
+            if (tid < 256) {
+                double a[4][4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int r = i0 + 4 * tr + i, cc = j0 + tc + 16 * q;
+                        a[i][q] = (r < n && cc < n) ? A(r, cc) : 0.0;
+                    }
+                for (int kk = 0; kk < K; ++kk) {
+                    double l[4], u[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) l[i] = s_lt[4 * tr + i][kk];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) u[q] = s_ut[kk][tc + 16 * q];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) a[i][q] = __dsub_rn(a[i][q], __dmul_rn(l[i], u[q]));
                 }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int r = i0 + 4 * tr + i, cc = j0 + tc + 16 * q;
+                        if (r < n && cc < n) A(r, cc) = a[i][q];
+                    }
+            }
             __syncthreads();
         }
     }
