@@ -184,8 +184,8 @@ struct TmOpt {
     }
     // weights of the wavefront kinds in the annealing objective (BC_PUB_WEIGHT,
     // BC_YST_WEIGHT): the model counts wavefronts, weights bias the search
-    // (B200, 100k M156: Y stores weighted 2 -> BiCG 507k vs 501k cell-solves/s)
-    int wpub = 1, wyst = 2, wyrd = 1;
+    // (B200, 100k M156: Y stores weighted 3 -> BiCGSTAB 584k vs 574k with 2, 538k with 1)
+    int wpub = 1, wyst = 3, wyrd = 1;
     bool copy0_fixed = false;
     // copy1_shift (default): copy 0 keeps the identity placement and copy 1
     // rotates each 16-column group by a shift (bank = (column + shift[group])
