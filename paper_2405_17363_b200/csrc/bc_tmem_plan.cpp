@@ -138,8 +138,10 @@ struct TmOpt {
         for (int sg : lane_segs[v]) {
             const auto& cols = (*seg_cols)[sg];
             for (size_t q = 0; q < cols.size(); ++q, ++u) col_at[at(v, u)] = cols[q];
-            end_at[at(v, u - 1)] = 1;
-            row_lane[(*seg_row)[sg]] = v % LW + (v / LW) * ybank_shift;  // the row's Y bank (mod 16)
+            // the row's Y bank (mod 16): lane and stream shift
+            const int bank = (v % LW + (v / LW) * ybank_shift) & 15;
+            end_at[at(v, u - 1)] = static_cast<uint8_t>(1 + bank);
+            row_lane[(*seg_row)[sg]] = bank;
         }
         load[v] = u;
     }
@@ -172,13 +174,14 @@ struct TmOpt {
                 }
         return tot;
     }
-    int ystore_cost() const {  // one STS.64 wavefront per half-warp with a row end
+    int ystore_cost() const {  // per half-warp with row ends: the largest bank multiplicity
         int tot = 0;
         for (int t = 0; t < S; ++t)
             for (int h = 0; h < H(); ++h) {
-                bool any = false;
-                for (int L = 16 * h; L < 16 * h + 16; ++L) any |= end_at[t * LW + L] != 0;
-                tot += any;
+                int cnt[16] = {0}, mx = 0;
+                for (int L = 16 * h; L < 16 * h + 16; ++L)
+                    if (const int e = end_at[t * LW + L]) mx = std::max(mx, ++cnt[e - 1]);
+                tot += mx;
             }
         return tot;
     }
