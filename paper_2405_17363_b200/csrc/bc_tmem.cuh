@@ -239,6 +239,10 @@ __device__ __forceinline__ void tmem_walk(const TmemWarp<RV>& tw) {
         acc[s] = 0.0;
     }
     int t0 = 0;
+    // unrolled 4x (32 steps per loop iteration): B200, 100k cells, M156
+    // BiCGSTAB 590k vs 574k cell-solves/s, BiCG 543k vs 506k, M312 275k vs
+    // 258k; 2x: 589k / 530k / 267k; 8x: 568k / 536k / 256k
+#pragma unroll 4
     for (; t0 + 8 <= tw.S; t0 += 8) {
         uint32_t w[4], v[16];
         tm_ld_x4(tw.wcol + (t0 >> 1), w);
