@@ -431,12 +431,13 @@ const TmemCfg* pick_tmem_cfg(const bc::GroupPlan& gp, const bc::TmemPlan& tp) {
 // The first candidate with a kernel instance wins.
 bc::TmemPlan* tmem_plan(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int groups, const TmemCfg** cfg) {
     if (tmem_disabled() || !tmem_fits(gp)) return nullptr;
-    int cand[4], nc = 0;
+    int cand[5], nc = 0;
     if (const int pref = tmem_team_pref()) cand[nc++] = pref;
     if (groups <= 4 * ctx->sms) cand[nc++] = 4;
     else if (groups <= 8 * ctx->sms) cand[nc++] = 2;
     cand[nc++] = 0;  // the default, decided from the one-warp schedule below
-    cand[nc++] = 4;  // last resort: four-warp teams (coupled groups)
+    cand[nc++] = 4;  // four-warp teams (coupled groups)
+    cand[nc++] = 1;  // last resort: one warp, whatever its lane-quarter occupancy
     const bool quick = groups <= 8 * ctx->sms;
     for (int i = 0; i < nc; ++i) {
         int team = cand[i];
@@ -445,7 +446,7 @@ bc::TmemPlan* tmem_plan(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, 
             bc::TmemPlan& one = tmem_schedule(ctx, pat, gp, 1, quick);
             team = tmem_groups_per_quarter(one.tm.steps) >= 2 ? 1 : 2;
         }
-        if (gp.geo.Q % team) continue;
+        if (gp.geo.Q % team || (team == 1 && gp.geo.Q > 16)) continue;
         bc::TmemPlan& tp = tmem_schedule(ctx, pat, gp, team, quick);
         if (const TmemCfg* c = pick_tmem_cfg(gp, tp)) {
             *cfg = c;
