@@ -683,16 +683,23 @@ void upload_multi_tables(const bc::Pattern& pat, DevBuf* trp, DevBuf* trow, DevB
     up(diag, dg);
 }
 
-// Dense LU fallback (bc_lu.cuh) for the listed groups; throws SingularMatrix.
+// LU fallback (bc_lu.cuh) for the listed groups; throws SingularMatrix.
 // g_rms == nullptr: solutions only (the caller computes the residual).
+// Coupled groups are factored block by block (mode 0); a group with a non-
+// finite input or result is rerun densely (mode 1), like one-cell groups.
 void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_values, const double* d_rhs,
-            double* d_x, double* g_rms, int s, int nnz, int block_width, cudaStream_t st) {
-    int64_t nmax = 0;
-    for (const auto& e : ents) nmax = std::max<int64_t>(nmax, static_cast<int64_t>(e.kc) * s);
+            double* d_x, double* g_rms, int s, int nnz, int block_width, cudaStream_t st, int mode = 0) {
+    int64_t nmax = 0, kmax = 0;
+    for (const auto& e : ents) {
+        nmax = std::max<int64_t>(nmax, static_cast<int64_t>(e.kc) * s);
+        kmax = std::max<int64_t>(kmax, e.kc);
+    }
     if (nmax > bc::kMaxGroupRows) fail(BC_ERR_INVALID_ARGUMENT, "LU fallback group exceeds 2048 rows");
+    const bool blockdiag = mode == 0 && kmax > 1;
+    const int64_t stride = blockdiag ? kmax * s * s : nmax * nmax;
     const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(ents.size()),
-                                                                 (int64_t(1) << 31) / (nmax * nmax * 8)));
-    check_cuda(ctx->lu_scratch.ensure(sizeof(double) * nmax * nmax * batch), "cudaMalloc(lu)");
+                                                                 (int64_t(1) << 31) / (stride * 8)));
+    check_cuda(ctx->lu_scratch.ensure(sizeof(double) * stride * batch), "cudaMalloc(lu)");
     check_cuda(ctx->lu_entries.ensure(sizeof(bc::LuEntry) * ents.size()), "cudaMalloc");
     check_cuda(ctx->lu_status.ensure(sizeof(int32_t) * ents.size()), "cudaMalloc");
     check_cuda(ctx->lu_rms_scratch.ensure(sizeof(double) * (ents.size() + 1)), "cudaMalloc");
@@ -718,10 +725,11 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
         lp.row_ptr = ctx->d_rp.as<int32_t>();
         lp.col_idx = ctx->d_ci.as<int32_t>();
         lp.scratch = ctx->lu_scratch.as<double>();
-        lp.n_max = nmax;
+        lp.stride = stride;
         lp.species = s;
         lp.nnz = nnz;
         lp.block_width = block_width;
+        lp.mode = blockdiag ? 0 : 1;
         bc::lu_fallback_kernel<<<cnt, 256, smem, st>>>(lp);
         check_cuda(cudaGetLastError(), "lu_fallback_kernel launch");
         ctx->launches++;
@@ -731,8 +739,15 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
     check_cuda(cudaMemcpyAsync(status.data(), ctx->lu_status.p, sizeof(int32_t) * ents.size(), cudaMemcpyDeviceToHost,
                                st), "D2H lu status");
     check_cuda(cudaStreamSynchronize(st), "lu_fallback_kernel");
-    for (int32_t v : status)
-        if (v) fail(BC_ERR_SINGULAR_MATRIX, "lu_solve: exactly singular matrix");
+    std::vector<bc::LuEntry> dense;
+    for (size_t i = 0; i < ents.size(); ++i) {
+        if (status[i] == 1) fail(BC_ERR_SINGULAR_MATRIX, "lu_solve: exactly singular matrix");
+        if (status[i] == 2) dense.push_back(ents[i]);
+    }
+    if (!dense.empty()) {
+        if (!blockdiag) fail(BC_ERR_CUDA, "lu_fallback_kernel: unexpected status");
+        run_lu(ctx, dense, d_values, d_rhs, d_x, g_rms, s, nnz, block_width, st, 1);
+    }
 }
 
 struct MultiResult {

@@ -1,12 +1,32 @@
 // bc_lu.cuh -- breakdown fallback on the device (strategies.cpp:46-60).
 //
-// One CTA per broken-down group: densify the group's block-diagonal matrix
-// (dense_lu.cpp:8-16), LU with partial pivoting -- max magnitude, ties to the
-// lowest row, rows physically swapped (dense_lu.cpp:18-63 addresses them
-// through perm[]; the values are the same), blocked in column panels -- forward
-// and backward substitution in the reference's summation order, then the
-// fallback residual through the group's reduction plan (one interval, or
-// block_width-wide intervals + sequential combine for Multi-cells).
+// One CTA per broken-down group: LU with partial pivoting of the group's
+// block-diagonal matrix (dense_lu.cpp:18-63: max magnitude, ties to the lowest
+// row; rows physically swapped here, addressed through perm[] there -- the
+// values are the same), blocked in column panels, forward and backward
+// substitution in the reference's summation order, then the fallback residual
+// through the group's reduction plan (one interval, or block_width-wide
+// intervals + sequential combine for Multi-cells).
+//
+// Two modes.
+//  * Dense (mode 1, and every one-cell group): densify the whole group
+//    (dense_lu.cpp:8-16) and factor it, exactly the reference's arithmetic.
+//  * Block-diagonal (mode 0, groups of k > 1 cells): the reference densifies a
+//    k-cell group into a (k*s)^2 matrix whose off-diagonal blocks are zero and
+//    runs the O((k*s)^3) LU over it.  With finite values every cross-block
+//    operation is `a - (+-0)` or `(+-0) * finite`, which leaves nonzero values
+//    unchanged and can only flip the SIGN OF A ZERO.  This mode factors the k
+//    diagonal blocks one after another (k^2 times less work) and replays those
+//    sign effects exactly:
+//      - factorization: a -0 entry of block c becomes +0 iff some pivot of an
+//        earlier block is negative (the update subtracts l*u = (+0/pivot)*(+0));
+//      - forward (j ascending, earlier blocks first): a row whose right-hand
+//        side is -0 becomes +0 iff some earlier column j has
+//        signbit(pivot_j) != signbit(y_j) (the product (+0/pivot_j)*y_j is -0);
+//      - backward (j ascending, in-block first): a row whose in-block sum is -0
+//        becomes +0 iff some later x_j has its sign bit set ((+0)*x_j is -0).
+//    Any non-finite input or result (where 0*inf = NaN would spread across
+//    blocks) reports status 2 and the host reruns that group in dense mode.
 #pragma once
 
 #include <cstdint>
@@ -26,14 +46,15 @@ struct LuParams {
     const double* rhs;
     double* x_out;
     double* g_rms;
-    int32_t* status;  // per entry: 0 ok, 1 singular
+    int32_t* status;  // per entry: 0 ok, 1 singular, 2 non-finite (mode 0: rerun dense)
     const LuEntry* entries;
     const int32_t* row_ptr;  // pattern (device)
     const int32_t* col_idx;
-    double* scratch;         // per entry: n_max * n_max
-    int64_t n_max;
+    double* scratch;         // per entry: `stride` doubles
+    int64_t stride;          // dense: n_max^2; block-diagonal: k_max * s^2
     int species, nnz;
     int block_width;         // 0 = single interval
+    int mode;                // 0 block-diagonal when k > 1, 1 dense
 };
 
 __device__ __forceinline__ void lu_argmax_combine(double& m, int& i, double m2, int i2) {
@@ -44,25 +65,22 @@ __device__ __forceinline__ void lu_argmax_combine(double& m, int& i, double m2, 
     }
 }
 
+__device__ __forceinline__ bool is_neg_zero(double v) { return v == 0.0 && signbit(v); }
+
 // Right-looking LU in panels of kLuPanel columns on physically swapped rows:
 // every element still receives its updates a_ij -= l_ik * u_kj one k at a
 // time in ascending k, each product and difference rounded separately, with
 // the operands the reference's unblocked loop uses -- so the factors are bit-
 // identical -- but the trailing matrix is read and written once per panel
-// instead of once per k (K-fold less L2/HBM traffic), in 32x32 tiles whose
+// instead of once per k (K-fold less L2/HBM traffic), in 64x64 tiles whose
 // L and U panels are staged in shared memory.
 constexpr int kLuPanel = 16;
 constexpr int kLuTile = 64;  // A22 tile edge: 256 threads x (4 x 4) register micro-tiles
 
-__global__ void __launch_bounds__(256) lu_fallback_kernel(const LuParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const LuEntry ent = p.entries[blockIdx.x];
-    const int s = p.species;
-    const int n = ent.kc * s;
-    double* lu = p.scratch + static_cast<size_t>(blockIdx.x) * p.n_max * p.n_max;
-    int* perm = reinterpret_cast<int*>(smem_raw);
-    double* sum = reinterpret_cast<double*>(smem_raw + sizeof(int) * ((n + 1) & ~1));
-    double* slots = sum + n;  // >= padded length (also used for products)
+// Factor the n x n row-major matrix `lu` in place (all threads of the CTA);
+// perm[] (shared) starts as the identity and records the row swaps.  Returns
+// false when the matrix is exactly singular (dense_lu.cpp:35).
+__device__ bool lu_factor(double* lu, const int n, int* perm) {
     __shared__ double red_m[8];
     __shared__ int red_i[8];
     __shared__ int s_pivot, s_singular;
@@ -70,18 +88,7 @@ __global__ void __launch_bounds__(256) lu_fallback_kernel(const LuParams p) {
     __shared__ double s_ut[kLuPanel][kLuTile];      // U12 tile (panel x cols)
     static_assert(kLuTile == 64, "the A22 micro-tiling below assumes 256 threads on a 64 x 64 tile");
     const int tid = threadIdx.x, nt = blockDim.x;
-    const double* vals = p.values + ent.cell0 * p.nnz;
-    const double* b = p.rhs + ent.cell0 * s;
     auto A = [&](int i, int j) -> double& { return lu[static_cast<int64_t>(i) * n + j]; };
-
-    // dense_lu.cpp:8-16 densify
-    for (int64_t idx = tid; idx < static_cast<int64_t>(n) * n; idx += nt) lu[idx] = 0.0;
-    __syncthreads();
-    for (int i = tid; i < n; i += nt) {
-        const int c = i / s, r = i % s;
-        for (int e = p.row_ptr[r]; e < p.row_ptr[r + 1]; ++e) A(i, c * s + p.col_idx[e]) = vals[c * p.nnz + e];
-        perm[i] = i;
-    }
     if (tid == 0) s_singular = 0;
     __syncthreads();
 
@@ -125,10 +132,7 @@ __global__ void __launch_bounds__(256) lu_fallback_kernel(const LuParams p) {
                 perm[bi] = t;
             }
             __syncthreads();
-            if (s_singular) {
-                if (tid == 0) p.status[blockIdx.x] = 1;
-                return;
-            }
+            if (s_singular) return false;
             const int piv = s_pivot;
             if (piv != k)  // the whole row moves (its trailing part is as stale as row k's)
                 for (int c = tid; c < n; c += nt) {
@@ -202,25 +206,133 @@ __global__ void __launch_bounds__(256) lu_fallback_kernel(const LuParams p) {
             __syncthreads();
         }
     }
+    return true;
+}
 
-    // forward: L y = P b, row i subtracts j = 0..i-1 in order (wavefront)
-    for (int i = tid; i < n; i += nt) sum[i] = b[perm[i]];
+// Forward substitution L y = P b (dense_lu.cpp:53-57) on y[] (shared, holding
+// P b): row i subtracts j = 0..i-1 in order, as a wavefront over j.
+__device__ void lu_forward(const double* lu, const int n, double* y) {
+    const int tid = threadIdx.x, nt = blockDim.x;
     for (int j = 0; j < n; ++j) {
         __syncthreads();
-        const double xj = sum[j];
-        for (int i = j + 1 + tid; i < n; i += nt) sum[i] = __dsub_rn(sum[i], __dmul_rn(A(i, j), xj));
+        const double xj = y[j];
+        for (int i = j + 1 + tid; i < n; i += nt)
+            y[i] = __dsub_rn(y[i], __dmul_rn(lu[static_cast<int64_t>(i) * n + j], xj));
     }
     __syncthreads();
-    // backward: U x = y, row ii subtracts j = ii+1..n-1 in order
+}
+
+// Backward substitution U x = y (dense_lu.cpp:58-62) in place on x[]: row ii
+// subtracts j = ii+1..n-1 in order.  later_neg: a -0 sum turns +0 before the
+// division (block-diagonal mode: the zero products of later blocks, see top).
+__device__ void lu_backward(const double* lu, const int n, double* x, double* slots, const bool later_neg) {
+    const int tid = threadIdx.x, nt = blockDim.x;
     for (int ii = n - 1; ii >= 0; --ii) {
-        for (int j = ii + 1 + tid; j < n; j += nt) slots[j] = __dmul_rn(A(ii, j), sum[j]);
+        for (int j = ii + 1 + tid; j < n; j += nt) slots[j] = __dmul_rn(lu[static_cast<int64_t>(ii) * n + j], x[j]);
         __syncthreads();
         if (tid == 0) {
-            double acc = sum[ii];
+            double acc = x[ii];
             for (int j = ii + 1; j < n; ++j) acc = __dsub_rn(acc, slots[j]);
-            sum[ii] = __ddiv_rn(acc, A(ii, ii));
+            if (later_neg && is_neg_zero(acc)) acc = 0.0;
+            x[ii] = __ddiv_rn(acc, lu[static_cast<int64_t>(ii) * n + ii]);
         }
         __syncthreads();
+    }
+}
+
+// Scatter cells [c0, c0 + cells) of the group into the zeroed dense matrix
+// `lu` (row length ld): dense_lu.cpp:8-16 on the block-diagonal matrix.
+__device__ void lu_densify(double* lu, const int ld, const double* vals, const int32_t* row_ptr,
+                           const int32_t* col_idx, const int s, const int nnz, const int cells) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int n = cells * s;
+    for (int64_t idx = tid; idx < static_cast<int64_t>(n) * ld; idx += nt) lu[idx] = 0.0;
+    __syncthreads();
+    for (int i = tid; i < n; i += nt) {
+        const int c = i / s, r = i % s;
+        for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e)
+            lu[static_cast<int64_t>(i) * ld + (ld == s ? 0 : c * s) + col_idx[e]] = vals[c * nnz + e];
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) lu_fallback_kernel(const LuParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const LuEntry ent = p.entries[blockIdx.x];
+    const int s = p.species;
+    const int n = ent.kc * s;
+    double* lu = p.scratch + static_cast<size_t>(blockIdx.x) * p.stride;
+    int* perm = reinterpret_cast<int*>(smem_raw);
+    double* sum = reinterpret_cast<double*>(smem_raw + sizeof(int) * ((n + 1) & ~1));
+    double* slots = sum + n;  // >= padded length (also used for products)
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const double* vals = p.values + ent.cell0 * p.nnz;
+    const double* b = p.rhs + ent.cell0 * s;
+
+    for (int i = tid; i < n; i += nt) perm[i] = i % (p.mode == 0 && ent.kc > 1 ? s : n);
+    if (p.mode == 0 && ent.kc > 1) {
+        // block-diagonal mode: finite inputs only
+        int bad = 0;
+        for (int64_t q = tid; q < static_cast<int64_t>(ent.kc) * p.nnz; q += nt) bad |= !isfinite(vals[q]);
+        for (int q = tid; q < n; q += nt) bad |= !isfinite(b[q]);
+        if (__syncthreads_or(bad)) {
+            if (tid == 0) p.status[blockIdx.x] = 2;
+            return;
+        }
+        bool neg_pivot = false, fwd_flip = false;
+        for (int c = 0; c < ent.kc; ++c) {
+            double* blk = lu + static_cast<int64_t>(c) * s * s;
+            lu_densify(blk, s, vals + static_cast<int64_t>(c) * p.nnz, p.row_ptr, p.col_idx, s, p.nnz, 1);
+            if (neg_pivot)
+                for (int q = tid; q < s * s; q += nt)
+                    if (is_neg_zero(blk[q])) blk[q] = 0.0;
+            __syncthreads();
+            if (!lu_factor(blk, s, perm + c * s)) {
+                if (tid == 0) p.status[blockIdx.x] = 1;
+                return;
+            }
+            int neg = 0, nonfinite = 0;
+            for (int q = tid; q < s * s; q += nt) nonfinite |= !isfinite(blk[q]);
+            for (int i = tid; i < s; i += nt) neg |= signbit(blk[i * s + i]) ? 1 : 0;
+            neg_pivot = __syncthreads_or(neg) || neg_pivot;
+            if (__syncthreads_or(nonfinite)) {
+                if (tid == 0) p.status[blockIdx.x] = 2;
+                return;
+            }
+            double* y = sum + c * s;
+            for (int i = tid; i < s; i += nt) {
+                double v = b[c * s + perm[c * s + i]];
+                if (fwd_flip && is_neg_zero(v)) v = 0.0;
+                y[i] = v;
+            }
+            lu_forward(blk, s, y);
+            int flip = 0;
+            for (int i = tid; i < s; i += nt) flip |= (signbit(blk[i * s + i]) != signbit(y[i])) ? 1 : 0;
+            fwd_flip = __syncthreads_or(flip) || fwd_flip;
+        }
+        bool later_neg = false;
+        for (int c = ent.kc - 1; c >= 0; --c) {
+            double* xc = sum + c * s;
+            lu_backward(lu + static_cast<int64_t>(c) * s * s, s, xc, slots, later_neg);
+            int neg = 0;
+            for (int i = tid; i < s; i += nt) neg |= signbit(xc[i]) ? 1 : 0;
+            later_neg = __syncthreads_or(neg) || later_neg;
+        }
+        int nonfinite = 0;
+        for (int i = tid; i < n; i += nt) nonfinite |= !isfinite(sum[i]);
+        if (__syncthreads_or(nonfinite)) {
+            if (tid == 0) p.status[blockIdx.x] = 2;
+            return;
+        }
+    } else {
+        lu_densify(lu, n, vals, p.row_ptr, p.col_idx, s, p.nnz, ent.kc);
+        if (!lu_factor(lu, n, perm)) {
+            if (tid == 0) p.status[blockIdx.x] = 1;
+            return;
+        }
+        for (int i = tid; i < n; i += nt) sum[i] = b[perm[i]];
+        lu_forward(lu, n, sum);
+        lu_backward(lu, n, sum, slots, false);
     }
     double* xo = p.x_out + ent.cell0 * s;
     for (int i = tid; i < n; i += nt) xo[i] = sum[i];
