@@ -709,10 +709,18 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
     check_cuda(cudaMemcpyAsync(ctx->lu_entries.p, dev_ents.data(), sizeof(bc::LuEntry) * dev_ents.size(),
                                cudaMemcpyHostToDevice, st), "H2D lu entries");
     const int64_t pmax = bc::padded_len(nmax);
-    const size_t smem = sizeof(int) * ((nmax + 1) & ~1) + sizeof(double) * (nmax + std::max(pmax, nmax));
-    if (smem > 48 * 1024)
-        check_cuda(cudaFuncSetAttribute(bc::lu_fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        kMaxDynSmem - 1024), "cudaFuncSetAttribute(lu)");
+    // panels in shared memory while a panel of the largest factored matrix fits in 48 KB
+    const int64_t prow = blockdiag ? s : nmax;
+    const int panel_rows = prow * (bc::kLuPanel + 1) * 8 <= 48 * 1024 ? static_cast<int>(prow) : 0;
+    const size_t smem = sizeof(double) * panel_rows * (bc::kLuPanel + 1) + sizeof(int) * ((nmax + 1) & ~1) +
+                        sizeof(double) * (nmax + std::max(pmax, nmax));
+    // opt in above 48 KB of static + dynamic shared memory (per device: set on every call)
+    cudaFuncAttributes fa{};
+    check_cuda(cudaFuncGetAttributes(&fa, bc::lu_fallback_kernel), "cudaFuncGetAttributes(lu)");
+    const int lu_dyn_max = kMaxDynSmem - static_cast<int>(fa.sharedSizeBytes);
+    check_cuda(cudaFuncSetAttribute(bc::lu_fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_dyn_max),
+               "cudaFuncSetAttribute(lu)");
+    if (smem > static_cast<size_t>(lu_dyn_max)) fail(BC_ERR_INVALID_ARGUMENT, "LU fallback: group too large");
     for (size_t b0 = 0; b0 < ents.size(); b0 += batch) {
         const int cnt = static_cast<int>(std::min<int64_t>(batch, ents.size() - b0));
         bc::LuParams lp{};
@@ -730,6 +738,7 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
         lp.nnz = nnz;
         lp.block_width = block_width;
         lp.mode = blockdiag ? 0 : 1;
+        lp.panel_rows = panel_rows;
         bc::lu_fallback_kernel<<<cnt, 256, smem, st>>>(lp);
         check_cuda(cudaGetLastError(), "lu_fallback_kernel launch");
         ctx->launches++;

@@ -55,6 +55,7 @@ struct LuParams {
     int species, nnz;
     int block_width;         // 0 = single interval
     int mode;                // 0 block-diagonal when k > 1, 1 dense
+    int panel_rows;          // > 0: panels are factored in shared memory (rows <= panel_rows)
 };
 
 __device__ __forceinline__ void lu_argmax_combine(double& m, int& i, double m2, int i2) {
@@ -80,7 +81,79 @@ constexpr int kLuTile = 64;  // A22 tile edge: 256 threads x (4 x 4) register mi
 // Factor the n x n row-major matrix `lu` in place (all threads of the CTA);
 // perm[] (shared) starts as the identity and records the row swaps.  Returns
 // false when the matrix is exactly singular (dense_lu.cpp:35).
-__device__ bool lu_factor(double* lu, const int n, int* perm) {
+// Panel of columns [k0, k1) factored by warp 0 in shared memory (pbuf: rows
+// [k0, n) x kLuPanel + 1): the same pivot choice and per-element update order
+// as the CTA-wide loop below, with warp syncs instead of CTA barriers.  Row
+// swaps are applied to the panel here and to the other columns afterwards
+// (nothing else reads them in between).  Returns false if singular.
+__device__ bool lu_panel_warp(double* lu, const int n, int* perm, double* pbuf, const int k0, const int k1,
+                              int* piv_out) {
+    constexpr int LD = kLuPanel + 1;
+    const int lane = threadIdx.x;  // warp 0 only
+    const int K = k1 - k0, rows = n - k0;
+    for (int q = lane; q < rows * K; q += 32) {
+        const int r = q / K, c = q % K;
+        pbuf[r * LD + c] = lu[static_cast<int64_t>(k0 + r) * n + k0 + c];
+    }
+    __syncwarp();
+    for (int kk = 0; kk < K; ++kk) {
+        // dense_lu.cpp:32-41: largest magnitude in column k, ties to the lowest row
+        const double a0 = fabs(pbuf[kk * LD + kk]);
+        double bm = -1.0;
+        int bi = n;
+        if (isnan(a0)) {
+            bm = a0;  // every later comparison with NaN fails: pivot stays k
+            bi = kk;
+        } else {
+            for (int r = kk + lane; r < rows; r += 32) {
+                const double mag = fabs(pbuf[r * LD + kk]);
+                if (!isnan(mag)) lu_argmax_combine(bm, bi, mag, r);
+            }
+            for (int off = 16; off >= 1; off >>= 1) {
+                const double m2 = __shfl_xor_sync(0xffffffffu, bm, off);
+                const int i2 = __shfl_xor_sync(0xffffffffu, bi, off);
+                lu_argmax_combine(bm, bi, m2, i2);
+            }
+        }
+        if (bm == 0.0) return false;  // dense_lu.cpp:35
+        if (lane == 0) {
+            piv_out[kk] = k0 + bi;
+            const int t = perm[k0 + kk];
+            perm[k0 + kk] = perm[k0 + bi];
+            perm[k0 + bi] = t;
+        }
+        if (bi != kk && lane < K) {
+            const double t = pbuf[kk * LD + lane];
+            pbuf[kk * LD + lane] = pbuf[bi * LD + lane];
+            pbuf[bi * LD + lane] = t;
+        }
+        __syncwarp();
+        // l_rk = a_rk / pivot, then row r's rest of the panel, in registers
+        const double pv = pbuf[kk * LD + kk];
+        double u[kLuPanel];
+#pragma unroll
+        for (int c = 0; c < kLuPanel; ++c) u[c] = pbuf[kk * LD + c];
+        for (int r = kk + 1 + lane; r < rows; r += 32) {
+            double* row = pbuf + r * LD;
+            const double l = __ddiv_rn(row[kk], pv);
+            double a[kLuPanel];
+#pragma unroll
+            for (int c = 0; c < kLuPanel; ++c) a[c] = row[c];
+            row[kk] = l;
+#pragma unroll
+            for (int c = 0; c < kLuPanel; ++c)
+                if (c > kk && c < K) row[c] = __dsub_rn(a[c], __dmul_rn(l, u[c]));
+        }
+        __syncwarp();
+    }
+    for (int q = lane; q < rows * K; q += 32) {
+        const int r = q / K, c = q % K;
+        lu[static_cast<int64_t>(k0 + r) * n + k0 + c] = pbuf[r * LD + c];
+    }
+    return true;
+}
+
+__device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
     __shared__ double red_m[8];
     __shared__ int red_i[8];
     __shared__ int s_pivot, s_singular;
@@ -92,10 +165,32 @@ __device__ bool lu_factor(double* lu, const int n, int* perm) {
     if (tid == 0) s_singular = 0;
     __syncthreads();
 
+    __shared__ int s_piv[kLuPanel];
     for (int k0 = 0; k0 < n; k0 += kLuPanel) {
         const int k1 = min(n, k0 + kLuPanel);
+        if (pbuf) {
+            if (tid < 32) {
+                const bool ok = lu_panel_warp(lu, n, perm, pbuf, k0, k1, s_piv);
+                if (tid == 0 && !ok) s_singular = 1;
+            }
+            __syncthreads();
+            if (s_singular) return false;
+            // the panel's row swaps, in order, on the columns outside it
+            for (int c = tid; c < n; c += nt) {
+                if (c >= k0 && c < k1) continue;
+                for (int kk = 0; kk < k1 - k0; ++kk) {
+                    const int pr = s_piv[kk];
+                    if (pr != k0 + kk) {
+                        const double t = A(k0 + kk, c);
+                        A(k0 + kk, c) = A(pr, c);
+                        A(pr, c) = t;
+                    }
+                }
+            }
+            __syncthreads();
+        }
         // panel factorization: columns [k0, k1), rows [k0, n)
-        for (int k = k0; k < k1; ++k) {
+        for (int k = k0; k < (pbuf ? k0 : k1); ++k) {
             // dense_lu.cpp:32-41: largest magnitude in column k, ties to the lowest row
             const double a0 = fabs(A(k, k));
             double bm = -1.0;
@@ -225,19 +320,26 @@ __device__ void lu_forward(const double* lu, const int n, double* y) {
 // Backward substitution U x = y (dense_lu.cpp:58-62) in place on x[]: row ii
 // subtracts j = ii+1..n-1 in order.  later_neg: a -0 sum turns +0 before the
 // division (block-diagonal mode: the zero products of later blocks, see top).
+// The row sums form one dependent chain, so warp 0 alone runs it (lanes form
+// the products, lane 0 the ordered sum) with warp-level syncs only.
 __device__ void lu_backward(const double* lu, const int n, double* x, double* slots, const bool later_neg) {
-    const int tid = threadIdx.x, nt = blockDim.x;
-    for (int ii = n - 1; ii >= 0; --ii) {
-        for (int j = ii + 1 + tid; j < n; j += nt) slots[j] = __dmul_rn(lu[static_cast<int64_t>(ii) * n + j], x[j]);
-        __syncthreads();
-        if (tid == 0) {
-            double acc = x[ii];
-            for (int j = ii + 1; j < n; ++j) acc = __dsub_rn(acc, slots[j]);
-            if (later_neg && is_neg_zero(acc)) acc = 0.0;
-            x[ii] = __ddiv_rn(acc, lu[static_cast<int64_t>(ii) * n + ii]);
+    const int tid = threadIdx.x;
+    if (tid < 32) {
+        for (int ii = n - 1; ii >= 0; --ii) {
+            const double* row = lu + static_cast<int64_t>(ii) * n;
+            for (int j = ii + 1 + tid; j < n; j += 32) slots[j] = __dmul_rn(row[j], x[j]);
+            __syncwarp();
+            if (tid == 0) {
+                double acc = x[ii];
+#pragma unroll 8
+                for (int j = ii + 1; j < n; ++j) acc = __dsub_rn(acc, slots[j]);
+                if (later_neg && is_neg_zero(acc)) acc = 0.0;
+                x[ii] = __ddiv_rn(acc, row[ii]);
+            }
+            __syncwarp();
         }
-        __syncthreads();
     }
+    __syncthreads();
 }
 
 // Scatter cells [c0, c0 + cells) of the group into the zeroed dense matrix
@@ -256,14 +358,22 @@ __device__ void lu_densify(double* lu, const int ld, const double* vals, const i
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) lu_fallback_kernel(const LuParams p) {
+__global__ void __launch_bounds__(256, 3) lu_fallback_kernel(const LuParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const LuEntry ent = p.entries[blockIdx.x];
     const int s = p.species;
     const int n = ent.kc * s;
     double* lu = p.scratch + static_cast<size_t>(blockIdx.x) * p.stride;
-    int* perm = reinterpret_cast<int*>(smem_raw);
-    double* sum = reinterpret_cast<double*>(smem_raw + sizeof(int) * ((n + 1) & ~1));
+    // dynamic shared memory: [panel buffer] perm | sum | slots
+    double* pbuf = nullptr;
+    const int prow = p.mode == 0 && ent.kc > 1 ? s : n;
+    unsigned char* base = smem_raw;
+    if (p.panel_rows > 0) {
+        if (prow <= p.panel_rows) pbuf = reinterpret_cast<double*>(smem_raw);
+        base += sizeof(double) * p.panel_rows * (kLuPanel + 1);
+    }
+    int* perm = reinterpret_cast<int*>(base);
+    double* sum = reinterpret_cast<double*>(base + sizeof(int) * ((n + 1) & ~1));
     double* slots = sum + n;  // >= padded length (also used for products)
     const int tid = threadIdx.x, nt = blockDim.x;
     const double* vals = p.values + ent.cell0 * p.nnz;
@@ -287,7 +397,7 @@ __global__ void __launch_bounds__(256) lu_fallback_kernel(const LuParams p) {
                 for (int q = tid; q < s * s; q += nt)
                     if (is_neg_zero(blk[q])) blk[q] = 0.0;
             __syncthreads();
-            if (!lu_factor(blk, s, perm + c * s)) {
+            if (!lu_factor(blk, s, perm + c * s, pbuf)) {
                 if (tid == 0) p.status[blockIdx.x] = 1;
                 return;
             }
@@ -326,7 +436,7 @@ __global__ void __launch_bounds__(256) lu_fallback_kernel(const LuParams p) {
         }
     } else {
         lu_densify(lu, n, vals, p.row_ptr, p.col_idx, s, p.nnz, ent.kc);
-        if (!lu_factor(lu, n, perm)) {
+        if (!lu_factor(lu, n, perm, pbuf)) {
             if (tid == 0) p.status[blockIdx.x] = 1;
             return;
         }
