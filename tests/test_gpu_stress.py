@@ -53,3 +53,14 @@ def test_random_patterns_large(solver, seed):
             continue
         for algo in (Algo.BICGSTAB_JACOBI, Algo.BICG):
             check(solver, rp, ci, v, b, k, algo, 1e-12, 120)
+
+
+@pytest.mark.parametrize("species,k", [(1024, 1), (512, 2), (128, 8), (341, 3), (33, 31)])
+def test_largest_groups(solver, species, k):
+    """Groups of exactly (or just under) the 1024-row limit (exec_model.cpp:
+    k * s <= 1024): the four-warp TMEM teams' widest trees, both algorithms."""
+    rng = np.random.default_rng(species * 7 + k)
+    rp, ci, v, b = random_batch(rng, 2 * k + 1, species, 4.0 / species)
+    for algo in (Algo.BICGSTAB_JACOBI, Algo.BICG):
+        rep = check(solver, rp, ci, v, b, k, algo, 1e-12, 60)
+        assert len(rep.per_block_iterations) == 3
