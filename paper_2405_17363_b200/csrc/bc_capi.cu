@@ -121,7 +121,7 @@ struct bc_ctx {
     std::map<std::pair<int, int>, bc::GroupPlan> plans;  // (k, with_transpose)
     std::vector<DevBuf> plan_bufs;
     DevBuf values, rhs, x, giters, grms, gflags, counters, lu_scratch, lu_entries, lu_status,
-        f_scratch, lu_rms_scratch, t_values, t_work;
+        f_scratch, lu_rms_scratch, lu_chain, t_values, t_work;
     // device-resident simulation (bc_simulate)
     DevBuf sim_tabs, sim_sign, sim_rates, sim_y, sim_prev, sim_values, sim_rhs, sim_dx, sim_red;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -688,7 +688,8 @@ void upload_multi_tables(const bc::Pattern& pat, DevBuf* trp, DevBuf* trow, DevB
 // Coupled groups are factored block by block (mode 0); a group with a non-
 // finite input or result is rerun densely (mode 1), like one-cell groups.
 void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_values, const double* d_rhs,
-            double* d_x, double* g_rms, int s, int nnz, int block_width, cudaStream_t st, int mode = 0) {
+            double* d_x, double* g_rms, int s, int nnz, int block_width, cudaStream_t st, int mode = 0,
+            uint8_t* d_chain_flags = nullptr, int conv = 0, int flip = 0, int later_neg = 0) {
     int64_t nmax = 0, kmax = 0;
     for (const auto& e : ents) {
         nmax = std::max<int64_t>(nmax, static_cast<int64_t>(e.kc) * s);
@@ -739,6 +740,10 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
         lp.block_width = block_width;
         lp.mode = blockdiag ? 0 : 1;
         lp.panel_rows = panel_rows;
+        lp.conv = conv;
+        lp.flip = flip;
+        lp.later_neg = later_neg;
+        lp.chain_flags = d_chain_flags ? d_chain_flags + b0 : nullptr;
         bc::lu_fallback_kernel<<<cnt, 256, smem, st>>>(lp);
         check_cuda(cudaGetLastError(), "lu_fallback_kernel launch");
         ctx->launches++;
@@ -756,6 +761,37 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
     if (!dense.empty()) {
         if (!blockdiag) fail(BC_ERR_CUDA, "lu_fallback_kernel: unexpected status");
         run_lu(ctx, dense, d_values, d_rhs, d_x, g_rms, s, nnz, block_width, st, 1);
+    }
+}
+
+// The sign-of-zero chain (bc_lu.cuh, top) across the cells of one block-
+// diagonal system solved cell by cell: cells run with no flips first; the scan
+// redoes, in chain order, the few cells whose zeros an earlier (forward) or
+// later (backward) cell flips, with the flags of their redone runs.
+void lu_sign_chain(bc_ctx* ctx, int64_t cells, const double* d_values, const double* d_rhs, double* d_x, int s,
+                   int nnz, uint8_t* d_fl, cudaStream_t st) {
+    std::vector<uint8_t> fl(static_cast<size_t>(cells));
+    check_cuda(cudaMemcpyAsync(fl.data(), d_fl, fl.size(), cudaMemcpyDeviceToHost, st), "D2H lu chain");
+    check_cuda(cudaStreamSynchronize(st), "lu chain");
+    std::vector<uint8_t> conv(fl.size(), 0), flip(fl.size(), 0);
+    auto redo = [&](int64_t c, int later) {
+        const std::vector<bc::LuEntry> one{{c, 0, 1, 0}};
+        run_lu(ctx, one, d_values, d_rhs, d_x, nullptr, s, nnz, 0, st, 1, d_fl + c, conv[c], flip[c], later);
+        check_cuda(cudaMemcpyAsync(&fl[c], d_fl + c, 1, cudaMemcpyDeviceToHost, st), "D2H lu chain");
+        check_cuda(cudaStreamSynchronize(st), "lu chain");
+    };
+    bool neg_pivot = false, fwd = false;
+    for (int64_t c = 0; c < cells; ++c) {
+        conv[c] = neg_pivot && (fl[c] & bc::kChainNegZeroVal);
+        flip[c] = fwd && (fl[c] & bc::kChainNegZeroRhs);
+        if (conv[c] || flip[c]) redo(c, 0);
+        neg_pivot = neg_pivot || (fl[c] & bc::kChainNegPivot);
+        fwd = fwd || (fl[c] & bc::kChainFwd);
+    }
+    bool later = false;
+    for (int64_t c = cells - 1; c >= 0; --c) {
+        if (later && (fl[c] & bc::kChainNegZeroSum)) redo(c, 1);
+        later = later || (fl[c] & bc::kChainBwd);
     }
 }
 
@@ -872,7 +908,7 @@ void bc_ctx_destroy(bc_ctx* ctx) {
     cudaSetDevice(ctx->device);
     for (DevBuf* b : {&ctx->d_rp, &ctx->d_ci, &ctx->values, &ctx->rhs, &ctx->x, &ctx->giters,
                       &ctx->grms, &ctx->gflags, &ctx->counters, &ctx->lu_scratch,
-                      &ctx->lu_entries, &ctx->lu_status, &ctx->f_scratch, &ctx->lu_rms_scratch, &ctx->t_values,
+                      &ctx->lu_entries, &ctx->lu_status, &ctx->f_scratch, &ctx->lu_rms_scratch, &ctx->lu_chain, &ctx->t_values,
                       &ctx->t_work, &ctx->m_trp, &ctx->m_trow, &ctx->m_tval, &ctx->m_diag, &ctx->m_ranges,
                       &ctx->m_work, &ctx->m_part, &ctx->m_out, &ctx->sim_tabs, &ctx->sim_sign, &ctx->sim_rates,
                       &ctx->sim_y, &ctx->sim_prev, &ctx->sim_values, &ctx->sim_rhs, &ctx->sim_dx, &ctx->sim_red})
@@ -1168,13 +1204,19 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
             const int64_t ntot = prm->cells * s;
             if (multi && ntot > 2048) {
                 // Multi-cells breakdown on a large system: the block-diagonal
-                // LU factors cell by cell (the dense LU of strategies.cpp:47
-                // differs from it only in the sign of zeros), then the
-                // fallback residual goes through the global plan.
+                // LU runs cell by cell, and the host replays the chain of
+                // sign-of-zero rules the reference's dense LU (strategies.cpp:47)
+                // applies across cells (bc_lu.cuh), then the fallback residual
+                // goes through the global plan.
                 std::vector<bc::LuEntry> cells_e;
                 for (int64_t c = 0; c < prm->cells; ++c) cells_e.push_back({c, 0, 1, 0});
                 check_cuda(ctx->lu_rms_scratch.ensure(sizeof(double) * 8), "cudaMalloc");
-                run_lu(ctx, cells_e, d_values, d_rhs, d_x, nullptr, static_cast<int>(s), static_cast<int>(nnz), 0, st);
+                check_cuda(ctx->lu_chain.ensure(static_cast<size_t>(prm->cells)), "cudaMalloc(lu chain)");
+                uint8_t* d_fl = ctx->lu_chain.as<uint8_t>();
+                run_lu(ctx, cells_e, d_values, d_rhs, d_x, nullptr, static_cast<int>(s), static_cast<int>(nnz), 0, st,
+                       1, d_fl);
+                lu_sign_chain(ctx, prm->cells, d_values, d_rhs, d_x, static_cast<int>(s), static_cast<int>(nnz), d_fl,
+                              st);
                 const MultiResult mr = run_multi(ctx, pat, ctx->d_rp.as<int32_t>(), ctx->d_ci.as<int32_t>(), ctx->m_trp,
                                                  ctx->m_trow, ctx->m_tval, ctx->m_diag, prm->cells, multi_ranges,
                                                  d_values, d_rhs, nullptr, d_x, prm->tol, prm->max_iter, prm->algo,

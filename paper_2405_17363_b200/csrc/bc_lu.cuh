@@ -56,7 +56,19 @@ struct LuParams {
     int block_width;         // 0 = single interval
     int mode;                // 0 block-diagonal when k > 1, 1 dense
     int panel_rows;          // > 0: panels are factored in shared memory (rows <= panel_rows)
+    // dense mode, cells as links of a longer block-diagonal chain (Multi-cells
+    // systems too large to densify, solved cell by cell): the three sign-of-
+    // zero rules applied to this cell, and its flags for the host's chain scan
+    int conv, flip, later_neg;
+    uint8_t* chain_flags;    // per entry, or null: kChain* bits
 };
+
+constexpr uint8_t kChainNegPivot = 1;     // some pivot is negative
+constexpr uint8_t kChainNegZeroVal = 2;   // some matrix value is -0
+constexpr uint8_t kChainFwd = 4;          // some signbit(pivot_j) != signbit(y_j)
+constexpr uint8_t kChainNegZeroRhs = 8;   // some right-hand side entry is -0
+constexpr uint8_t kChainBwd = 16;         // some x has its sign bit set
+constexpr uint8_t kChainNegZeroSum = 32;  // some backward row summed to -0
 
 __device__ __forceinline__ void lu_argmax_combine(double& m, int& i, double m2, int i2) {
     // larger magnitude wins; equal magnitude -> lower row (strict > scan)
@@ -322,9 +334,11 @@ __device__ void lu_forward(const double* lu, const int n, double* y) {
 // division (block-diagonal mode: the zero products of later blocks, see top).
 // The row sums form one dependent chain, so warp 0 alone runs it (lanes form
 // the products, lane 0 the ordered sum) with warp-level syncs only.
-__device__ void lu_backward(const double* lu, const int n, double* x, double* slots, const bool later_neg) {
+__device__ bool lu_backward(const double* lu, const int n, double* x, double* slots, const bool later_neg) {
+    __shared__ int s_negzero_sum;
     const int tid = threadIdx.x;
     if (tid < 32) {
+        bool z = false;
         for (int ii = n - 1; ii >= 0; --ii) {
             const double* row = lu + static_cast<int64_t>(ii) * n;
             for (int j = ii + 1 + tid; j < n; j += 32) slots[j] = __dmul_rn(row[j], x[j]);
@@ -333,13 +347,18 @@ __device__ void lu_backward(const double* lu, const int n, double* x, double* sl
                 double acc = x[ii];
 #pragma unroll 8
                 for (int j = ii + 1; j < n; ++j) acc = __dsub_rn(acc, slots[j]);
-                if (later_neg && is_neg_zero(acc)) acc = 0.0;
+                if (is_neg_zero(acc)) {
+                    z = true;
+                    if (later_neg) acc = 0.0;
+                }
                 x[ii] = __ddiv_rn(acc, row[ii]);
             }
             __syncwarp();
         }
+        if (tid == 0) s_negzero_sum = z;
     }
     __syncthreads();
+    return s_negzero_sum != 0;
 }
 
 // Scatter cells [c0, c0 + cells) of the group into the zeroed dense matrix
@@ -436,13 +455,38 @@ __global__ void __launch_bounds__(256, 3) lu_fallback_kernel(const LuParams p) {
         }
     } else {
         lu_densify(lu, n, vals, p.row_ptr, p.col_idx, s, p.nnz, ent.kc);
+        int nzv = 0;
+        for (int64_t q = tid; q < static_cast<int64_t>(ent.kc) * p.nnz; q += nt) nzv |= is_neg_zero(vals[q]);
+        if (p.conv)
+            for (int64_t q = tid; q < static_cast<int64_t>(n) * n; q += nt)
+                if (is_neg_zero(lu[q])) lu[q] = 0.0;
+        __syncthreads();
         if (!lu_factor(lu, n, perm, pbuf)) {
             if (tid == 0) p.status[blockIdx.x] = 1;
             return;
         }
-        for (int i = tid; i < n; i += nt) sum[i] = b[perm[i]];
+        int nzb = 0;
+        for (int i = tid; i < n; i += nt) {
+            double v = b[perm[i]];
+            nzb |= is_neg_zero(v);
+            if (p.flip && is_neg_zero(v)) v = 0.0;
+            sum[i] = v;
+        }
         lu_forward(lu, n, sum);
-        lu_backward(lu, n, sum, slots, false);
+        int neg = 0, fwd = 0;
+        for (int i = tid; i < n; i += nt) {
+            const double u = lu[static_cast<int64_t>(i) * n + i];
+            neg |= signbit(u) ? 1 : 0;
+            fwd |= signbit(u) != signbit(sum[i]) ? 1 : 0;
+        }
+        __syncthreads();  // the flags above read y before the back substitution overwrites it
+        const bool z = lu_backward(lu, n, sum, slots, p.later_neg != 0);
+        int bwd = 0;
+        for (int i = tid; i < n; i += nt) bwd |= signbit(sum[i]) ? 1 : 0;
+        const uint8_t fl = (__syncthreads_or(neg) ? kChainNegPivot : 0) | (__syncthreads_or(nzv) ? kChainNegZeroVal : 0) |
+                           (__syncthreads_or(fwd) ? kChainFwd : 0) | (__syncthreads_or(nzb) ? kChainNegZeroRhs : 0) |
+                           (__syncthreads_or(bwd) ? kChainBwd : 0) | (z ? kChainNegZeroSum : 0);
+        if (p.chain_flags && tid == 0) p.chain_flags[blockIdx.x] = fl;
     }
     double* xo = p.x_out + ent.cell0 * s;
     for (int i = tid; i < n; i += nt) xo[i] = sum[i];

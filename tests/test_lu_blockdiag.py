@@ -18,9 +18,9 @@ import oracle_ffi as of
 from paper_2405_17363_b200 import Algo, BatchedSystem, DeviceSpec, Strategy, StrategyConfig
 
 
-def edge_case_batch(rng, species, cells, k, nonfinite=False):
+def edge_case_batch(rng, species, cells, k, nonfinite=False, density=0.45):
     n = species
-    dense = rng.random((n, n)) < 0.45
+    dense = rng.random((n, n)) < density
     np.fill_diagonal(dense, True)
     rows, cols = np.nonzero(dense)
     row_ptr = np.zeros(n + 1, np.int32)
@@ -115,3 +115,23 @@ def test_block_cells_n_breakdown_groups_m156(solver):
     np.testing.assert_array_equal(of.bits(rep.per_cell_x), of.bits(want.x))
     np.testing.assert_array_equal(of.bits(rep.per_block_residual_rms), of.bits(want.rms))
     np.testing.assert_array_equal(rep.per_block_flags, want.flags)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(2))
+def test_multi_cells_large_breakdown_sign_chain(solver, seed):
+    """Multi-cells over 300 cells (2,400 rows): one system too large to densify,
+    so the device solves it cell by cell and the host replays the cross-cell
+    sign-of-zero chain (bc_capi.cu lu_sign_chain).  Bitwise against the
+    oracle's dense 2400^2 LU (dense_lu.cpp), which differs from independent
+    per-cell LUs in the sign of zeros on these inputs."""
+    rng = np.random.default_rng(seed)
+    rp, ci, v, b = edge_case_batch(rng, 8, 300, 300, density=0.9)
+    st, want = of.orc_solve_batch(1, int(Algo.BICG), 0, rp, ci, v, b, 1e-30, 40, workers=8)
+    assert st == 0 and want.report.breakdown_fallbacks == 1
+    per_cell = np.stack([of.lu_solve("orc", rp, ci, v[c], b[c])[1] for c in range(300)])
+    assert (of.bits(per_cell) != of.bits(want.x)).any()  # the chain matters here
+    sysm = BatchedSystem(8, 300, rp, ci, v, b)
+    rep = solver.run_strategy(sysm, StrategyConfig(Strategy.MultiCells), DeviceSpec(), 1e-30, 40, 1, Algo.BICG)
+    np.testing.assert_array_equal(of.bits(rep.per_cell_x), of.bits(want.x))
+    assert of.bits(rep.max_residual_rms) == of.bits(want.report.max_residual_rms)
