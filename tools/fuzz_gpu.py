@@ -24,6 +24,18 @@ STRAT_ORC = {Strategy.OneCell: 0, Strategy.MultiCells: 1, Strategy.BlockCells: 2
 
 
 def case(rng):
+    if rng.random() < 0.25:  # breakdowns, signed zeros, negative pivots (tests/test_lu_blockdiag.py)
+        from test_lu_blockdiag import edge_case_batch
+        species = int(rng.integers(4, 40))
+        k = int(rng.integers(1, min(12, 1024 // species) + 1))
+        cells = int(rng.integers(1, 60))
+        kind = (Strategy.BlockCells, Strategy.OneCell, Strategy.MultiCells)[int(rng.integers(0, 3))]
+        # (not replayed: a non-finite value in a Multi-cells system too large to densify)
+        nonfinite = rng.random() < 0.1 and not (kind == Strategy.MultiCells and cells * species > 2048)
+        rp, ci, v, b = edge_case_batch(rng, species, cells, k, nonfinite=nonfinite,
+                                       density=float(rng.uniform(0.3, 0.9)))
+        return (f"edge{species}", rp, ci, v, b, kind, k if kind == Strategy.BlockCells else None,
+                Algo.BICG if rng.random() < 0.5 else Algo.BICGSTAB_JACOBI, 1e-30, int(rng.integers(5, 60)))
     if rng.random() < 0.5:
         species = int(rng.choice([16, 24, 40, 64, 100, 156, 200, 312]))
         m = Mechanism(species, 3 * species, int(rng.integers(0, 5)))
@@ -40,7 +52,7 @@ def case(rng):
     kmax = max(1, 1024 // species)
     kinds = [(Strategy.BlockCells, 1), (Strategy.BlockCells, None), (Strategy.OneCell, None),
              (Strategy.BlockCells, int(rng.integers(1, kmax + 1)))]
-    if cells * species <= 20000:
+    if cells * species <= 4000:  # a Multi-cells breakdown makes the oracle densify the whole system
         kinds.append((Strategy.MultiCells, None))
     if cells <= 2000:
         kinds.append((Strategy.ThreadPerCell, None))
