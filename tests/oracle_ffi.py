@@ -77,6 +77,9 @@ def ref() -> C.CDLL:
         lib.ref_bicg_solve.argtypes = [_i64, _p, _p, _p, _p, _p, _f64, _i64, _p, _i64, C.c_int, _p,
                                        C.POINTER(_i64), C.POINTER(_f64), C.POINTER(_i32), C.POINTER(_i32)]
         lib.ref_lu_solve.argtypes = [_i64, _p, _p, _p, _p, _p]
+        lib.ref_bicgstab_solve.argtypes = lib.ref_bicg_solve.argtypes
+        lib.ref_solve_batch_bicgstab.argtypes = [C.c_int, _i64, _i64, _i64, _p, _p, _p, _p, _f64, _i64, _i64, _i64,
+                                                 _p, _p, _p, _p, C.POINTER(RefReport)]
         lib.ref_tree_reduce.restype = _f64
         lib.ref_tree_reduce.argtypes = [_p, _i64, _i64]
         lib.ref_plan_reduce.restype = _f64
@@ -135,6 +138,42 @@ def ref_solve_batch(strategy, k, row_ptr, col_idx, values, rhs, tol, max_iter, m
     return st, BatchResult(x, it, None, None, rep)
 
 
+def ref_solve_batch_bicgstab(strategy, k, row_ptr, col_idx, values, rhs, tol, max_iter, mtpb=1024, workers=1,
+                             x=None):
+    """Jacobi-BiCGSTAB through the reference's own primitives and drivers
+    (oracle/ref_bicgstab.cpp): the checker of the north-star path.  Same
+    outputs as orc_solve_batch (x, per-group iterations / rms / flags)."""
+    species = len(row_ptr) - 1
+    cells = values.shape[0]
+    ng = orc().orc_group_count(strategy, cells, species, mtpb, k)
+    if ng < 0:
+        ng = 1
+    x = np.empty((cells, species)) if x is None else x
+    it = np.zeros(ng, np.int64)
+    rms = np.zeros(ng)
+    fl = np.zeros(ng, np.uint8)
+    rep = RefReport()
+    st = ref().ref_solve_batch_bicgstab(strategy, k, species, cells, ptr(np.ascontiguousarray(row_ptr, np.int32)),
+                                        ptr(np.ascontiguousarray(col_idx, np.int32)), ptr(np.ascontiguousarray(values)),
+                                        ptr(np.ascontiguousarray(rhs)), tol, max_iter, mtpb, workers, ptr(x), ptr(it),
+                                        ptr(rms), ptr(fl), C.byref(rep))
+    return st, BatchResult(x, it, rms, fl, rep)
+
+
+def ref_solve_checker(algo, strategy, k, row_ptr, col_idx, values, rhs, tol, max_iter, mtpb=1024, workers=1):
+    """The strongest checker available for `algo` (0 BiCG, 1 Jacobi-BiCGSTAB):
+    the compiled reference (BiCG: run_strategy; BiCGSTAB: its primitives
+    composed) when oracle/_ref exists, else the C restatement.  Returns
+    (status, BatchResult with x/iters/rms/flags, kind)."""
+    if have_ref():
+        if algo == 1:
+            st, r = ref_solve_batch_bicgstab(strategy, k, row_ptr, col_idx, values, rhs, tol, max_iter, mtpb,
+                                             workers)
+            return st, r, "reference primitives (oracle/_ref ref_solve_batch_bicgstab)"
+    st, r = orc_solve_batch(strategy, algo, k, row_ptr, col_idx, values, rhs, tol, max_iter, mtpb, workers)
+    return st, r, "C restatement (oracle/liborc)"
+
+
 def csr64(row_ptr, col_idx):
     return np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col_idx, np.int64)
 
@@ -163,6 +202,20 @@ def ref_bicg_single(row_ptr, col_idx, vals, b, x0, tol, max_iter, ranges=None, h
                               ptr(np.ascontiguousarray(x0 if x0 is not None else np.zeros(n), np.float64)), tol,
                               max_iter, ptr(ranges), len(ranges) // 2, int(host_stage), ptr(x), C.byref(it),
                               C.byref(rms), C.byref(cv), C.byref(bd))
+    return st, x, OrcOutcome(it.value, rms.value, cv.value, bd.value)
+
+
+def ref_bicgstab_single(row_ptr, col_idx, vals, b, x0, tol, max_iter, ranges=None, host_stage=False):
+    n = len(row_ptr) - 1
+    rp, ci = csr64(row_ptr, col_idx)
+    ranges = np.array([[0, n]] if ranges is None else ranges, np.int64).reshape(-1)
+    x = np.empty(n)
+    it, rms, cv, bd = _i64(), _f64(), _i32(), _i32()
+    st = ref().ref_bicgstab_solve(n, ptr(rp), ptr(ci), ptr(np.ascontiguousarray(vals, np.float64)),
+                                  ptr(np.ascontiguousarray(b, np.float64)),
+                                  ptr(np.ascontiguousarray(x0 if x0 is not None else np.zeros(n), np.float64)), tol,
+                                  max_iter, ptr(ranges), len(ranges) // 2, int(host_stage), ptr(x), C.byref(it),
+                                  C.byref(rms), C.byref(cv), C.byref(bd))
     return st, x, OrcOutcome(it.value, rms.value, cv.value, bd.value)
 
 

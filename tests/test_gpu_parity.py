@@ -101,21 +101,40 @@ def test_m156_bicgstab_bitwise_vs_oracle(solver, m156, m156_batches, regime, kin
     reg, v, b = m156_batches[regime]
     sysm = system_of(m156.row_ptr, m156.col_idx, v, b)
     rep = run_gpu(solver, sysm, kind, k, Algo.BICGSTAB_JACOBI, reg.tol, reg.max_iter)
-    st, res = of.orc_solve_batch(STRAT_ORC[kind], 1, 0 if k is None else k, m156.row_ptr, m156.col_idx, v, b,
+    kk = 0 if k is None else k
+    st, res = of.orc_solve_batch(STRAT_ORC[kind], 1, kk, m156.row_ptr, m156.col_idx, v, b,
                                  reg.tol, reg.max_iter, workers=8)
     assert st == 0
     assert_matches_oracle(rep, res, f"bicgstab {regime} {kind} {k}")
+    if of.have_ref():
+        # the same algorithm computed by the reference's own spmv / axpby /
+        # plan_reduce_map / lu_solve and strategy drivers (oracle/ref_bicgstab.cpp)
+        st, rres = of.ref_solve_batch_bicgstab(STRAT_ORC[kind], kk, m156.row_ptr, m156.col_idx, v, b, reg.tol,
+                                               reg.max_iter, workers=8)
+        assert st == 0
+        assert_matches_oracle(rep, rres, f"bicgstab {regime} {kind} {k} vs reference primitives")
     north_star_tolerances(rep, res)
     # Block-cells(k) groups up to 1024 rows run on the TMEM kernel (four-warp teams for the coupled ones)
     want = {Strategy.MultiCells: KERNEL_MULTI, Strategy.ThreadPerCell: KERNEL_THREAD}.get(kind, KERNEL_TMEM)
     assert rep.kernels & ~16 == want, (rep.kernels, want)  # the intended kernel ran (16 = LU fallback)
-    if regime == "C":
-        # converging regime: the solution agrees with the reference's dense LU
-        for c in range(0, 100, 17):
+    if regime == "C" and kind != Strategy.MultiCells:
+        # converging regime, north-star criterion: every converged cell within
+        # 1e-10 relative of the reference's dense LU (dense_lu.cpp:18-63).  A
+        # coupled group's convergence test is over the group's RMS, so one of
+        # its k cells may sit up to sqrt(k) above it (Block-cells(N), k = 6:
+        # worst 1.05e-10 on this batch, CPU-measured with the same bits)
+        x = np.asarray(rep.per_cell_x)
+        k_eff = 1 if kind in (Strategy.OneCell, Strategy.ThreadPerCell) else int(rep.cells_per_block)
+        flags = np.repeat(np.asarray(rep.per_block_flags), k_eff)[:100]
+        checked = 0
+        for c in range(100):
+            if not flags[c] & 1:
+                continue
             st, xl = of.lu_solve("ref" if of.have_ref() else "orc", m156.row_ptr, m156.col_idx, v[c], b[c])
             assert st == 0
-            x = np.asarray(rep.per_cell_x)[c]
-            assert np.abs(x - xl).max() / np.abs(xl).max() < 1e-6
+            assert np.abs(x[c] - xl).max() / np.abs(xl).max() <= 1e-10 * np.sqrt(k_eff), c
+            checked += 1
+        assert checked >= 50, checked
 
 
 def test_m312_block_cells(solver):

@@ -167,3 +167,85 @@ def test_oracle_lu_vs_reference():
         st2, x2 = of.lu_solve("orc", rp, ci, v[0], b[0])
         assert st1 == st2 == 0
         np.testing.assert_array_equal(of.bits(x1), of.bits(x2))
+
+
+# --- BiCGSTAB: the restatement against the reference's own primitives ------
+
+
+@needs_ref
+@pytest.mark.parametrize("seed", range(6))
+def test_bicgstab_restatement_bitwise_vs_reference_primitives(seed):
+    """orc_bicgstab_solve (bc_oracle.c) == the Jacobi-BiCGSTAB composed of the
+    reference's spmv / axpby / plan_reduce_map / lu_solve and its strategy
+    drivers (oracle/ref_bicgstab.cpp), for every strategy and plan."""
+    rng = np.random.default_rng(300 + seed)
+    cells = int(rng.integers(1, 30))
+    species = int(rng.integers(2, 50))
+    rp, ci, v, b = random_batch(rng, cells, species, float(rng.uniform(0.05, 0.5)))
+    kmax = max(1, 1024 // species)
+    for strategy, k in [(0, 0), (1, 0), (2, 0), (2, 1), (2, int(rng.integers(1, min(cells, kmax) + 1)))]:
+        for mtpb in (1024, 256):
+            if species > mtpb or (strategy == 2 and k * species > mtpb):
+                continue
+            for tol, mi in ((1e-12, 400), (1e-30, 60)):
+                st1, r1 = of.ref_solve_batch_bicgstab(strategy, k, rp, ci, v, b, tol, mi, mtpb=mtpb, workers=3)
+                st2, r2 = of.orc_solve_batch(strategy, 1, k, rp, ci, v, b, tol, mi, mtpb=mtpb)
+                assert st1 == st2 == 0
+                np.testing.assert_array_equal(of.bits(r1.x), of.bits(r2.x))
+                np.testing.assert_array_equal(r1.iters, r2.iters)
+                np.testing.assert_array_equal(of.bits(r1.rms), of.bits(r2.rms))
+                np.testing.assert_array_equal(r1.flags, r2.flags)
+                assert r1.report.breakdown_fallbacks == r2.report.breakdown_fallbacks
+                assert r1.report.iterations_sum == r2.report.iterations_sum
+
+
+@needs_ref
+def test_bicgstab_single_multi_block_plan_vs_reference_primitives():
+    rng = np.random.default_rng(17)
+    for n in (1, 5, 32, 100, 300):
+        rp, ci, v, b = random_batch(rng, 1, n, min(0.3, 6.0 / n))
+        x0 = rng.uniform(-1, 1, n)
+        bw = max(1, n // 3)
+        ranges = [[s, min(n, s + bw)] for s in range(0, n, bw)]
+        for tol in (1e-13, 1e-30):
+            st1, x1, o1 = of.ref_bicgstab_single(rp, ci, v[0], b[0], x0, tol, 200, ranges, True)
+            st2, x2, o2 = of.orc_solve_single(1, rp, ci, v[0], b[0], x0, tol, 200, ranges)
+            assert st1 == st2 == 0
+            np.testing.assert_array_equal(of.bits(x1), of.bits(x2))
+            assert (o1.iterations, o1.converged, o1.breakdown) == (o2.iterations, o2.converged, o2.breakdown)
+            assert of.bits(o1.final_residual_rms) == of.bits(o2.final_residual_rms)
+
+
+@needs_ref
+@pytest.mark.parametrize("h,tol", [(120.0, 1e-30), (1.0, 1e-10)])
+def test_bicgstab_restatement_vs_reference_primitives_m156(m156, h, tol):
+    """CB05-sized M156 cells in both regimes (P: 1000 iterations, breakdowns
+    included; C: converging), Block-cells(1) and Block-cells(N)."""
+    v, b = m156.newton_batch(0, 24, 100_000, h)
+    for k in (1, 0):
+        st1, r1 = of.ref_solve_batch_bicgstab(2, k, m156.row_ptr, m156.col_idx, v, b, tol, 1000, workers=8)
+        st2, r2 = of.orc_solve_batch(2, 1, k, m156.row_ptr, m156.col_idx, v, b, tol, 1000, workers=8)
+        assert st1 == st2 == 0
+        np.testing.assert_array_equal(of.bits(r1.x), of.bits(r2.x))
+        np.testing.assert_array_equal(r1.iters, r2.iters)
+        np.testing.assert_array_equal(of.bits(r1.rms), of.bits(r2.rms))
+        np.testing.assert_array_equal(r1.flags, r2.flags)
+
+
+@needs_ref
+def test_bicgstab_north_star_tolerance_vs_reference_lu(m156):
+    """North star: converged Jacobi-BiCGSTAB solutions within 1e-10 relative
+    of the reference's dense LU (dense_lu.cpp:18-63) on C-regime M156 cells."""
+    v, b = m156.newton_batch(0, 40, 40, 1.0)
+    st, r = of.ref_solve_batch_bicgstab(2, 1, m156.row_ptr, m156.col_idx, v, b, 1e-10, 1000, workers=8)
+    assert st == 0
+    ok = 0
+    for c in range(40):
+        if not (r.flags[c] & 1):
+            continue
+        st, xl = of.lu_solve("ref", m156.row_ptr, m156.col_idx, v[c], b[c])
+        assert st == 0
+        rel = np.abs(r.x[c] - xl).max() / np.abs(xl).max()
+        assert rel <= 1e-10, (c, rel)
+        ok += 1
+    assert ok >= 30
