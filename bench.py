@@ -14,13 +14,25 @@ collective on the data path (barrier + max-of-times only).
             stream, max over ranks, cells of all ranks / time
   e2e       through the public API (Solver.run_strategy) with pinned HOST
             inputs: H2D of values+rhs, solve, D2H of x + per-group outputs
-  roofline  dominant kernel (block_cells_kernel): algorithmic streaming bytes
-            (it*(16*nnz+80*n)+16*n+16 per cell) / its event time,
-            against MEASURED_PEAKS.json hbm_gbs
-  cpu_baseline  the reference's own solver (oracle/_ref, run_strategy
-            Block-cells(1), all host threads) on a bounded sample, rank 0, N=1
+  roofline  dominant kernel (block_cells_tmem_kernel): algorithmic streaming
+            bytes (it*(16*nnz+80*n)+16*n+16 per cell) / its event
+            time, against MEASURED_PEAKS.json hbm_gbs (the metric's label); the
+            binding resource (shared-memory pipe) from the planner's bank model,
+            measured in this run, next to the committed ncu capture
+  parity    the last timed step's output (every cell at N=1) against the
+            checker -- Jacobi-BiCGSTAB composed from the reference's own
+            compiled primitives (oracle/_ref), BiCG: the reference's
+            run_strategy -- bit for bit: x, per-group iterations, rms, flags
+  cpu_baseline  the same checker run is the reference's CPU path on all host
+            threads over the whole workload (rank 0, N=1), plus bounded
+            single-thread samples and the stock BiCG run_strategy
+  bicg_companion  the reference's own algorithm (BiCG) on the GPU, same
+            cells, for a like-for-like ratio against the stock reference
 
-  --impl reference   times the reference's CPU implementation only.
+  --impl reference   times the reference's CPU implementation only: the
+            whole workload every step through oracle/_ref (BiCGSTAB: composed
+            from the reference's primitives and strategy drivers; BiCG: its
+            stock run_strategy), inputs from the reference's own generator.
 """
 from __future__ import annotations
 
@@ -56,6 +68,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the bit-for-bit check of the last step")
+    ap.add_argument("--parity-cells", type=int, default=100_000,
+                    help="cells checked per run (all of them at N=1 up to this many; strided groups beyond)")
+    ap.add_argument("--no-companion", action="store_true", help="skip the GPU BiCG companion measurement")
     return ap.parse_args()
 
 
@@ -130,37 +146,43 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_reference_rate(values, rhs, row_ptr, col_idx, reg, budget_s, algo_name="bicg", threads=None):
-    """The reference's run_strategy (Block-cells(1), all host threads unless
-    `threads`) on a bounded prefix sample of the workload.  Returns (rate,
-    cores, sample, kind)."""
+def cpu_reference_rate(values, rhs, row_ptr, col_idx, reg, budget_s, algo_name="bicg", threads=None,
+                       cfg_code=(2, 1)):
+    """The reference's CPU path (oracle/_ref: BiCG = its stock run_strategy,
+    BiCGSTAB = composed from its primitives; the C restatement only where
+    oracle/_ref is absent) on a bounded prefix sample of the workload, all host
+    threads unless `threads`.  Returns (rate, cores, sample, kind)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_ffi as of
     cores = threads or os.cpu_count() or 1
-    use_ref = of.have_ref() and algo_name == "bicg"
+    algo = 0 if algo_name == "bicg" else 1
+    strat, k = cfg_code
+    use_ref = of.have_ref()
     kind = "reference" if use_ref else "port"
 
     def run(nc):
-        """Seconds of solver time: SolveReport::wall_time_ns for the reference
-        (the whole run_strategy call, strategies.cpp:241-247), wall clock for the port."""
+        """Seconds of solver time: SolveReport::wall_time_ns (the whole
+        run_strategy call, strategies.cpp:241-247) for oracle/_ref, wall clock
+        for the port."""
         if use_ref:
-            st, res = of.ref_solve_batch(2, 1, row_ptr, col_idx, values[:nc], rhs[:nc], reg.tol, reg.max_iter,
-                                         workers=cores)
+            rb = of.RefBatch(row_ptr, col_idx, values[:nc], rhs[:nc])
+            st, res = rb.run(algo, strat, k, reg.tol, reg.max_iter, workers=cores)
+            rb.close()
             assert st == 0, st
             return res.report.wall_time_ns / 1e9
-        else:
-            st, res = of.orc_solve_batch(2, 0 if algo_name == "bicg" else 1, 1, row_ptr, col_idx, values[:nc],
-                                         rhs[:nc], reg.tol, reg.max_iter, workers=cores)
-            assert st == 0, st
-            return None
+        t0 = time.perf_counter()
+        st, res = of.orc_solve_batch(strat, algo, k, row_ptr, col_idx, values[:nc], rhs[:nc], reg.tol, reg.max_iter,
+                                     workers=cores)
+        assert st == 0, st
+        return time.perf_counter() - t0
 
     probe = min(len(values), 4 * cores)
-    t0 = time.perf_counter()
-    dt = run(probe) or (time.perf_counter() - t0)
+    dt = run(probe)
     nc = int(min(len(values), max(probe, probe * budget_s / max(dt, 1e-3))))
-    t0 = time.perf_counter()
-    dt = run(nc) or (time.perf_counter() - t0)
-    solver = "reference run_strategy Block-cells(1) BiCG" if use_ref else f"oracle port {algo_name}"
+    dt = run(nc)
+    solver = (("reference run_strategy (BiCG)" if algo == 0 else
+               "Jacobi-BiCGSTAB composed from the reference's primitives") if use_ref
+              else f"C restatement {algo_name}")
     sample = f"{solver}, first {nc} cells of the workload, {cores} threads, {dt:.1f} s"
     return nc / dt, cores, sample, kind
 
@@ -200,31 +222,174 @@ def make_workload(cells, first, total, reg, species=SPECIES):
     return m, values, rhs
 
 
+def bench_config(args, n, nnz, cells, n_total, reg, world):
+    """The `config` both arms print (identical for the same flags)."""
+    algo_label = "Jacobi-BiCGSTAB" if args.algo == "bicgstab" else "BiCG"
+    return {
+        "workload": (f"M{n} ({n} species, {nnz} nnz) first Newton system of step 0, {cells} cells/GPU "
+                     f"({n_total} total), {args.strategy}, {algo_label}, "
+                     f"{reg.name} regime (h={reg.h:g} s, tol={reg.tol:g}, max_iter={reg.max_iter})"),
+        "cells_per_gpu": cells, "global_cells": n_total, "strategy": args.strategy,
+        "algorithm": args.algo, "regime": reg.name,
+        "l2": f"inputs larger than L2 ({cells * nnz * 8 / 1e9:.3f} GB values per GPU vs 126 MB L2)",
+        "parallelism": (f"replicas over {world} GPU(s) (Multi-cells is one global system)"
+                        if args.strategy == "multi-cells" and world > 1
+                        else f"cell-range sharding over {world} GPU(s), no collectives"),
+    }
+
+
+def ref_strategy(name):
+    """(strategy code, k) for oracle/_ref: 0 one-cell, 1 multi-cells, 2 block-cells (k 0 = N)."""
+    if name.startswith("block-cells-"):
+        k = name.rsplit("-", 1)[-1]
+        return 2, 0 if k == "N" else int(k)
+    return {"one-cell": (0, 0), "multi-cells": (1, 0), "thread-per-cell": (0, 0)}[name]
+
+
+def reference_inputs(species, first, count, total, h):
+    """The reference's own generator (mechanism.cpp / simulate.cpp:46-64 via
+    oracle/_ref ref_newton_batch), in host threads over cell ranges."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_ffi as of
+    lib = of.ref()
+    nnz = of._i64()
+    assert lib.ref_mechanism_pattern(species, 3 * species, SEED, of.C.byref(nnz), None, None) == 0
+    rp = np.zeros(species + 1, np.int32)
+    ci = np.zeros(nnz.value, np.int32)
+    assert lib.ref_mechanism_pattern(species, 3 * species, SEED, of.C.byref(nnz), of.ptr(rp), of.ptr(ci)) == 0
+    values = np.empty((count, nnz.value))
+    rhs = np.empty((count, species))
+    nt = max(1, min(os.cpu_count() or 1, 32))
+    bounds = [count * t // nt for t in range(nt + 1)]
+
+    def part(t):
+        a, b = bounds[t], bounds[t + 1]
+        if b > a:
+            st = lib.ref_newton_batch(species, 3 * species, SEED, first + a, b - a, total, 1, h,
+                                      of.ptr(values[a:b]), of.ptr(rhs[a:b]))
+            assert st == 0, st
+    ths = [threading.Thread(target=part, args=(t,)) for t in range(nt)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    return rp, ci, values, rhs
+
+
 def main_reference(args):
+    """The reference's CPU path on the box's host cores, the WHOLE workload
+    every step (rank 0 alone under torchrun): BiCGSTAB composed from the
+    reference's compiled spmv/axpby/plan_reduce_map/lu_solve and its strategy
+    drivers (oracle/ref_bicgstab.cpp), or for --algo bicg its stock
+    run_strategy.  The BatchedSystem is built once (the reference's host form),
+    so a step is exactly one solve; its time is the reference's own
+    SolveReport::wall_time_ns clock.  The stock BiCG run_strategy is timed once
+    beside it, so both algorithms have a reference number."""
+    import numpy as np
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_ffi as of
+    if not of.have_ref():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libbcref.so not built"}), flush=True)
+        return
     reg = regime(args.regime)
-    n_total = args.cells * args.gpus
-    m, values, rhs = make_workload(min(args.cells, 50_000), 0, n_total, reg, args.species)
-    budget = max(2.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
-    rates = []
+    n_total = args.cells * world
+    cells = args.cells
+    rp, ci, values, rhs = reference_inputs(args.species, 0, cells, n_total, reg.h)
+    nnz = int(rp[-1])
+    strat, k = ref_strategy(args.strategy)
+    cores = os.cpu_count() or 1
+    algo = 1 if args.algo == "bicgstab" else 0
+    rb = of.RefBatch(rp, ci, values, rhs)
+    x = np.empty((cells, args.species))
+    times = []
     for i in range(args.warmup + args.steps):
-        rate, cores, sample, kind = cpu_reference_rate(values, rhs, m.row_ptr, m.col_idx, reg, budget)
+        st, res = rb.run(algo, strat, k, reg.tol, reg.max_iter, workers=cores, x=x)
+        assert st == 0, st
         if i >= args.warmup:
-            rates.append(rate)
-    value = statistics.median(rates)
+            times.append(res.report.wall_time_ns / 1e9)
+    total_s = sum(times)
+    value = cells * args.steps / total_s
+    impl = ("Jacobi-BiCGSTAB composed from the reference's compiled spmv/axpby/plan_reduce_map/lu_solve and its "
+            "strategy drivers (oracle/_ref ref_bicgstab.cpp)" if algo == 1 else "the reference's stock run_strategy")
+    extra = None
+    if algo == 1:  # the reference's own algorithm, stock code path, once on the same cells
+        st, r0 = rb.run(0, strat, k, reg.tol, reg.max_iter, workers=cores, x=x)
+        assert st == 0, st
+        extra = {"value": cells / (r0.report.wall_time_ns / 1e9), "unit": UNIT, "cores": cores,
+                 "sample": f"stock run_strategy (BiCG) on all {cells} cells, one run, {cores} threads"}
+    rb.close()
     out = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * args.cells / value,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"M{args.species}, {args.cells} cells/GPU, Block-cells(1), {reg.name} regime; reference CPU "
-                               "solver (unpreconditioned BiCG, its only algorithm) on bounded samples",
-                   "algorithm": "bicg (reference)", "regime": reg.name},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+        "config": bench_config(args, args.species, nnz, cells, n_total, reg, world),
+        "reference_impl": impl,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"{impl}: all {cells} cells every step, {cores} threads, "
+                                   f"SolveReport::wall_time_ns"},
+        "reference_bicg": extra,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
+
+
+def parity_check(args, rep, m, h_values, h_rhs, reg, cfg_code, k, budget_cells, threads):
+    """Bit-for-bit check of one GPU solve against the checker on strided whole
+    groups (all of them when budget_cells >= cells).  Returns the parity dict
+    and, when every cell was checked, the checker's all-core timing."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_ffi as of
+    strat, kk = cfg_code
+    cells = h_values.shape[0]
+    x_gpu = rep.per_cell_x.cpu().numpy() if hasattr(rep.per_cell_x, "cpu") else np.asarray(rep.per_cell_x)
+    it_gpu = np.asarray(rep.per_block_iterations)
+    ng = len(it_gpu)
+    ksz = 1 if strat in (0,) else (k if strat == 2 else cells)
+    gsize = np.full(ng, ksz, np.int64)
+    gsize[-1] = cells - ksz * (ng - 1)
+    gfirst = np.concatenate([[0], np.cumsum(gsize)[:-1]])
+    stride = max(1, int(np.ceil(cells / max(1, budget_cells))))
+    groups = np.arange(0, ng, stride)
+    if stride > 1 and groups[-1] != ng - 1 and gsize[-1] != ksz:
+        groups = np.append(groups, ng - 1)  # the remainder group goes last, as in the whole batch
+    sel = np.concatenate([np.arange(gfirst[g], gfirst[g] + gsize[g]) for g in groups])
+    v = np.ascontiguousarray(h_values[sel])
+    b = np.ascontiguousarray(h_rhs[sel])
+    algo = 1 if args.algo == "bicgstab" else 0
+    t0 = time.perf_counter()
+    if of.have_ref():
+        rb = of.RefBatch(m.row_ptr, m.col_idx, v, b)
+        st, res = rb.run(algo, strat, kk, reg.tol, reg.max_iter, workers=threads)
+        rb.close()
+        checker = ("oracle/_ref: Jacobi-BiCGSTAB composed from the reference's primitives" if algo == 1
+                   else "oracle/_ref: the reference's run_strategy")
+        secs = res.report.wall_time_ns / 1e9
+    else:
+        st, res = of.orc_solve_batch(strat, algo, kk, m.row_ptr, m.col_idx, v, b, reg.tol, reg.max_iter,
+                                     workers=threads)
+        checker = "oracle/liborc: the C restatement"
+        secs = time.perf_counter() - t0
+    assert st == 0, st
+    xg = x_gpu[sel]
+    cell_bad = (xg.view(np.uint64) != res.x.view(np.uint64)).any(axis=1)
+    g_bad = it_gpu[groups] != res.iters
+    if res.rms is not None:
+        g_bad |= np.asarray(rep.per_block_residual_rms)[groups].view(np.uint64) != res.rms.view(np.uint64)
+        g_bad |= np.asarray(rep.per_block_flags)[groups] != res.flags
+    den = np.maximum(np.abs(res.x).max(axis=1), 1e-300)
+    rel = float((np.abs(xg - res.x).max(axis=1) / den).max())
+    out = {"cells_checked": int(len(sel)), "groups_checked": int(len(groups)), "of_cells": int(cells),
+           "mismatched_cells": int(cell_bad.sum()), "mismatched_groups": int(g_bad.sum()),
+           "max_rel_err_x": rel, "max_iteration_diff": int(np.abs(it_gpu[groups] - res.iters).max()),
+           "checker": checker, "checker_threads": threads, "checker_s": round(secs, 2),
+           "compared": "x bits per cell; per-group iterations" + (", rms bits, flags" if res.rms is not None else "")}
+    return out, (len(sel) / secs if len(sel) == cells else None), checker
 
 
 def main_b200(args):
@@ -259,13 +424,24 @@ def main_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared_gpu else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
     reg = regime(args.regime)
     algo = Algo.BICGSTAB_JACOBI if args.algo == "bicgstab" else Algo.BICG
     cfg = strategy_config(args.strategy)
     k = cfg.cells_per_block or (1024 // args.species if cfg.kind == Strategy.BlockCells else 1)
+    replicas = cfg.kind == Strategy.MultiCells  # one global system: replicas only (sharding.py)
     n_total = args.cells * world  # weak scaling: every rank solves args.cells cells of the global batch
-    first, cells = shard_range(n_total, k, rank, world)  # contiguous, group-aligned ranges, no collectives
-    m, h_values, h_rhs = make_workload(cells, first, n_total, reg, args.species)
+    if replicas:
+        first, cells = 0, args.cells
+    else:
+        first, cells = shard_range(n_total, k, rank, world)  # contiguous, group-aligned ranges, no collectives
+    m, h_values, h_rhs = make_workload(cells, first, args.cells if replicas else n_total, reg, args.species)
     nnz, n = m.nnz, m.species
 
     solver = Solver(local)
@@ -276,15 +452,15 @@ def main_b200(args):
     dsys = BatchedSystem(n, cells, m.row_ptr, m.col_idx, d_values, d_rhs)
     dev = DeviceSpec()
 
-    def step(timing=False):
-        return solver.run_strategy(dsys, cfg, dev, reg.tol, reg.max_iter, 1, algo, stream=stream.cuda_stream,
+    def step(timing=False, a=algo):
+        return solver.run_strategy(dsys, cfg, dev, reg.tol, reg.max_iter, 1, a, stream=stream.cuda_stream,
                                    timing=timing, x_out=d_x)
 
     for _ in range(args.warmup):
         rep = step()
     launches0 = solver.kernel_launches
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    kernel_ms, iters_total, reports = [], 0, []
+    kernel_ms, reports = [], []
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -299,6 +475,7 @@ def main_b200(args):
         t_wall = time.perf_counter() - t_wall
     barrier()
     launches = solver.kernel_launches - launches0
+    x_timed = d_x.cpu().numpy()  # the last timed step's solution, for the parity check below
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = max_over_ranks(sum(step_ms))
     value = n_total * args.steps / (total_ms / 1e3)
@@ -319,11 +496,20 @@ def main_b200(args):
     peak, peak_kind = measured_peak_hbm()
     compulsory = cells * (8 * nnz + 16 * n + 16)
     kname = dominant_kernel(rep.kernels)
+    clocks = clk.summary()
     tr = ncu_traffic()
-    if not tr or tr.get("kernel") != kname or tr.get("cells") != cells or tr.get("species", 156) != n:
+    if not tr or tr.get("kernel") != kname or tr.get("cells") != cells or tr.get("species", 156) != n \
+            or tr.get("algorithm", "bicgstab") != args.algo:
         tr = None  # the committed ncu capture is for another workload
     flops_per_it = (4 * nnz + 24 * n) if algo == Algo.BICGSTAB_JACOBI else (4 * nnz + 21 * n)
     fp64 = float(cell_iters.sum()) * flops_per_it / (kmean / 1e3) / 1e12
+    # the binding resource, from this run: the planner's bank-model wavefronts
+    # per group-iteration x the group-iterations / (SMs x SM clock x kernel time)
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    smem_model = None
+    if rep.model_spmv_wavefronts > 0 and clocks.get("sm_mhz"):
+        wf = rep.model_spmv_wavefronts * float(iters.sum())
+        smem_model = wf / (sms * clocks["sm_mhz"] * 1e6 * kmean / 1e3)
 
     # e2e through the public API with pinned host inputs
     e2e = None
@@ -348,49 +534,95 @@ def main_b200(args):
                "d2h_bytes_per_step": int(hx.nbytes + ng * (4 + 8 + 1)), "steps": e_steps,
                "ms_per_step": e_ms / e_steps}
 
-    cpu = None
+    # the reference's own algorithm on the GPU, same cells: a like-for-like
+    # companion to the stock reference's BiCG number
+    companion = None
+    if algo == Algo.BICGSTAB_JACOBI and not args.no_companion:
+        step(a=Algo.BICG)
+        c_steps = 3
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(c_steps):
+            rc = step(a=Algo.BICG)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        c_ms = max_over_ranks(e0.elapsed_time(e1))
+        companion = {"value": n_total * c_steps / (c_ms / 1e3), "unit": UNIT, "steps": c_steps,
+                     "ms_per_step": c_ms / c_steps, "algorithm": "bicg",
+                     "iterations_sum": int(sum_over_ranks(rc.iterations_sum))}
+        rep = reports[-1]
+
+    # parity: the last timed step's output against the checker, bit for bit
+    parity, cpu = None, None
+    if not args.no_parity:
+        rep.per_cell_x = x_timed
+        threads = max(1, (os.cpu_count() or 1) // (world if not shared_gpu else world))
+        budget = cells if world == 1 else max(1, args.parity_cells // world)
+        budget = min(budget, args.parity_cells)
+        parity, all_rate, checker = parity_check(args, rep, m, h_values, h_rhs, reg, ref_strategy(args.strategy),
+                                                 k, budget, threads)
+        for key in ("cells_checked", "mismatched_cells", "mismatched_groups", "groups_checked"):
+            parity[key] = int(sum_over_ranks(parity[key]))
+        parity["max_rel_err_x"] = max_over_ranks(parity["max_rel_err_x"])
+        if rank == 0 and world == 1 and all_rate:
+            cpu = {"value": all_rate, "unit": UNIT, "cores": threads,
+                   "kind": "reference" if "oracle/_ref" in checker else "port",
+                   "sample": f"{checker}: all {cells} cells of the workload (the parity run), {threads} threads"}
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, cores, sample, kind = cpu_reference_rate(h_values, h_rhs, m.row_ptr, m.col_idx, reg, args.cpu_seconds)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+        code = ref_strategy(args.strategy)
+        if cpu is None:
+            rate, cores, sample, kind = cpu_reference_rate(h_values, h_rhs, m.row_ptr, m.col_idx, reg,
+                                                           args.cpu_seconds, args.algo, cfg_code=code)
+            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
         # BASELINE.json configs[1]: the reference on one host thread as well
         rate1, _, sample1, kind1 = cpu_reference_rate(h_values, h_rhs, m.row_ptr, m.col_idx, reg,
-                                                      max(2.0, args.cpu_seconds / 3), threads=1)
+                                                      max(2.0, args.cpu_seconds / 3), args.algo, threads=1,
+                                                      cfg_code=code)
         cpu["single_thread"] = {"value": rate1, "unit": UNIT, "cores": 1, "kind": kind1, "sample": sample1}
+        if args.algo == "bicgstab":  # the reference's stock algorithm (BiCG run_strategy), all cores
+            rate_b, cores_b, sample_b, kind_b = cpu_reference_rate(h_values, h_rhs, m.row_ptr, m.col_idx, reg,
+                                                                   args.cpu_seconds, "bicg", cfg_code=code)
+            cpu["reference_bicg"] = {"value": rate_b, "unit": UNIT, "cores": cores_b, "kind": kind_b,
+                                     "sample": sample_b}
 
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {
-                "workload": (f"M{n} ({n} species, {nnz} nnz) first Newton system of step 0, {cells} cells/GPU "
-                             f"({n_total} total), {args.strategy}, {'Jacobi-BiCGSTAB' if algo else 'BiCG'}, "
-                             f"{reg.name} regime (h={reg.h:g} s, tol={reg.tol:g}, max_iter={reg.max_iter})"),
-                "cells_per_gpu": cells, "global_cells": n_total, "strategy": args.strategy,
-                "algorithm": args.algo, "regime": reg.name, "iterations_sum": int(merged["iterations_sum"]),
-                "breakdown_fallbacks": int(merged["breakdown_fallbacks"]),
-                "l2": f"inputs larger than L2 ({h_values.nbytes / 1e9:.3f} GB values per GPU vs 126 MB L2)",
-                "parallelism": f"cell-range sharding over {world} GPU(s), no collectives"
-                               + (f" ({world} ranks sharing {ngpu} GPU(s): a test of the N>1 path, not a"
-                                  " scaling number)" if shared_gpu else ""),
-            },
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "config": bench_config(args, n, nnz, cells, n_total, reg, world),
+            "solve": {"iterations_sum": int(merged["iterations_sum"]),
+                      "breakdown_fallbacks": int(merged["breakdown_fallbacks"]),
+                      "ranks_share_gpus": bool(shared_gpu)},
+            "roofline": {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": (tr or {}).get("dram_bytes_per_launch_scaled"),
                          "kernel": kname, "kernel_ms": kmean, "algorithmic_bytes": alg_bytes,
                          "peak_kind": peak_kind,
+                         "frac_is": "SURVEY.md 8d streaming-HBM bytes / HBM peak (the metric's label); the "
+                                    "kernel keeps the per-iteration bytes on chip, so the bound is the "
+                                    "shared-memory pipe (binding)",
                          "compulsory_bytes": compulsory,
                          "compulsory_frac": compulsory / (kmean / 1e3) / 1e9 / peak,
                          "fp64_tflops": fp64,
-                         # what actually binds the kernel (ncu --set full of the same workload, profiles/):
-                         # the per-iteration bytes never leave the SM, so HBM is not it
-                         "measured_bound": None if not tr else {
-                             "resource": "shared-memory pipe (LSU wavefronts)", "frac": tr.get("shared_pipe_frac"),
-                             "issue_active_frac": tr.get("issue_active_frac"),
-                             "fp64_pipe_frac": tr.get("fp64_pipe_frac"), "source": f"ncu tag {tr.get('tag')}"}},
+                         "binding": {
+                             "resource": "shared-memory LSU pipe (wavefronts)",
+                             "frac_model": smem_model,
+                             "model_wavefronts_per_group_iteration": rep.model_spmv_wavefronts,
+                             "frac_model_is": "planner bank-model SpMV wavefronts x group-iterations / "
+                                              "(SMs x measured SM clock x kernel time), this run",
+                             "frac_ncu": (tr or {}).get("shared_pipe_frac"),
+                             "issue_active_frac_ncu": (tr or {}).get("issue_active_frac"),
+                             "fp64_pipe_frac_ncu": (tr or {}).get("fp64_pipe_frac"),
+                             "ncu_source": f"profiles/ncu_block_cells_traffic.json tag {tr.get('tag')}" if tr else None}},
+            "parity": parity,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "bicg_companion": companion,
             "gpu_launches": int(launches),
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "wall_s_timed": t_wall,
         }
         print(json.dumps(out), flush=True)

@@ -101,6 +101,8 @@ typedef struct {
     int64_t kernel_launches;      /* kernels this call launched */
     int32_t kernels;              /* BC_KERNEL_* bits of the kernels this call launched */
     int32_t reserved;
+    double model_spmv_wavefronts; /* TMEM kernel: the planner's modelled shared-memory wavefronts of
+                                     one group-iteration's SpMVs (0 if it did not run) */
 } bc_report;
 
 enum {
@@ -127,6 +129,9 @@ const char* bc_last_error(const bc_ctx* ctx);
  * strategies.cpp:91-107): species rows, CSR with strictly increasing
  * columns per row.  nnz = row_ptr[species].  Builds the device schedules. */
 int bc_set_pattern(bc_ctx* ctx, int32_t species, const int32_t* row_ptr, const int32_t* col_idx);
+
+/* The installed pattern's species and nnz (info[0], info[1]). */
+int bc_ctx_pattern_info(const bc_ctx* ctx, int32_t* info);
 
 /* Group geometry of a solve (plan_kernel + solve_block_cells partition):
  * number of groups and the k used (fractional for Multi-cells). */
@@ -181,6 +186,34 @@ int bc_bicg_solve(bc_ctx* ctx, int32_t algo, int32_t n, const int32_t* row_ptr,
 
 /* Number of kernels launched since context creation (evidence counter). */
 int64_t bc_kernel_launches(const bc_ctx* ctx);
+
+/*
+ * Device set: the drop-in API over several GPUs of one box,
+ * the GPU counterpart of solve_block_cells' worker pool
+ * (strategies.cpp:221-247).  One bc_ctx and one stream per device (a device
+ * may be listed twice: two contexts on one GPU).  bc_devset_solve shards the
+ * batch into contiguous group-aligned cell ranges (the leftover group on the
+ * last shard), runs one host thread per device, and merges the report in
+ * group order as merge_groups (strategies.cpp:71-87) does: every output is
+ * bit-identical to bc_solve on one device.  No collective.  Multi-cells runs
+ * on the first device only (one global system).  With more than one device
+ * the arrays must be host memory (pageable or pinned).
+ */
+typedef struct bc_devset bc_devset;
+/* Pinned, portable, mapped host staging memory (cudaHostAlloc), for callers
+ * that pack into it: host inputs in pinned memory stream into the solve
+ * while it runs, and a pinned x_out is written by the kernels in place. */
+int bc_host_alloc(uint64_t bytes, void** out);
+void bc_host_free(void* p);
+
+int bc_devset_create(int n_devices, const int* devices, bc_devset** out);
+void bc_devset_destroy(bc_devset* set);
+int bc_devset_size(const bc_devset* set);
+const char* bc_devset_last_error(const bc_devset* set);
+int bc_devset_set_pattern(bc_devset* set, int32_t species, const int32_t* row_ptr, const int32_t* col_idx);
+int bc_devset_solve(bc_devset* set, const bc_solve_params* prm, const double* values, const double* rhs,
+                    double* x_out, int32_t* group_iters, double* group_rms, uint8_t* group_flags,
+                    bc_report* report);
 
 /*
  * Device Newton-system assembly (simulate.cpp:29-42 +

@@ -18,6 +18,7 @@ from .solver import (  # noqa: F401
     Algo,
     BatchedSystem,
     CudaError,
+    DeviceSet,
     DeviceSpec,
     InvalidGrouping,
     ReductionPlan,

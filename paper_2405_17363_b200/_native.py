@@ -32,6 +32,7 @@ class Report(C.Structure):
         ("n_groups", _i64), ("iterations_effective", _i64), ("iterations_sum", _i64),
         ("max_residual_rms", _f64), ("breakdown_fallbacks", _i64), ("cells_per_block", _f64),
         ("device_ms", _f64), ("kernel_launches", _i64), ("kernels", _i32), ("reserved", _i32),
+        ("model_spmv_wavefronts", _f64),
     ]
 
 
@@ -98,6 +99,18 @@ def b200() -> C.CDLL:
             _f64, _c_p, _c_p, _c_p, _c_p, _c_p]
         lib.bc_simulate.argtypes = [_c_p, C.POINTER(SimParams), C.POINTER(MechTables), _c_p, _c_p, _c_p,
                                     C.POINTER(_i64)]
+        lib.bc_ctx_pattern_info.argtypes = [_c_p, _c_p]
+        lib.bc_devset_create.argtypes = [C.c_int, _c_p, C.POINTER(_c_p)]
+        lib.bc_devset_destroy.argtypes = [_c_p]
+        lib.bc_devset_destroy.restype = None
+        lib.bc_devset_size.argtypes = [_c_p]
+        lib.bc_devset_last_error.argtypes = [_c_p]
+        lib.bc_devset_last_error.restype = C.c_char_p
+        lib.bc_devset_set_pattern.argtypes = [_c_p, _i32, _c_p, _c_p]
+        lib.bc_devset_solve.argtypes = lib.bc_solve.argtypes
+        lib.bc_host_alloc.argtypes = [_u64, C.POINTER(_c_p)]
+        lib.bc_host_free.argtypes = [_c_p]
+        lib.bc_host_free.restype = None
         _b200 = lib
     return _b200
 

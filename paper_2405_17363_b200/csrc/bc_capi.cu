@@ -132,6 +132,7 @@ struct bc_ctx {
     unsigned int* h_ones = nullptr;     // pinned source of the flag writes
     int64_t launches = 0;
     int32_t kernels = 0;  // BC_KERNEL_* bits since the last bc_solve started
+    double model_spmv_wf = 0.0;  // modelled shared wavefronts per group-iteration of the last TMEM launch
     std::map<BlockFn, bool> smem_set;
 };
 
@@ -547,6 +548,8 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
     check_cuda(cudaGetLastError(), "block_cells_tmem_kernel launch");
     ctx->launches++;
     ctx->kernels |= BC_KERNEL_TMEM;
+    // the planner's bank model: one pass per SpMV (BiCG's pair schedule does A p and A^T p~ in one)
+    ctx->model_spmv_wf = static_cast<double>(tp.tm.model_total) * (tp.tm.pair ? 1 : 2);
     return true;
 }
 
@@ -932,7 +935,13 @@ int bc_set_pattern(bc_ctx* ctx, int32_t species, const int32_t* row_ptr, const i
     if (!ctx) return BC_ERR_INVALID_ARGUMENT;
     return guarded(ctx, [&] {
         bc::Pattern p = make_pattern(species, row_ptr, col_idx);
-        for (auto& kv : ctx->plans) (void)kv;
+        // Same pattern as installed: keep its schedules.  The comparison is
+        // against the context's own state, so a pattern installed behind a
+        // caller's back (bc_simulate installs the mechanism's) is never reused
+        // by mistake.
+        if (ctx->has_pattern && p.species == ctx->pat.species && p.row_ptr == ctx->pat.row_ptr &&
+            p.col_idx == ctx->pat.col_idx)
+            return BC_OK;
         ctx->plans.clear();
         for (DevBuf& b : ctx->plan_bufs) b.release();
         ctx->plan_bufs.clear();
@@ -948,6 +957,14 @@ int bc_set_pattern(bc_ctx* ctx, int32_t species, const int32_t* row_ptr, const i
         ctx->has_pattern = true;
         return BC_OK;
     });
+}
+
+int bc_ctx_pattern_info(const bc_ctx* ctx, int32_t* info) {
+    if (!ctx || !info) return BC_ERR_INVALID_ARGUMENT;
+    if (!ctx->has_pattern) return BC_ERR_NO_PATTERN;
+    info[0] = ctx->pat.species;
+    info[1] = ctx->pat.nnz;
+    return BC_OK;
 }
 
 int bc_plan(int32_t species, const bc_solve_params* prm, int64_t* n_groups, double* cpb) {
@@ -1272,6 +1289,7 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
             report->breakdown_fallbacks = fallbacks;
             report->kernel_launches = ctx->launches - launches0;
             report->kernels = ctx->kernels;
+            report->model_spmv_wavefronts = (ctx->kernels & BC_KERNEL_TMEM) ? ctx->model_spmv_wf : 0.0;
             if (timing) {
                 float ms = 0.f;
                 check_cuda(cudaEventElapsedTime(&ms, ctx->e0, ctx->e1), "cudaEventElapsedTime");

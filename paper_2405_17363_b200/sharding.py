@@ -49,7 +49,10 @@ def merge_reports(local: Dict[str, float], group=None) -> Dict[str, float]:
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return out
     dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
-    mx = torch.tensor([float(local[k]) for k in REPORT_MAX], dtype=torch.float64, device=dev)
+    # merge_groups folds with std::max, which never picks up a NaN residual
+    # (NaN < x and x < NaN are both false): drop NaN before the MAX all-reduce
+    mx = torch.tensor([0.0 if local[k] != local[k] else float(local[k]) for k in REPORT_MAX], dtype=torch.float64,
+                      device=dev)
     sm = torch.tensor([int(local[k]) for k in REPORT_SUM], dtype=torch.int64, device=dev)
     dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
     dist.all_reduce(sm, op=dist.ReduceOp.SUM, group=group)

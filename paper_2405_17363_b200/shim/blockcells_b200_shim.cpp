@@ -32,6 +32,8 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "blockcells/dense_lu.hpp"
 #include "blockcells_b200.h"
@@ -58,7 +60,6 @@ b200::Algorithm env_algorithm() {
 // One context per (calling thread, device): contexts are not thread-safe.
 struct CtxHolder {
     bc_ctx* ctx = nullptr;
-    std::vector<int32_t> row_ptr, col_idx;  // last pattern handed to the GPU
     ~CtxHolder() {
         if (ctx) bc_ctx_destroy(ctx);
     }
@@ -74,6 +75,80 @@ bc_ctx* context() {
                                                   std::to_string(st) + ")");
     }
     return h.ctx;
+}
+
+// BLOCKCELLS_B200_DEVICES="0,1,...,7": the batched strategies run on a
+// device set (bc_devset_solve: contiguous group-aligned shards, one host
+// thread per GPU, merge in group order -- SURVEY.md §8e), so the reference's
+// own callers (run_simulation -> run_strategy, simulate.cpp:137-140) use every
+// listed GPU with no change.  Unset: one device (BLOCKCELLS_B200_DEVICE).
+struct SetHolder {
+    bc_devset* set = nullptr;
+    bool probed = false;
+    ~SetHolder() {
+        if (set) bc_devset_destroy(set);
+    }
+};
+
+bc_devset* device_set() {
+    thread_local SetHolder h;
+    if (!h.probed) {
+        h.probed = true;
+        const char* e = std::getenv("BLOCKCELLS_B200_DEVICES");
+        if (!e || !*e) return nullptr;
+        std::vector<int> devs;
+        std::string spec(e);
+        for (std::size_t pos = 0; pos <= spec.size();) {
+            const std::size_t next = std::min(spec.find(',', pos), spec.size());
+            if (next > pos) devs.push_back(std::atoi(spec.substr(pos, next - pos).c_str()));
+            pos = next + 1;
+        }
+        if (devs.empty()) return nullptr;
+        const int st = bc_devset_create(static_cast<int>(devs.size()), devs.data(), &h.set);
+        if (st != BC_OK)
+            throw std::runtime_error("blockcells_b200: cannot open the devices in BLOCKCELLS_B200_DEVICES (status " +
+                                     std::to_string(st) + ")");
+    }
+    return h.set;
+}
+
+// Pinned staging for the C ABI's flat arrays, reused across calls (grown on
+// demand): pinned inputs stream into the solve while it runs and the kernels
+// write x into pinned memory in place.
+struct Staging {
+    void* p = nullptr;
+    std::size_t bytes = 0;
+    ~Staging() { bc_host_free(p); }
+    double* get(std::size_t want) {
+        if (want > bytes) {
+            bc_host_free(p);
+            p = nullptr;
+            bytes = 0;
+            if (bc_host_alloc(want, &p) != BC_OK) throw std::bad_alloc();
+            bytes = want;
+        }
+        return static_cast<double*>(p);
+    }
+};
+
+// Host threads for packing / unpacking / checking (the results do not depend
+// on them, as the reference's do not depend on worker_count).
+std::size_t host_threads(std::size_t worker_count) {
+    const std::size_t hw = std::max(1u, std::thread::hardware_concurrency());
+    return worker_count == 0 ? hw : std::max(worker_count, std::min<std::size_t>(hw, 8));
+}
+
+template <class F>
+void parallel_for(std::size_t n, std::size_t threads, F&& f) {
+    threads = std::max<std::size_t>(1, std::min(threads, n / 256 + 1));
+    if (threads == 1) {
+        f(0, n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (std::size_t t = 0; t < threads; ++t)
+        pool.emplace_back([&, t] { f(n * t / threads, n * (t + 1) / threads); });
+    for (std::thread& th : pool) th.join();
 }
 
 [[noreturn]] void raise_status(int st, const char* msg) {
@@ -92,29 +167,65 @@ void check(bc_ctx* ctx, int st) {
     if (st != BC_OK) raise_status(st, bc_last_error(ctx));
 }
 
-void set_pattern(bc_ctx* ctx, const CsrMatrix& m) {
-    thread_local std::vector<int32_t> rp, ci;
-    std::vector<int32_t> nrp(m.row_ptr.begin(), m.row_ptr.end()), nci(m.col_idx.begin(), m.col_idx.end());
-    if (nrp == rp && nci == ci) return;
-    check(ctx, bc_set_pattern(ctx, static_cast<int32_t>(m.n_rows), nrp.data(), nci.data()));
-    rp.swap(nrp);
-    ci.swap(nci);
+// BatchedSystem::check (strategies.cpp:91-107) over host threads: each
+// thread finds the first bad cell of its range; the lowest one is reported,
+// so the exception is the one the sequential loop throws.
+void check_system(const BatchedSystem& system, std::size_t threads) {
+    if (system.cells == 0) throw std::invalid_argument("batched system: no cells");
+    if (system.species == 0) throw std::invalid_argument("batched system: no species");
+    if (system.per_cell_matrices.size() != system.cells || system.per_cell_rhs.size() != system.cells)
+        throw std::invalid_argument("batched system: per-cell arrays mismatch");
+    const CsrMatrix& first = system.per_cell_matrices.front();
+    const std::size_t n = system.cells, none = n;
+    const std::size_t nt = std::max<std::size_t>(1, std::min(threads, n / 256 + 1));
+    std::vector<std::size_t> bad_m(nt, none), bad_b(nt, none);
+    std::vector<int> why(nt, 0);
+    std::vector<std::thread> pool;
+    for (std::size_t t = 0; t < nt; ++t)
+        pool.emplace_back([&, t] {
+            for (std::size_t c = n * t / nt; c < n * (t + 1) / nt; ++c) {
+                const CsrMatrix& m = system.per_cell_matrices[c];
+                if (m.n_rows != system.species || m.n_cols != system.species) {
+                    bad_m[t] = c, why[t] = 1;
+                    break;
+                }
+                if (m.row_ptr != first.row_ptr || m.col_idx != first.col_idx) {
+                    bad_m[t] = c, why[t] = 2;
+                    break;
+                }
+            }
+            for (std::size_t c = n * t / nt; c < n * (t + 1) / nt; ++c)
+                if (system.per_cell_rhs[c].size() != system.species) {
+                    bad_b[t] = c;
+                    break;
+                }
+        });
+    for (std::thread& th : pool) th.join();
+    for (std::size_t t = 0; t < nt; ++t)
+        if (bad_m[t] != none)
+            throw std::invalid_argument(why[t] == 1 ? "batched system: cell matrix dimension"
+                                                    : "batched system: cells do not share one sparsity pattern");
+    for (std::size_t t = 0; t < nt; ++t)
+        if (bad_b[t] != none) throw std::invalid_argument("batched system: rhs dimension");
 }
 
 SolveReport run_gpu(const BatchedSystem& system, int strategy, std::optional<std::size_t> k,
-                    const DeviceSpec& device, double tol, std::size_t max_iter, Strategy kind) {
-    system.check();  // strategies.cpp:91-107
+                    const DeviceSpec& device, double tol, std::size_t max_iter, Strategy kind,
+                    std::size_t worker_count = 1) {
+    const std::size_t threads = host_threads(worker_count);
+    check_system(system, threads);  // strategies.cpp:91-107
     const auto start = Clock::now();
-    bc_ctx* ctx = context();
+    bc_devset* set = device_set();
+    bc_ctx* ctx = set ? nullptr : context();
     const CsrMatrix& first = system.per_cell_matrices.front();
-    set_pattern(ctx, first);
-    const std::size_t s = system.species, cells = system.cells, nnz = first.nnz();
-    // pack BatchedSystem -> the C ABI's cell-major arrays
-    std::vector<double> values(cells * nnz), rhs(cells * s), x(cells * s);
-    for (std::size_t c = 0; c < cells; ++c) {
-        std::memcpy(values.data() + c * nnz, system.per_cell_matrices[c].values.data(), sizeof(double) * nnz);
-        std::memcpy(rhs.data() + c * s, system.per_cell_rhs[c].data(), sizeof(double) * s);
+    {
+        const std::vector<int32_t> rp(first.row_ptr.begin(), first.row_ptr.end()),
+            ci(first.col_idx.begin(), first.col_idx.end());
+        const int st = set ? bc_devset_set_pattern(set, static_cast<int32_t>(system.species), rp.data(), ci.data())
+                           : bc_set_pattern(ctx, static_cast<int32_t>(system.species), rp.data(), ci.data());
+        if (st != BC_OK) raise_status(st, set ? bc_devset_last_error(set) : bc_last_error(ctx));
     }
+    const std::size_t s = system.species, cells = system.cells, nnz = first.nnz();
     bc_solve_params prm{};
     prm.strategy = strategy;
     prm.algo = env_algorithm() == b200::Algorithm::BiCG ? BC_ALGO_BICG : BC_ALGO_BICGSTAB_JACOBI;
@@ -129,10 +240,28 @@ SolveReport run_gpu(const BatchedSystem& system, int strategy, std::optional<std
     device.check();
     int64_t n_groups = 0;
     double cpb = 0;
-    check(ctx, bc_plan(static_cast<int32_t>(s), &prm, &n_groups, &cpb));
+    {
+        const int st = bc_plan(static_cast<int32_t>(s), &prm, &n_groups, &cpb);
+        if (st != BC_OK) raise_status(st, set ? bc_devset_last_error(set) : bc_last_error(ctx));
+    }
+    // pack BatchedSystem -> the C ABI's cell-major arrays, in pinned staging
+    thread_local Staging st_values, st_rhs, st_x;
+    double* values = st_values.get(sizeof(double) * cells * nnz);
+    double* rhs = st_rhs.get(sizeof(double) * cells * s);
+    double* x = st_x.get(sizeof(double) * cells * s);
+    parallel_for(cells, threads, [&](std::size_t c0, std::size_t c1) {
+        for (std::size_t c = c0; c < c1; ++c) {
+            std::memcpy(values + c * nnz, system.per_cell_matrices[c].values.data(), sizeof(double) * nnz);
+            std::memcpy(rhs + c * s, system.per_cell_rhs[c].data(), sizeof(double) * s);
+        }
+    });
     std::vector<int32_t> iters(n_groups);
     bc_report rep{};
-    check(ctx, bc_solve(ctx, &prm, values.data(), rhs.data(), x.data(), iters.data(), nullptr, nullptr, &rep));
+    {
+        const int st = set ? bc_devset_solve(set, &prm, values, rhs, x, iters.data(), nullptr, nullptr, &rep)
+                           : bc_solve(ctx, &prm, values, rhs, x, iters.data(), nullptr, nullptr, &rep);
+        if (st != BC_OK) raise_status(st, set ? bc_devset_last_error(set) : bc_last_error(ctx));
+    }
 
     SolveReport report;  // merge_groups, strategies.cpp:71-87
     report.strategy = kind;
@@ -142,8 +271,10 @@ SolveReport run_gpu(const BatchedSystem& system, int strategy, std::optional<std
     report.iterations_effective = static_cast<std::size_t>(rep.iterations_effective);
     report.max_residual_rms = rep.max_residual_rms;
     report.breakdown_fallbacks = static_cast<std::size_t>(rep.breakdown_fallbacks);
-    report.per_cell_x.reserve(cells);
-    for (std::size_t c = 0; c < cells; ++c) report.per_cell_x.emplace_back(x.begin() + c * s, x.begin() + (c + 1) * s);
+    report.per_cell_x.resize(cells);
+    parallel_for(cells, threads, [&](std::size_t c0, std::size_t c1) {
+        for (std::size_t c = c0; c < c1; ++c) report.per_cell_x[c].assign(x + c * s, x + (c + 1) * s);
+    });
     report.wall_time_ns = elapsed_ns(start);
     return report;
 }
@@ -355,6 +486,14 @@ SolveReport solve_one_cell(const BatchedSystem& system, double tol, std::size_t 
     return run_gpu(system, BC_STRATEGY_ONE_CELL, std::nullopt, device, tol, max_iter, Strategy::OneCell);
 }
 
+namespace {
+// run_strategy's worker_count reaches the packing threads of One-cell too
+SolveReport solve_one_cell_workers(const BatchedSystem& system, double tol, std::size_t max_iter,
+                                   const DeviceSpec& device, std::size_t workers) {
+    return run_gpu(system, BC_STRATEGY_ONE_CELL, std::nullopt, device, tol, max_iter, Strategy::OneCell, workers);
+}
+}  // namespace
+
 SolveReport solve_multi_cells(const BatchedSystem& system, const DeviceSpec& device, double tol,
                               std::size_t max_iter) {
     return run_gpu(system, BC_STRATEGY_MULTI_CELLS, std::nullopt, device, tol, max_iter, Strategy::MultiCells);
@@ -362,14 +501,15 @@ SolveReport solve_multi_cells(const BatchedSystem& system, const DeviceSpec& dev
 
 SolveReport solve_block_cells(const BatchedSystem& system, std::optional<std::size_t> cells_per_block,
                               const DeviceSpec& device, double tol, std::size_t max_iter,
-                              std::size_t /*worker_count*/) {
-    return run_gpu(system, BC_STRATEGY_BLOCK_CELLS, cells_per_block, device, tol, max_iter, Strategy::BlockCells);
+                              std::size_t worker_count) {
+    return run_gpu(system, BC_STRATEGY_BLOCK_CELLS, cells_per_block, device, tol, max_iter, Strategy::BlockCells,
+                   worker_count);
 }
 
 SolveReport run_strategy(const BatchedSystem& system, const StrategyConfig& config, const DeviceSpec& device,
                          double tol, std::size_t max_iter, std::size_t worker_count) {
     switch (config.kind) {
-        case Strategy::OneCell: return solve_one_cell(system, tol, max_iter, device);
+        case Strategy::OneCell: return solve_one_cell_workers(system, tol, max_iter, device, worker_count);
         case Strategy::MultiCells: return solve_multi_cells(system, device, tol, max_iter);
         case Strategy::BlockCells:
             return solve_block_cells(system, config.cells_per_block, device, tol, max_iter, worker_count);

@@ -65,6 +65,16 @@ class DeviceSpec:
     shared_mem_per_sm: int = 96 * 1024
     shared_slot_bytes: int = 8
 
+    def check(self) -> None:
+        """DeviceSpec::check (exec_model.hpp:40-42): every limit positive and
+        max_threads_per_block <= max_threads_per_sm, std::invalid_argument there."""
+        for f in ("max_threads_per_block", "warp_size", "max_warps_per_sm", "max_blocks_per_sm",
+                  "max_threads_per_sm", "shared_mem_per_sm", "shared_slot_bytes"):
+            if int(getattr(self, f)) <= 0:
+                raise ValueError(f"device spec: {f} must be positive")
+        if self.max_threads_per_block > self.max_threads_per_sm:
+            raise ValueError("device spec: max_threads_per_block exceeds max_threads_per_sm")
+
 
 @dataclass
 class StrategyConfig:
@@ -95,6 +105,11 @@ class BatchedSystem:
             raise ValueError("batched system: no species")
         if tuple(_shape(self.values)) != (self.cells, self.nnz) or tuple(_shape(self.rhs)) != (self.cells, self.species):
             raise ValueError("batched system: per-cell arrays mismatch")
+        _check_f64(self.values, "values")
+        _check_f64(self.rhs, "rhs")
+        if _is_torch_cuda(self.values) != _is_torch_cuda(self.rhs) or (
+                _is_torch_cuda(self.values) and self.values.device != self.rhs.device):
+            raise ValueError("batched system: values and rhs must live on the same device")
 
 
 @dataclass
@@ -114,6 +129,7 @@ class SolveReport:
     device_ms: float = 0.0
     kernel_launches: int = 0
     kernels: int = 0                     # KERNEL_* bits of the kernels launched
+    model_spmv_wavefronts: float = 0.0   # planner's modelled shared wavefronts per group-iteration (TMEM kernel)
 
 
 # bc_report.kernels bits (include/blockcells_b200.h)
@@ -147,6 +163,29 @@ def _shape(a):
 
 def _is_torch_cuda(a) -> bool:
     return hasattr(a, "is_cuda") and bool(a.is_cuda)
+
+
+def _check_f64(a, name: str) -> None:
+    """The C ABI reads 8 bytes per element: anything but float64 would be
+    read past its end."""
+    dt = getattr(a, "dtype", None)
+    if hasattr(a, "data_ptr"):  # torch tensor
+        import torch
+        ok = dt == torch.float64
+    else:
+        ok = dt == np.float64
+    if not ok:
+        raise ValueError(f"{name} must be float64 (got {dt})")
+
+
+def _check_out(x, shape, like, name: str, device: int) -> None:
+    """A caller-supplied output: exact shape, float64, contiguous, and on
+    the solver's GPU when it is a CUDA tensor."""
+    if tuple(_shape(x)) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)} (got {tuple(_shape(x))})")
+    _check_f64(x, name)
+    if _is_torch_cuda(x) and device >= 0 and x.device.index != device:
+        raise ValueError(f"{name} is on {x.device}, the solver runs on cuda:{device}")
 
 
 def _ptr(a):
@@ -188,7 +227,6 @@ class Solver:
         if st != 0:
             raise CudaError(f"bc_ctx_create(device={device}) failed with status {st}")
         self.device = device
-        self._pattern_key = None
 
     def close(self) -> None:
         if self._ctx:
@@ -206,15 +244,17 @@ class Solver:
         return int(_native.b200().bc_kernel_launches(self._ctx))
 
     def set_pattern(self, species: int, row_ptr: np.ndarray, col_idx: np.ndarray) -> None:
+        """bc_set_pattern keeps the context's schedules when the pattern is the
+        one already installed (it compares against its own state, so nothing
+        is cached here that bc_simulate could make stale)."""
         rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
         ci = np.ascontiguousarray(col_idx, dtype=np.int32)
-        key = (int(species), rp.tobytes(), ci.tobytes())
-        if key == self._pattern_key:
-            return
+        if rp.ndim != 1 or rp.shape[0] != int(species) + 1 or ci.ndim != 1 or ci.shape[0] < int(rp[-1]):
+            raise ValueError("csr: row_ptr/col_idx shape does not match species")
         _raise(self._ctx, _native.b200().bc_set_pattern(self._ctx, int(species), _ptr(rp), _ptr(ci)))
-        self._pattern_key = key
 
     def group_count(self, system: BatchedSystem, config: StrategyConfig, device: DeviceSpec = DeviceSpec()) -> Tuple[int, float]:
+        device.check()
         self.set_pattern(system.species, system.row_ptr, system.col_idx)
         prm = self._params(system, config, Algo.BICG, device, 1.0, 1, None, False)
         ng, cpb = C.c_int64(), C.c_double()
@@ -247,8 +287,13 @@ class Solver:
         """strategies.cpp:251-264.  worker_count is accepted for API parity; the
         GPU result is independent of it, as the reference's is."""
         system.check()
+        device.check()
         if max_iter < 1:
             raise ValueError("bicg: max_iter must be >= 1")
+        if _is_torch_cuda(system.values) and system.values.device.index != self.device:
+            raise ValueError(f"batched system is on {system.values.device}, the solver runs on cuda:{self.device}")
+        if x_out is not None:
+            _check_out(x_out, (system.cells, system.species), system.values, "x_out", self.device)
         self.set_pattern(system.species, system.row_ptr, system.col_idx)
         prm = self._params(system, config, algo, device, tol, max_iter, stream, timing)
         lib = _native.b200()
@@ -277,7 +322,8 @@ class Solver:
             per_block_iterations=iters.astype(np.int64), max_residual_rms=float(rep.max_residual_rms),
             wall_time_ns=int(wall), breakdown_fallbacks=int(rep.breakdown_fallbacks), per_cell_x=x_out,
             per_block_residual_rms=rms, per_block_flags=flags, device_ms=float(rep.device_ms),
-            kernel_launches=int(rep.kernel_launches), kernels=int(rep.kernels))
+            kernel_launches=int(rep.kernel_launches), kernels=int(rep.kernels),
+            model_spmv_wavefronts=float(rep.model_spmv_wavefronts))
 
     # strategies.hpp:60-77
     def solve_one_cell(self, system, tol, max_iter, device: DeviceSpec = DeviceSpec(), algo=Algo.BICG, **kw):
@@ -309,6 +355,79 @@ class Solver:
         _raise(self._ctx, st)
         return SolveOutcome(x, int(out.iterations), float(out.final_residual_rms), bool(out.converged),
                             bool(out.breakdown))
+
+
+class DeviceSet:
+    """The drop-in API over several GPUs of one box (bc_devset, SURVEY.md
+    §8e): contiguous group-aligned shards, one host thread per GPU, report
+    merged in group order -- bit-identical to one Solver.  A device may be
+    listed twice (two contexts on one GPU).  Arrays: host memory (numpy;
+    pinned buffers stream into the solve)."""
+
+    def __init__(self, devices):
+        lib = _native.b200()
+        devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+        self._set = C.c_void_p()
+        st = lib.bc_devset_create(len(devices), devs, C.byref(self._set))
+        if st != 0:
+            raise CudaError(f"bc_devset_create({list(devices)}) failed with status {st}")
+        self.devices = list(devices)
+
+    def close(self) -> None:
+        if self._set:
+            _native.b200().bc_devset_destroy(self._set)
+            self._set = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _raise(self, code):
+        if code == 0:
+            return
+        msg = _native.b200().bc_devset_last_error(self._set).decode()
+        exc = {-2: InvalidGrouping, -3: UnsupportedMechanism, -4: SingularMatrix, -1: ValueError,
+               -6: ValueError, -7: MemoryError}.get(code)
+        raise (exc or CudaError)(msg if exc else f"{msg} (status {code})")
+
+    def run_strategy(self, system: BatchedSystem, config: StrategyConfig, device: DeviceSpec = DeviceSpec(),
+                     tol: float = 1e-30, max_iter: int = 1000, worker_count: int = 1,
+                     algo: Algo = Algo.BICG, timing: bool = False, x_out=None) -> SolveReport:
+        system.check()
+        device.check()
+        if max_iter < 1:
+            raise ValueError("bicg: max_iter must be >= 1")
+        if x_out is None:
+            x_out = np.empty((system.cells, system.species), dtype=np.float64)
+        else:
+            _check_out(x_out, (system.cells, system.species), system.values, "x_out", -1)
+        lib = _native.b200()
+        rp = np.ascontiguousarray(system.row_ptr, dtype=np.int32)
+        ci = np.ascontiguousarray(system.col_idx, dtype=np.int32)
+        self._raise(lib.bc_devset_set_pattern(self._set, int(system.species), _ptr(rp), _ptr(ci)))
+        prm = Solver._params(system, config, algo, device, tol, max_iter, None, timing)
+        ng, cpb = C.c_int64(), C.c_double()
+        _raise(None, lib.bc_plan(int(system.species), C.byref(prm), C.byref(ng), C.byref(cpb)))
+        ng = int(ng.value)
+        iters = np.empty(ng, np.int32)
+        rms = np.empty(ng, np.float64)
+        flags = np.empty(ng, np.uint8)
+        rep = Report()
+        t0 = time.perf_counter_ns()
+        st = lib.bc_devset_solve(self._set, C.byref(prm), _ptr(system.values), _ptr(system.rhs), _ptr(x_out),
+                                 _ptr(iters), _ptr(rms), _ptr(flags), C.byref(rep))
+        wall = time.perf_counter_ns() - t0
+        self._raise(st)
+        return SolveReport(
+            strategy=Strategy(config.kind), cells_per_block=float(rep.cells_per_block),
+            iterations_effective=int(rep.iterations_effective), iterations_sum=int(rep.iterations_sum),
+            per_block_iterations=iters.astype(np.int64), max_residual_rms=float(rep.max_residual_rms),
+            wall_time_ns=int(wall), breakdown_fallbacks=int(rep.breakdown_fallbacks), per_cell_x=x_out,
+            per_block_residual_rms=rms, per_block_flags=flags, device_ms=float(rep.device_ms),
+            kernel_launches=int(rep.kernel_launches), kernels=int(rep.kernels),
+            model_spmv_wavefronts=float(rep.model_spmv_wavefronts))
 
 
 _default: dict = {}

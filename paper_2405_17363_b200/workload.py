@@ -65,6 +65,13 @@ class Mechanism:
                      threads: int = 0) -> Tuple[np.ndarray, np.ndarray]:
         values = np.empty((count, self.nnz), np.float64) if values is None else values
         rhs = np.empty((count, self.species), np.float64) if rhs is None else rhs
+        for name, a, shape in (("values", values, (count, self.nnz)), ("rhs", rhs, (count, self.species)),
+                               ("y", y, (count, self.species)), ("y_prev", y_prev, (count, self.species))):
+            if a is None:
+                continue
+            if not isinstance(a, np.ndarray) or a.dtype != np.float64 or a.shape != shape or \
+                    not a.flags["C_CONTIGUOUS"]:
+                raise ValueError(f"newton_batch: {name} must be a C-contiguous float64 array of shape {shape}")
         st = self.lib.bcw_newton_batch(self._m, first, count, total_cells, mode, float(h), _p(y), _p(y_prev),
                                        _p(values), _p(rhs), threads)
         if st != 0:

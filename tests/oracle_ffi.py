@@ -78,6 +78,11 @@ def ref() -> C.CDLL:
                                        C.POINTER(_i64), C.POINTER(_f64), C.POINTER(_i32), C.POINTER(_i32)]
         lib.ref_lu_solve.argtypes = [_i64, _p, _p, _p, _p, _p]
         lib.ref_bicgstab_solve.argtypes = lib.ref_bicg_solve.argtypes
+        lib.ref_batch_create.restype = _p
+        lib.ref_batch_create.argtypes = [_i64, _i64, _p, _p, _p, _p]
+        lib.ref_batch_destroy.argtypes = [_p]
+        lib.ref_batch_run.argtypes = [_p, C.c_int, C.c_int, _i64, _f64, _i64, _i64, _i64, _p, _p, _p, _p,
+                                      C.POINTER(RefReport)]
         lib.ref_solve_batch_bicgstab.argtypes = [C.c_int, _i64, _i64, _i64, _p, _p, _p, _p, _f64, _i64, _i64, _i64,
                                                  _p, _p, _p, _p, C.POINTER(RefReport)]
         lib.ref_tree_reduce.restype = _f64
@@ -158,6 +163,42 @@ def ref_solve_batch_bicgstab(strategy, k, row_ptr, col_idx, values, rhs, tol, ma
                                         ptr(np.ascontiguousarray(rhs)), tol, max_iter, mtpb, workers, ptr(x), ptr(it),
                                         ptr(rms), ptr(fl), C.byref(rep))
     return st, BatchResult(x, it, rms, fl, rep)
+
+
+class RefBatch:
+    """The reference's host BatchedSystem (strategies.hpp:15-23), built once
+    in oracle/_ref and solved repeatedly: run(algo=0) is the stock
+    run_strategy (BiCG), run(algo=1) the composed Jacobi-BiCGSTAB."""
+
+    def __init__(self, row_ptr, col_idx, values, rhs):
+        self.species = len(row_ptr) - 1
+        self.cells = values.shape[0]
+        self.row_ptr = np.ascontiguousarray(row_ptr, np.int32)
+        self.h = ref().ref_batch_create(self.species, self.cells, ptr(self.row_ptr),
+                                        ptr(np.ascontiguousarray(col_idx, np.int32)),
+                                        ptr(np.ascontiguousarray(values)), ptr(np.ascontiguousarray(rhs)))
+        if not self.h:
+            raise MemoryError("ref_batch_create failed")
+
+    def run(self, algo, strategy, k, tol, max_iter, mtpb=1024, workers=1, x=None):
+        ng = orc().orc_group_count(strategy, self.cells, self.species, mtpb, k)
+        ng = max(ng, 1)
+        x = np.empty((self.cells, self.species)) if x is None else x
+        it = np.zeros(ng, np.int64)
+        rms = np.zeros(ng) if algo == 1 else None
+        fl = np.zeros(ng, np.uint8) if algo == 1 else None
+        rep = RefReport()
+        st = ref().ref_batch_run(self.h, algo, strategy, k, tol, max_iter, mtpb, workers, ptr(x), ptr(it), ptr(rms),
+                                 ptr(fl), C.byref(rep))
+        return st, BatchResult(x, it, rms, fl, rep)
+
+    def close(self):
+        if self.h:
+            ref().ref_batch_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
 
 
 def ref_solve_checker(algo, strategy, k, row_ptr, col_idx, values, rhs, tol, max_iter, mtpb=1024, workers=1):

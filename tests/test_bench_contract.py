@@ -18,7 +18,7 @@ def test_reference_arm_json_line():
     if not (of.have_ref() or os.path.exists(of.ORC_PATH)):
         pytest.skip("no CPU checker built")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
-                        "--warmup", "1", "--cells", "2000", "--cpu-seconds", "1"],
+                        "--warmup", "1", "--cells", "300", "--cpu-seconds", "1"],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
@@ -30,3 +30,13 @@ def test_reference_arm_json_line():
     cb = line["cpu_baseline"]
     assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["sample"]
     assert cb["value"] == line["value"]
+    assert line["ms_per_step"] > 0 and line["steps"] == 1
+    # the same config dict the B200 arm prints for the same flags (the driver's same_config)
+    import argparse
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2405_17363_b200 import REGIME_P
+    args = argparse.Namespace(algo="bicgstab", strategy="block-cells-1")
+    assert line["config"] == bench.bench_config(args, 156, 1556, 300, 300, REGIME_P, 1)
+    # the stock reference algorithm is timed beside the composed BiCGSTAB
+    assert line["reference_bicg"]["value"] > 0

@@ -249,3 +249,25 @@ def test_bicgstab_north_star_tolerance_vs_reference_lu(m156):
         assert rel <= 1e-10, (c, rel)
         ok += 1
     assert ok >= 30
+
+
+@needs_ref
+def test_resident_reference_batch_matches_one_shot():
+    """bench.py's reference arm: the resident BatchedSystem gives the same
+    bits as the one-shot wrappers (stock BiCG run_strategy, composed BiCGSTAB)."""
+    rng = np.random.default_rng(21)
+    rp, ci, v, b = random_batch(rng, 23, 31, 0.2)
+    rb = of.RefBatch(rp, ci, v, b)
+    for k in (1, 0, 5):
+        st1, r1 = rb.run(0, 2, k, 1e-12, 300, workers=4)
+        st2, r2 = of.ref_solve_batch(2, k, rp, ci, v, b, 1e-12, 300, workers=2)
+        assert st1 == st2 == 0
+        np.testing.assert_array_equal(of.bits(r1.x), of.bits(r2.x))
+        np.testing.assert_array_equal(r1.iters, r2.iters)
+        st1, r1 = rb.run(1, 2, k, 1e-12, 300, workers=4)
+        st2, r2 = of.ref_solve_batch_bicgstab(2, k, rp, ci, v, b, 1e-12, 300, workers=1)
+        assert st1 == st2 == 0
+        np.testing.assert_array_equal(of.bits(r1.x), of.bits(r2.x))
+        np.testing.assert_array_equal(r1.flags, r2.flags)
+        np.testing.assert_array_equal(of.bits(r1.rms), of.bits(r2.rms))
+    rb.close()
