@@ -307,13 +307,29 @@ def main_reference(args):
     rb = of.RefBatch(rp, ci, values, rhs)
     x = np.empty((cells, args.species))
     times = []
-    for i in range(args.warmup + args.steps):
+    st, res = rb.run(algo, strat, k, reg.tol, reg.max_iter, workers=cores, x=x)  # warm-up 1: the whole workload
+    assert st == 0, st
+    # Every step is the whole workload unless that would take the run past
+    # ~7 minutes; then each step is the same contiguous prefix sample, sized
+    # to fit (ms_per_step is always the measured time of what a step solved).
+    per_step = res.report.wall_time_ns / 1e9
+    sample = cells
+    if per_step * (args.warmup + args.steps) > 420.0:
+        sample = max(1, int(cells * 420.0 / (per_step * (args.warmup + args.steps))))
+        if strat == 2 and k > 1:
+            sample = max(k, sample // k * k)
+        rb.close()
+        rb = of.RefBatch(rp, ci, np.ascontiguousarray(values[:sample]), np.ascontiguousarray(rhs[:sample]))
+        x = np.empty((sample, args.species))
+    for i in range(1, args.warmup + args.steps):
         st, res = rb.run(algo, strat, k, reg.tol, reg.max_iter, workers=cores, x=x)
         assert st == 0, st
         if i >= args.warmup:
             times.append(res.report.wall_time_ns / 1e9)
+    if args.warmup == 0:
+        times.insert(0, per_step)
     total_s = sum(times)
-    value = cells * args.steps / total_s
+    value = sample * args.steps / total_s
     impl = ("Jacobi-BiCGSTAB composed from the reference's compiled spmv/axpby/plan_reduce_map/lu_solve and its "
             "strategy drivers (oracle/_ref ref_bicgstab.cpp)" if algo == 1 else "the reference's stock run_strategy")
     extra = None
@@ -330,8 +346,9 @@ def main_reference(args):
         "config": bench_config(args, args.species, nnz, cells, n_total, reg, world),
         "reference_impl": impl,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"{impl}: all {cells} cells every step, {cores} threads, "
-                                   f"SolveReport::wall_time_ns"},
+                         "sample": (f"{impl}: " + (f"all {cells} cells" if sample == cells else
+                                                           f"the first {sample} of {cells} cells") +
+                                    f" every step, {cores} threads, SolveReport::wall_time_ns")},
         "reference_bicg": extra,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
