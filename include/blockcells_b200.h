@@ -110,7 +110,8 @@ enum {
     BC_KERNEL_BLOCK = 2,  /* block_cells_kernel (BiCG / wide groups, shared-memory operands) */
     BC_KERNEL_MULTI = 4,  /* multi_cells_kernel (cooperative, grid-wide reductions) */
     BC_KERNEL_THREAD = 8, /* thread_per_cell_kernel (+ interleave_kernel) */
-    BC_KERNEL_LU = 16     /* lu_fallback_kernel */
+    BC_KERNEL_LU = 16,    /* lu_fallback_kernel */
+    BC_KERNEL_LATENCY = 32 /* block_cells_latency_kernel (small batches: one CTA, one thread per row) */
 };
 
 typedef struct {

@@ -11,6 +11,7 @@ from .solver import (  # noqa: F401
     FLAG_CONVERGED,
     FLAG_FELL_BACK,
     KERNEL_BLOCK,
+    KERNEL_LATENCY,
     KERNEL_LU,
     KERNEL_MULTI,
     KERNEL_THREAD,

@@ -22,6 +22,7 @@
 #include "bc_newton.cuh"
 #include "bc_thread.cuh"
 #include "bc_tmem.cuh"
+#include "bc_latency.cuh"
 #include "bc_plan.hpp"
 #include "blockcells_b200.h"
 
@@ -109,6 +110,16 @@ const KernelCfg* pick_config(const bc::Geometry& g) {
 
 }  // namespace
 
+// Latency-mode row tables of a group geometry (bc_latency.cuh): [lmax][P]
+// value indices and gather byte offsets of each thread's row (and, for BiCG,
+// of its A^T row); device copies live in the context's plan buffers.
+struct LatPlan {
+    int P = 0, lmax = 0;
+    bool ok = false;
+    int32_t *rvi = nullptr, *tvi = nullptr, *didx = nullptr;
+    uint16_t *rxo = nullptr, *txo = nullptr;
+};
+
 struct bc_ctx {
     int device = 0;
     int sms = 0;
@@ -133,6 +144,7 @@ struct bc_ctx {
     int64_t launches = 0;
     int32_t kernels = 0;  // BC_KERNEL_* bits since the last bc_solve started
     double model_spmv_wf = 0.0;  // modelled shared wavefronts per group-iteration of the last TMEM launch
+    std::map<std::pair<int, int>, struct LatPlan> lat_plans;  // (k, bicg): latency-mode row tables
     std::map<BlockFn, bool> smem_set;
 };
 
@@ -553,6 +565,147 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
     return true;
 }
 
+// ---- latency mode (bc_latency.cuh) ----------------------------------------
+
+using LatFn = void (*)(bc::LatencyParams);
+struct LatCfg {
+    int W, LMAX, ALGO;
+    LatFn fn;
+};
+#define BC_LAT_CFG(W, L, A) {W, L, A, &bc::block_cells_latency_kernel<W, L, A>}
+const LatCfg kLatConfigs[] = {
+    BC_LAT_CFG(2, 16, kS), BC_LAT_CFG(2, 24, kS), BC_LAT_CFG(2, 32, kS),
+    BC_LAT_CFG(4, 16, kS), BC_LAT_CFG(4, 24, kS), BC_LAT_CFG(4, 32, kS),
+    BC_LAT_CFG(8, 16, kS), BC_LAT_CFG(8, 24, kS), BC_LAT_CFG(8, 32, kS),
+    BC_LAT_CFG(16, 16, kS), BC_LAT_CFG(16, 24, kS), BC_LAT_CFG(16, 32, kS),
+    BC_LAT_CFG(2, 16, kB), BC_LAT_CFG(2, 24, kB), BC_LAT_CFG(2, 32, kB),
+    BC_LAT_CFG(4, 16, kB), BC_LAT_CFG(4, 24, kB), BC_LAT_CFG(4, 32, kB),
+    BC_LAT_CFG(8, 16, kB), BC_LAT_CFG(8, 24, kB), BC_LAT_CFG(8, 32, kB),
+    BC_LAT_CFG(16, 16, kB), BC_LAT_CFG(16, 24, kB), BC_LAT_CFG(16, 32, kB),
+};
+#undef BC_LAT_CFG
+
+// BC_LATENCY: 0 never, 1 whenever a group qualifies; default: launches of at
+// most BC_LATENCY_MAX_GROUPS groups (default one per SM), where the
+// throughput kernel would leave SMs idle and one cell's iteration latency is
+// the whole run.
+bool latency_wanted(const bc_ctx* ctx, int groups) {
+    if (const char* e = std::getenv("BC_LATENCY")) {
+        if (std::string(e) == "0") return false;
+        if (std::string(e) == "1") return true;
+    }
+    if (tmem_team_pref() || tmem_disabled()) return false;  // an explicit kernel choice
+    const char* m = std::getenv("BC_LATENCY_MAX_GROUPS");
+    const int mx = m ? std::atoi(m) : ctx->sms;
+    return groups <= mx;
+}
+
+LatPlan& latency_plan(bc_ctx* ctx, const bc::Pattern& pat, int k, bool bicg) {
+    const auto key = std::make_pair(k, bicg ? 1 : 0);
+    auto it = ctx->lat_plans.find(key);
+    if (it != ctx->lat_plans.end()) return it->second;
+    LatPlan lp;
+    const int s = pat.species, nnz = pat.nnz;
+    const int64_t n = static_cast<int64_t>(k) * s;
+    const int P = static_cast<int>(bc::padded_len(n));
+    int lmax = 0;
+    std::vector<std::vector<int>> tcols(s);  // column j: CSR entries e in ascending row order
+    for (int i = 0; i < s; ++i) {
+        lmax = std::max(lmax, pat.row_ptr[i + 1] - pat.row_ptr[i]);
+        for (int e = pat.row_ptr[i]; e < pat.row_ptr[i + 1]; ++e) tcols[pat.col_idx[e]].push_back(e);
+    }
+    if (bicg)
+        for (const auto& cl : tcols) lmax = std::max(lmax, static_cast<int>(cl.size()));
+    lp.P = P;
+    lp.lmax = lmax;
+    lp.ok = P >= 64 && P <= 512 && lmax <= 32 && 8 * (2 * P + 1) < 65536;
+    if (lp.ok) {
+        const int L = lmax <= 16 ? 16 : lmax <= 24 ? 24 : 32;
+        std::vector<int32_t> rvi(static_cast<size_t>(L) * P, -1), tvi, didx(n, -1);
+        std::vector<uint16_t> rxo(static_cast<size_t>(L) * P, static_cast<uint16_t>(8 * P)), txo;
+        if (bicg) {
+            tvi.assign(static_cast<size_t>(L) * P, -1);
+            txo.assign(static_cast<size_t>(L) * P, static_cast<uint16_t>(8 * P));
+        }
+        for (int c = 0; c < k; ++c)
+            for (int i = 0; i < s; ++i) {
+                const int t = c * s + i;
+                for (int e = pat.row_ptr[i], q = 0; e < pat.row_ptr[i + 1]; ++e, ++q) {
+                    rvi[static_cast<size_t>(q) * P + t] = c * nnz + e;
+                    rxo[static_cast<size_t>(q) * P + t] = static_cast<uint16_t>(8 * (c * s + pat.col_idx[e]));
+                }
+                if (pat.diag[i] >= 0) didx[t] = c * nnz + pat.diag[i];
+                if (bicg) {
+                    int q = 0;
+                    for (int e : tcols[i]) {  // A^T row t = column i of cell c, ascending source row
+                        int src = 0;
+                        while (pat.row_ptr[src + 1] <= e) ++src;
+                        tvi[static_cast<size_t>(q) * P + t] = c * nnz + e;
+                        txo[static_cast<size_t>(q) * P + t] = static_cast<uint16_t>(8 * (P + 1 + c * s + src));
+                        ++q;
+                    }
+                }
+            }
+        lp.lmax = L;
+        lp.rvi = upload(ctx, rvi);
+        lp.rxo = upload(ctx, rxo);
+        lp.didx = upload(ctx, didx);
+        if (bicg) {
+            lp.tvi = upload(ctx, tvi);
+            lp.txo = upload(ctx, txo);
+        }
+    }
+    return ctx->lat_plans.emplace(key, lp).first->second;
+}
+
+bool launch_latency(bc_ctx* ctx, const bc::Pattern& pat, const bc::GroupPlan& gp, int algo, int64_t cell0,
+                    int64_t gout0, int groups, const double* values, const double* rhs, double* x, double tol,
+                    int64_t max_iter, cudaStream_t st, const bc::InputGate& gate = bc::InputGate{}) {
+    if (!latency_wanted(ctx, groups)) return false;
+    const bool bicg = algo == BC_ALGO_BICG;
+    LatPlan& lp = latency_plan(ctx, pat, gp.k, bicg);
+    if (!lp.ok) return false;
+    const int W = lp.P / 32, A = bicg ? bc::kBiCG : bc::kBiCGStab;
+    const LatCfg* cfg = nullptr;
+    for (const LatCfg& c : kLatConfigs)
+        if (c.W == W && c.LMAX == lp.lmax && c.ALGO == A) cfg = &c;
+    if (!cfg) return false;
+    bc::LatencyParams p{};
+    p.values = values;
+    p.rhs = rhs;
+    p.x_out = x;
+    p.g_iters = ctx->giters.as<int32_t>();
+    p.g_rms = ctx->grms.as<double>();
+    p.g_flags = ctx->gflags.as<uint8_t>();
+    p.rvi = lp.rvi;
+    p.rxo = lp.rxo;
+    p.tvi = lp.tvi;
+    p.txo = lp.txo;
+    p.didx = lp.didx;
+    p.cell_offset = cell0;
+    p.group_offset = gout0;
+    p.group_count = groups;
+    p.n = gp.geo.n;
+    p.nnz = pat.nnz;
+    p.P = lp.P;
+    p.species = pat.species;
+    p.kc = gp.k;
+    p.xslots = bicg ? 2 * lp.P + 1 : lp.P + 1;
+    p.sigma_max = sigma_threshold(tol, gp.geo.n);
+    p.tol = tol;
+    p.max_iter = static_cast<int>(std::min<int64_t>(max_iter, 0x7FFFFFFE));
+    p.gate = gate;
+    const size_t smem = sizeof(double) * (static_cast<size_t>(p.xslots) + 2 * 4 * 32 * static_cast<size_t>(W));
+    int per_sm = 0;
+    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cfg->fn, 32 * W, smem), "occupancy(latency)");
+    const int blocks = std::max(1, std::min(groups, ctx->sms * std::max(1, per_sm)));
+    cfg->fn<<<blocks, 32 * W, smem, st>>>(p);
+    check_cuda(cudaGetLastError(), "block_cells_latency_kernel launch");
+    ctx->launches++;
+    ctx->kernels |= BC_KERNEL_LATENCY;
+    return true;
+}
+
 // Launch the fused kernel over `groups` groups of kc cells starting at cell0.
 void launch_block(bc_ctx* ctx, const bc::Pattern& pat, const bc::GroupPlan& gp, int algo,
                   int64_t cell0, int64_t gout0, int groups, const double* values,
@@ -943,6 +1096,7 @@ int bc_set_pattern(bc_ctx* ctx, int32_t species, const int32_t* row_ptr, const i
             p.col_idx == ctx->pat.col_idx)
             return BC_OK;
         ctx->plans.clear();
+        ctx->lat_plans.clear();
         for (DevBuf& b : ctx->plan_bufs) b.release();
         ctx->plan_bufs.clear();
         check_cuda(ctx->d_rp.ensure(sizeof(int32_t) * p.row_ptr.size()), "cudaMalloc");
@@ -1108,6 +1262,7 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
         } else {
             for (const GroupSpan& sp : spans) {  // host-side planning before the timed region
                 bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);
+                if (latency_wanted(ctx, sp.count) && latency_plan(ctx, pat, sp.k, bicg).ok) continue;
                 const TmemCfg* cfg = nullptr;
                 if (bc::TmemPlan* tp = tmem_plan(ctx, pat, gp, sp.count, &cfg))
                     ensure_tmem_lane_tables(ctx, gp, *tp, cfg->RV);
@@ -1194,6 +1349,9 @@ int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, cons
             const GroupSpan& sp = spans[i];
             bc::GroupPlan& gp = get_plan(ctx, pat, sp.k, bicg, &ctx->plans);
             unsigned int* counter = ctx->counters.as<unsigned int>() + slot++;
+            if (launch_latency(ctx, pat, gp, prm->algo, sp.cell0, sp.gout0, sp.count, d_values, d_rhs, d_x,
+                               prm->tol, prm->max_iter, st, gates[i]))
+                continue;
             if (!launch_tmem(ctx, pat, gp, sp.cell0, sp.gout0, sp.count, d_values, d_rhs, d_x, prm->tol,
                                      prm->max_iter, counter, st, gates[i]))
                 launch_block(ctx, pat, gp, prm->algo, sp.cell0, sp.gout0, sp.count, d_values, d_rhs, nullptr, d_x,

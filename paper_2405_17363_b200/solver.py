@@ -133,7 +133,7 @@ class SolveReport:
 
 
 # bc_report.kernels bits (include/blockcells_b200.h)
-KERNEL_TMEM, KERNEL_BLOCK, KERNEL_MULTI, KERNEL_THREAD, KERNEL_LU = 1, 2, 4, 8, 16
+KERNEL_TMEM, KERNEL_BLOCK, KERNEL_MULTI, KERNEL_THREAD, KERNEL_LU, KERNEL_LATENCY = 1, 2, 4, 8, 16, 32
 
 
 @dataclass
