@@ -114,9 +114,9 @@ const KernelCfg* pick_config(const bc::Geometry& g) {
 // value indices and gather byte offsets of each thread's row (and, for BiCG,
 // of its A^T row); device copies live in the context's plan buffers.
 struct LatPlan {
-    int P = 0, lmax = 0;
+    int P = 0, T = 0, L = 0, xslots = 0, model = 0;
     bool ok = false;
-    int32_t *rvi = nullptr, *tvi = nullptr, *didx = nullptr;
+    int32_t *rowof = nullptr, *steps = nullptr, *rvi = nullptr, *tvi = nullptr, *didx = nullptr;
     uint16_t *rxo = nullptr, *txo = nullptr;
 };
 
@@ -569,21 +569,34 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
 
 using LatFn = void (*)(bc::LatencyParams);
 struct LatCfg {
-    int W, LMAX, ALGO;
+    int R, RV, LMAX, ALGO;  // tree slots per lane (P/32), warps = row slots per lane, padded row length
     LatFn fn;
 };
-#define BC_LAT_CFG(W, L, A) {W, L, A, &bc::block_cells_latency_kernel<W, L, A>}
+#define BC_LAT_CFG(R, RV, L, A) {R, RV, L, A, &bc::block_cells_latency_kernel<R, RV, L, A>}
+#define BC_LAT_CFGS(R, RV, A) BC_LAT_CFG(R, RV, 16, A), BC_LAT_CFG(R, RV, 24, A), BC_LAT_CFG(R, RV, 32, A)
+// P = 64 .. 256; the warps (RV) cover ceil(n/32) row slots -- an instance with
+// more warps than rows needs runs the extra rows as zeros.  P = 512 (M312:
+// ten warps of ~170 registers, spilling) measured slower than the TMEM
+// kernel's two-warp teams at 100 cells (6.74 vs 6.29 ms), so it has none.
 const LatCfg kLatConfigs[] = {
-    BC_LAT_CFG(2, 16, kS), BC_LAT_CFG(2, 24, kS), BC_LAT_CFG(2, 32, kS),
-    BC_LAT_CFG(4, 16, kS), BC_LAT_CFG(4, 24, kS), BC_LAT_CFG(4, 32, kS),
-    BC_LAT_CFG(8, 16, kS), BC_LAT_CFG(8, 24, kS), BC_LAT_CFG(8, 32, kS),
-    BC_LAT_CFG(16, 16, kS), BC_LAT_CFG(16, 24, kS), BC_LAT_CFG(16, 32, kS),
-    BC_LAT_CFG(2, 16, kB), BC_LAT_CFG(2, 24, kB), BC_LAT_CFG(2, 32, kB),
-    BC_LAT_CFG(4, 16, kB), BC_LAT_CFG(4, 24, kB), BC_LAT_CFG(4, 32, kB),
-    BC_LAT_CFG(8, 16, kB), BC_LAT_CFG(8, 24, kB), BC_LAT_CFG(8, 32, kB),
-    BC_LAT_CFG(16, 16, kB), BC_LAT_CFG(16, 24, kB), BC_LAT_CFG(16, 32, kB),
+    BC_LAT_CFGS(2, 2, kS), BC_LAT_CFGS(4, 4, kS), BC_LAT_CFGS(8, 5, kS), BC_LAT_CFGS(8, 8, kS),
+    BC_LAT_CFGS(2, 2, kB), BC_LAT_CFGS(4, 4, kB), BC_LAT_CFGS(8, 5, kB), BC_LAT_CFGS(8, 8, kB),
 };
+#undef BC_LAT_CFGS
 #undef BC_LAT_CFG
+
+// The instance for a group geometry: R = P/32, the fewest warps covering the rows.
+const LatCfg* latency_cfg(int64_t n, int lmax, bool bicg) {
+    const int64_t P = bc::padded_len(n);
+    const int R = static_cast<int>(P / 32), need = static_cast<int>((n + 31) / 32);
+    const int L = lmax <= 16 ? 16 : lmax <= 24 ? 24 : 32;
+    const LatCfg* best = nullptr;
+    for (const LatCfg& c : kLatConfigs)
+        if (c.R == R && c.RV >= need && c.LMAX == L && c.ALGO == (bicg ? bc::kBiCG : bc::kBiCGStab) &&
+            (!best || c.RV < best->RV))
+            best = &c;
+    return best;
+}
 
 // BC_LATENCY: 0 never, 1 whenever a group qualifies; default: launches of at
 // most BC_LATENCY_MAX_GROUPS groups (default one per SM), where the
@@ -605,54 +618,42 @@ LatPlan& latency_plan(bc_ctx* ctx, const bc::Pattern& pat, int k, bool bicg) {
     auto it = ctx->lat_plans.find(key);
     if (it != ctx->lat_plans.end()) return it->second;
     LatPlan lp;
-    const int s = pat.species, nnz = pat.nnz;
-    const int64_t n = static_cast<int64_t>(k) * s;
-    const int P = static_cast<int>(bc::padded_len(n));
-    int lmax = 0;
-    std::vector<std::vector<int>> tcols(s);  // column j: CSR entries e in ascending row order
-    for (int i = 0; i < s; ++i) {
-        lmax = std::max(lmax, pat.row_ptr[i + 1] - pat.row_ptr[i]);
-        for (int e = pat.row_ptr[i]; e < pat.row_ptr[i + 1]; ++e) tcols[pat.col_idx[e]].push_back(e);
-    }
-    if (bicg)
-        for (const auto& cl : tcols) lmax = std::max(lmax, static_cast<int>(cl.size()));
-    lp.P = P;
-    lp.lmax = lmax;
-    lp.ok = P >= 64 && P <= 512 && lmax <= 32 && 8 * (2 * P + 1) < 65536;
-    if (lp.ok) {
-        const int L = lmax <= 16 ? 16 : lmax <= 24 ? 24 : 32;
-        std::vector<int32_t> rvi(static_cast<size_t>(L) * P, -1), tvi, didx(n, -1);
-        std::vector<uint16_t> rxo(static_cast<size_t>(L) * P, static_cast<uint16_t>(8 * P)), txo;
-        if (bicg) {
-            tvi.assign(static_cast<size_t>(L) * P, -1);
-            txo.assign(static_cast<size_t>(L) * P, static_cast<uint16_t>(8 * P));
+    const int64_t n = static_cast<int64_t>(k) * pat.species;
+    const int64_t P = bc::padded_len(n);
+    if (P >= 64 && P <= 256) {
+        // longest row (BiCG: or A^T row) picks the instance's padded length
+        std::vector<int> clen(pat.species, 0);
+        int lmax = 0;
+        for (int i = 0; i < pat.species; ++i) {
+            lmax = std::max(lmax, pat.row_ptr[i + 1] - pat.row_ptr[i]);
+            for (int e = pat.row_ptr[i]; e < pat.row_ptr[i + 1]; ++e) clen[pat.col_idx[e]]++;
         }
-        for (int c = 0; c < k; ++c)
-            for (int i = 0; i < s; ++i) {
-                const int t = c * s + i;
-                for (int e = pat.row_ptr[i], q = 0; e < pat.row_ptr[i + 1]; ++e, ++q) {
-                    rvi[static_cast<size_t>(q) * P + t] = c * nnz + e;
-                    rxo[static_cast<size_t>(q) * P + t] = static_cast<uint16_t>(8 * (c * s + pat.col_idx[e]));
-                }
-                if (pat.diag[i] >= 0) didx[t] = c * nnz + pat.diag[i];
-                if (bicg) {
-                    int q = 0;
-                    for (int e : tcols[i]) {  // A^T row t = column i of cell c, ascending source row
-                        int src = 0;
-                        while (pat.row_ptr[src + 1] <= e) ++src;
-                        tvi[static_cast<size_t>(q) * P + t] = c * nnz + e;
-                        txo[static_cast<size_t>(q) * P + t] = static_cast<uint16_t>(8 * (P + 1 + c * s + src));
-                        ++q;
+        if (bicg)
+            for (int c : clen) lmax = std::max(lmax, c);
+        const LatCfg* cfg = lmax <= 32 ? latency_cfg(n, lmax, bicg) : nullptr;
+        if (cfg) {
+            try {
+                const bc::LatencySchedule ls = bc::build_latency_schedule(pat, k, bicg, 32 * cfg->RV);
+                lp.ok = ls.lmax <= 32 && ls.L == cfg->LMAX && ls.T == 32 * cfg->RV;
+                lp.P = ls.P;
+                lp.T = ls.T;
+                lp.L = ls.L;
+                lp.xslots = ls.xslots;
+                lp.model = ls.model_wavefronts;
+                if (lp.ok) {
+                    lp.rowof = upload(ctx, ls.rowof);
+                    lp.steps = upload(ctx, ls.steps);
+                    lp.rvi = upload(ctx, ls.rvi);
+                    lp.rxo = upload(ctx, ls.rxo);
+                    lp.didx = upload(ctx, ls.didx);
+                    if (bicg) {
+                        lp.tvi = upload(ctx, ls.tvi);
+                        lp.txo = upload(ctx, ls.txo);
                     }
                 }
+            } catch (const std::invalid_argument&) {
+                lp.ok = false;  // offsets beyond 16 bits: the throughput kernels take it
             }
-        lp.lmax = L;
-        lp.rvi = upload(ctx, rvi);
-        lp.rxo = upload(ctx, rxo);
-        lp.didx = upload(ctx, didx);
-        if (bicg) {
-            lp.tvi = upload(ctx, tvi);
-            lp.txo = upload(ctx, txo);
         }
     }
     return ctx->lat_plans.emplace(key, lp).first->second;
@@ -665,10 +666,10 @@ bool launch_latency(bc_ctx* ctx, const bc::Pattern& pat, const bc::GroupPlan& gp
     const bool bicg = algo == BC_ALGO_BICG;
     LatPlan& lp = latency_plan(ctx, pat, gp.k, bicg);
     if (!lp.ok) return false;
-    const int W = lp.P / 32, A = bicg ? bc::kBiCG : bc::kBiCGStab;
     const LatCfg* cfg = nullptr;
     for (const LatCfg& c : kLatConfigs)
-        if (c.W == W && c.LMAX == lp.lmax && c.ALGO == A) cfg = &c;
+        if (c.R == lp.P / 32 && 32 * c.RV == lp.T && c.LMAX == lp.L && c.ALGO == (bicg ? bc::kBiCG : bc::kBiCGStab))
+            cfg = &c;
     if (!cfg) return false;
     bc::LatencyParams p{};
     p.values = values;
@@ -677,6 +678,8 @@ bool launch_latency(bc_ctx* ctx, const bc::Pattern& pat, const bc::GroupPlan& gp
     p.g_iters = ctx->giters.as<int32_t>();
     p.g_rms = ctx->grms.as<double>();
     p.g_flags = ctx->gflags.as<uint8_t>();
+    p.rowof = lp.rowof;
+    p.steps = lp.steps;
     p.rvi = lp.rvi;
     p.rxo = lp.rxo;
     p.tvi = lp.tvi;
@@ -690,16 +693,24 @@ bool launch_latency(bc_ctx* ctx, const bc::Pattern& pat, const bc::GroupPlan& gp
     p.P = lp.P;
     p.species = pat.species;
     p.kc = gp.k;
-    p.xslots = bicg ? 2 * lp.P + 1 : lp.P + 1;
+    p.xs = lp.xslots;
     p.sigma_max = sigma_threshold(tol, gp.geo.n);
     p.tol = tol;
     p.max_iter = static_cast<int>(std::min<int64_t>(max_iter, 0x7FFFFFFE));
     p.gate = gate;
-    const size_t smem = sizeof(double) * (static_cast<size_t>(p.xslots) + 2 * 4 * 32 * static_cast<size_t>(W));
+    // Y [2][2][P] + one gather region per warp
+    const int threads = lp.T;
+    const size_t smem = sizeof(double) * (4 * static_cast<size_t>(lp.P) + static_cast<size_t>(threads / 32) * lp.xslots);
+    if (smem > static_cast<size_t>(kMaxDynSmem - 1024)) return false;
+    if (!ctx->smem_set[reinterpret_cast<BlockFn>(cfg->fn)]) {
+        check_cuda(cudaFuncSetAttribute(cfg->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem - 1024),
+                   "cudaFuncSetAttribute(latency)");
+        ctx->smem_set[reinterpret_cast<BlockFn>(cfg->fn)] = true;
+    }
     int per_sm = 0;
-    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cfg->fn, 32 * W, smem), "occupancy(latency)");
+    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cfg->fn, threads, smem), "occupancy(latency)");
     const int blocks = std::max(1, std::min(groups, ctx->sms * std::max(1, per_sm)));
-    cfg->fn<<<blocks, 32 * W, smem, st>>>(p);
+    cfg->fn<<<blocks, threads, smem, st>>>(p);
     check_cuda(cudaGetLastError(), "block_cells_latency_kernel launch");
     ctx->launches++;
     ctx->kernels |= BC_KERNEL_LATENCY;

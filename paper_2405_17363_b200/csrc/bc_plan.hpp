@@ -87,6 +87,23 @@ struct TmemSchedule {
     int conflict_cost = 0;          // modelled gather wavefronts per pass
 };
 
+// Latency-mode schedule (bc_latency_plan.cpp, bc_latency.cuh): one SpMV row
+// per thread, rows dealt to threads longest first, per-warp step counts,
+// gather offsets into the warp's private copy of the vector.
+struct LatencySchedule {
+    int n = 0, P = 0, T = 0;        // rows, tree slots, threads (whole warps covering n)
+    int lmax = 0, L = 0;            // longest row, padded step count (kernel template: 16, 24, 32)
+    int xslots = 0;                 // doubles of one warp's gather region
+    int model_wavefronts = 0;       // modelled gather wavefronts of one SpMV (A and A^T), all warps
+    std::vector<int32_t> rowof;     // [T] group row of thread t, -1 none
+    std::vector<int32_t> steps;     // [T] steps of thread t's warp
+    std::vector<int32_t> rvi, tvi;  // [L][T] group value index, -1 padding (A, A^T)
+    std::vector<uint16_t> rxo, txo; // [L][T] byte offsets of the gathers
+    std::vector<int32_t> didx;      // [P] group value index of row j's diagonal, -1 none
+};
+// threads: the kernel instance's thread count (>= 32 * ceil(n / 32))
+LatencySchedule build_latency_schedule(const Pattern& pat, int k, bool bicg, int threads);
+
 struct GroupPlan {
     int k = 1;
     Geometry geo;

@@ -57,8 +57,10 @@ def test_latency_m156_bitwise(solver, m156, regime, algo):
 
 @pytest.mark.parametrize("algo", [Algo.BICGSTAB_JACOBI, Algo.BICG])
 def test_latency_group_geometries(solver, force_latency, algo):
-    """P = 64, 128, 256, 512: coupled groups (k = 2, 3), the remainder group,
-    M312, and random patterns up to 32 entries per row / column."""
+    """P = 64, 128, 256: coupled groups (k = 2, 3 of small cells), the
+    remainder group, and random patterns up to 32 entries per row / column;
+    P = 512 (M312, M156 k = 3) is checked to fall back to the throughput
+    kernels, bit for bit all the same."""
     m312 = Mechanism(312, 936, 0)
     cases = []
     v, b = m312.newton_batch(0, 9, 9, REGIME_C.h)
