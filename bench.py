@@ -72,6 +72,8 @@ def parse():
     ap.add_argument("--parity-cells", type=int, default=100_000,
                     help="cells checked per run (all of them at N=1 up to this many; strided groups beyond)")
     ap.add_argument("--no-companion", action="store_true", help="skip the GPU BiCG companion measurement")
+    ap.add_argument("--no-dropin", action="store_true",
+                    help="skip e2e_dropin (blockcells::run_strategy through the C++ drop-in, tests/cpp/bin/dropin_bench)")
     return ap.parse_args()
 
 
@@ -551,6 +553,27 @@ def main_b200(args):
                "d2h_bytes_per_step": int(hx.nbytes + ng * (4 + 8 + 1)), "steps": e_steps,
                "ms_per_step": e_ms / e_steps}
 
+    # end to end through the reference's own C++ entry point (blockcells::run_strategy
+    # on the drop-in shim, a BatchedSystem of per-cell CsrMatrix/DenseVector)
+    dropin = None
+    exe = os.path.join(ROOT, "tests", "cpp", "bin", "dropin_bench")
+    if rank == 0 and world == 1 and not args.no_dropin and os.path.exists(exe) and \
+            cfg.kind == Strategy.BlockCells and cfg.cells_per_block == 1:
+        env = dict(os.environ, BLOCKCELLS_B200_DEVICE=str(local))
+        if args.algo == "bicgstab":
+            env["BLOCKCELLS_B200_ALGO"] = "bicgstab"
+        try:
+            r = subprocess.run([exe, str(cells), str(max(1, min(args.steps, 5))), "1", str(n)], env=env,
+                               capture_output=True, text=True, timeout=900)
+            if r.returncode == 0:
+                dropin = json.loads(r.stdout.strip().splitlines()[-1])
+                dropin["h2d_bytes_per_step"] = dropin.pop("input_bytes_per_step")
+                dropin["d2h_bytes_per_step"] = int(cells * n * 8)
+            else:
+                dropin = {"error": r.stderr[-300:]}
+        except Exception as exc:  # the measurement is optional; its absence is reported
+            dropin = {"error": str(exc)[:300]}
+
     # the reference's own algorithm on the GPU, same cells: a like-for-like
     # companion to the stock reference's BiCG number
     companion = None
@@ -637,6 +660,7 @@ def main_b200(args):
             "parity": parity,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_dropin": dropin,
             "bicg_companion": companion,
             "gpu_launches": int(launches),
             "clocks": clocks,

@@ -81,7 +81,8 @@ typedef struct {
     int64_t cells_per_block;       /* Block-cells k; 0 = floor(max_threads_per_block/species) */
     int64_t cells;                 /* number of cells in values/rhs                         */
     double tol;                    /* RMS residual tolerance (> 0)                          */
-    int64_t max_iter;              /* >= 1                                                  */
+    int64_t max_iter;              /* >= 1; iteration counts are int32: values above 2^31 - 2
+                                      act as 2^31 - 2 (hours of iterations for one cell)     */
     int64_t max_threads_per_block; /* DeviceSpec::max_threads_per_block (0 = 1024)          */
     void* stream;                  /* cudaStream_t to run on (NULL = legacy default)        */
     int32_t options;               /* BC_OPT_*                                              */

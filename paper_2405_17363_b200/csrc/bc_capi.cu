@@ -552,7 +552,10 @@ bool launch_tmem(bc_ctx* ctx, const bc::Pattern& pat, bc::GroupPlan& gp, int64_t
     p.cells_per_quarter = cpq;
     p.sigma_max = sigma_threshold(tol, gp.geo.n);
     p.tol = tol;
-    p.max_iter = static_cast<int>(std::min<int64_t>(max_iter, 0x7FFFFFFF));
+    // int loop counter: clamped one below INT_MAX so `++it` cannot overflow.  A
+    // cell still iterating after 2^31 - 2 iterations (hours of solve) stops
+    // there; per-group iteration counts are int32 in the C ABI anyway.
+    p.max_iter = static_cast<int>(std::min<int64_t>(max_iter, 0x7FFFFFFE));
     p.gate = gate;
     const int blocks = std::max(1, std::min(ctx->sms, (groups + teams - 1) / teams));
     check_cuda(cudaMemsetAsync(counter, 0, sizeof(unsigned int), st), "cudaMemsetAsync(counter)");
