@@ -883,14 +883,21 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
     // panels in shared memory while a panel of the largest factored matrix fits in 48 KB
     const int64_t prow = blockdiag ? s : nmax;
     const int panel_rows = prow * (bc::kLuPanel + 1) * 8 <= 48 * 1024 ? static_cast<int>(prow) : 0;
-    const size_t smem = sizeof(double) * panel_rows * (bc::kLuPanel + 1) + sizeof(int) * ((nmax + 1) & ~1) +
-                        sizeof(double) * (nmax + std::max(pmax, nmax));
+    size_t smem = sizeof(double) * panel_rows * (bc::kLuPanel + 1) + sizeof(int) * ((nmax + 1) & ~1) +
+                  sizeof(double) * (nmax + std::max(pmax, nmax));
     // opt in above 48 KB of static + dynamic shared memory (per device: set on every call)
     cudaFuncAttributes fa{};
     check_cuda(cudaFuncGetAttributes(&fa, bc::lu_fallback_kernel), "cudaFuncGetAttributes(lu)");
     const int lu_dyn_max = kMaxDynSmem - static_cast<int>(fa.sharedSizeBytes);
     check_cuda(cudaFuncSetAttribute(bc::lu_fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_dyn_max),
                "cudaFuncSetAttribute(lu)");
+    // block-diagonal groups whose s x s block fits: factor it in shared memory
+    // (BC_LU_SMEM=0 keeps the scratch-resident path for A/B)
+    const size_t smem_blk = sizeof(int) * ((nmax + 1) & ~1) +
+                            sizeof(double) * (nmax + std::max<int64_t>(pmax, static_cast<int64_t>(s) * s));
+    const char* lue = std::getenv("BC_LU_SMEM");
+    const bool use_smem_block = blockdiag && smem_blk <= static_cast<size_t>(lu_dyn_max) && !(lue && *lue == '0');
+    if (use_smem_block) smem = smem_blk;
     if (smem > static_cast<size_t>(lu_dyn_max)) fail(BC_ERR_INVALID_ARGUMENT, "LU fallback: group too large");
     for (size_t b0 = 0; b0 < ents.size(); b0 += batch) {
         const int cnt = static_cast<int>(std::min<int64_t>(batch, ents.size() - b0));
@@ -910,6 +917,7 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
         lp.block_width = block_width;
         lp.mode = blockdiag ? 0 : 1;
         lp.panel_rows = panel_rows;
+        lp.smem_block = use_smem_block ? 1 : 0;
         lp.conv = conv;
         lp.flip = flip;
         lp.later_neg = later_neg;

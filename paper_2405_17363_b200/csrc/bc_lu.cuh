@@ -56,6 +56,9 @@ struct LuParams {
     int block_width;         // 0 = single interval
     int mode;                // 0 block-diagonal when k > 1, 1 dense
     int panel_rows;          // > 0: panels are factored in shared memory (rows <= panel_rows)
+    int smem_block;          // block-diagonal mode: each s x s block is densified, factored and
+                             // forward-substituted in shared memory, then parked in scratch
+                             // for the backward pass (one CTA per SM; 156^2 doubles = 195 KB)
     // dense mode, cells as links of a longer block-diagonal chain (Multi-cells
     // systems too large to densify, solved cell by cell): the three sign-of-
     // zero rules applied to this cell, and its flags for the host's chain scan
@@ -383,17 +386,19 @@ __global__ void __launch_bounds__(256, 3) lu_fallback_kernel(const LuParams p) {
     const int s = p.species;
     const int n = ent.kc * s;
     double* lu = p.scratch + static_cast<size_t>(blockIdx.x) * p.stride;
-    // dynamic shared memory: [panel buffer] perm | sum | slots
+    // dynamic shared memory: [panel buffer] perm | sum | slots, or (smem_block)
+    // perm | sum | the block being factored (also the slots, once every block is done)
     double* pbuf = nullptr;
     const int prow = p.mode == 0 && ent.kc > 1 ? s : n;
     unsigned char* base = smem_raw;
-    if (p.panel_rows > 0) {
+    if (p.panel_rows > 0 && !p.smem_block) {
         if (prow <= p.panel_rows) pbuf = reinterpret_cast<double*>(smem_raw);
         base += sizeof(double) * p.panel_rows * (kLuPanel + 1);
     }
     int* perm = reinterpret_cast<int*>(base);
     double* sum = reinterpret_cast<double*>(base + sizeof(int) * ((n + 1) & ~1));
     double* slots = sum + n;  // >= padded length (also used for products)
+    double* sblk = p.smem_block ? slots : nullptr;
     const int tid = threadIdx.x, nt = blockDim.x;
     const double* vals = p.values + ent.cell0 * p.nnz;
     const double* b = p.rhs + ent.cell0 * s;
@@ -410,7 +415,8 @@ __global__ void __launch_bounds__(256, 3) lu_fallback_kernel(const LuParams p) {
         }
         bool neg_pivot = false, fwd_flip = false;
         for (int c = 0; c < ent.kc; ++c) {
-            double* blk = lu + static_cast<int64_t>(c) * s * s;
+            double* gblk = lu + static_cast<int64_t>(c) * s * s;
+            double* blk = sblk ? sblk : gblk;
             lu_densify(blk, s, vals + static_cast<int64_t>(c) * p.nnz, p.row_ptr, p.col_idx, s, p.nnz, 1);
             if (neg_pivot)
                 for (int q = tid; q < s * s; q += nt)
@@ -438,6 +444,9 @@ __global__ void __launch_bounds__(256, 3) lu_fallback_kernel(const LuParams p) {
             int flip = 0;
             for (int i = tid; i < s; i += nt) flip |= (signbit(blk[i * s + i]) != signbit(y[i])) ? 1 : 0;
             fwd_flip = __syncthreads_or(flip) || fwd_flip;
+            if (sblk)  // park the factors for the backward pass (the next block reuses the buffer)
+                for (int q = tid; q < s * s; q += nt) gblk[q] = sblk[q];
+            __syncthreads();
         }
         bool later_neg = false;
         for (int c = ent.kc - 1; c >= 0; --c) {
