@@ -12,7 +12,7 @@ import pytest
 
 import oracle_ffi as of
 from fixtures import random_batch
-from paper_2405_17363_b200 import (KERNEL_BLOCK, KERNEL_MULTI, KERNEL_THREAD, KERNEL_TMEM, Algo, BatchedSystem,
+from paper_2405_17363_b200 import (KERNEL_BLOCK, KERNEL_LATENCY, KERNEL_MULTI, KERNEL_THREAD, KERNEL_TMEM, Algo, BatchedSystem,
                                    DeviceSpec, InvalidGrouping, Mechanism, REGIME_C, REGIME_P, ReductionPlan,
                                    Strategy, StrategyConfig, UnsupportedMechanism)
 
@@ -87,8 +87,8 @@ def test_m156_bicg_bitwise_vs_reference(solver, m156, m156_batches, regime, kind
         assert st == 0
         assert_matches_reference(rep, rres, f"{regime} {kind} {k} vs reference")
     north_star_tolerances(rep, res)
-    if k == 1 or kind == Strategy.OneCell:  # one warp per cell: the TMEM kernel's pair schedule
-        assert rep.kernels & ~16 == KERNEL_TMEM, rep.kernels
+    if k == 1 or kind == Strategy.OneCell:  # 100 cells: latency mode (one CTA per cell); else the TMEM pair schedule
+        assert rep.kernels & ~16 in (KERNEL_TMEM, KERNEL_LATENCY), rep.kernels
 
 
 @pytest.mark.parametrize("regime", ["P", "C"])
@@ -115,8 +115,9 @@ def test_m156_bicgstab_bitwise_vs_oracle(solver, m156, m156_batches, regime, kin
         assert_matches_oracle(rep, rres, f"bicgstab {regime} {kind} {k} vs reference primitives")
     north_star_tolerances(rep, res)
     # Block-cells(k) groups up to 1024 rows run on the TMEM kernel (four-warp teams for the coupled ones)
-    want = {Strategy.MultiCells: KERNEL_MULTI, Strategy.ThreadPerCell: KERNEL_THREAD}.get(kind, KERNEL_TMEM)
-    assert rep.kernels & ~16 == want, (rep.kernels, want)  # the intended kernel ran (16 = LU fallback)
+    want = {Strategy.MultiCells: (KERNEL_MULTI,), Strategy.ThreadPerCell: (KERNEL_THREAD,)}.get(
+        kind, (KERNEL_TMEM, KERNEL_LATENCY))  # 100 cells of one-cell groups: latency mode
+    assert rep.kernels & ~16 in want, (rep.kernels, want)  # the intended kernel ran (16 = LU fallback)
     if regime == "C" and kind != Strategy.MultiCells:
         # converging regime, north-star criterion: every converged cell within
         # 1e-10 relative of the reference's dense LU (dense_lu.cpp:18-63).  A

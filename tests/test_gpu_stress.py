@@ -10,7 +10,7 @@ import pytest
 
 import oracle_ffi as of
 from fixtures import random_batch
-from paper_2405_17363_b200 import KERNEL_TMEM, Algo, BatchedSystem, DeviceSpec, Mechanism, Strategy, StrategyConfig
+from paper_2405_17363_b200 import KERNEL_LATENCY, KERNEL_TMEM, Algo, BatchedSystem, DeviceSpec, Mechanism, Strategy, StrategyConfig
 
 pytestmark = pytest.mark.gpu
 
@@ -38,8 +38,8 @@ def test_generated_mechanisms_every_grouping(solver, species, seed):
         for algo in (Algo.BICGSTAB_JACOBI, Algo.BICG):
             rep = check(solver, m.row_ptr, m.col_idx, v, b, k, algo, 1e-10, int(rng.integers(40, 400)))
             n = species * (k if k else 1024 // species)
-            if k == 1 and n >= 65:  # one-warp-per-cell shapes with an instance
-                assert rep.kernels & KERNEL_TMEM, (species, cells, k, algo, rep.kernels)
+            if k == 1 and n >= 65:  # one-cell groups with an instance: TMEM, or latency mode for small batches
+                assert rep.kernels & (KERNEL_TMEM | KERNEL_LATENCY), (species, cells, k, algo, rep.kernels)
 
 
 @pytest.mark.parametrize("seed", range(4))
