@@ -51,6 +51,8 @@ def main(tag):
         rows = ncu_csv("-i", rep, "--page", "raw", "--csv")
         h, u, v = rows[0], rows[1], rows[2]
         d = {h[i]: (u[i], v[i]) for i in range(len(h))}
+        instance = d.get("Kernel Name", ("", ""))[1]
+        lines.insert(3, f"# instance: {instance}")
         for k in KEYS:
             if k in d:
                 lines.append(f"{k:75s} {d[k][1]:>22s} {d[k][0]}")
@@ -84,11 +86,16 @@ def main(tag):
             "Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[metrics["dram__bytes_write.sum"][0]]
         with open(os.path.join(PROF, "ncu_block_cells_traffic.json"), "w") as f:
             pct = lambda k: float(metrics[k][1]) / 100.0 if k in metrics else None  # noqa: E731
-            json.dump({"kernel": "block_cells_tmem_kernel", "cells": 100000, "tag": tag,
+            json.dump({"kernel": "block_cells_tmem_kernel", "instance": instance, "algorithm": "bicgstab",
+                       "species": 156, "cells": 100000, "tag": tag,
                        "dram_bytes_per_launch_scaled": traffic,
                        "shared_pipe_frac": pct("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
                        "issue_active_frac": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                        "fp64_pipe_frac": pct("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                       "shared_ld_wavefronts": float(metrics.get("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+                                                                 ("", "0"))[1]),
+                       "shared_st_wavefronts": float(metrics.get("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum",
+                                                                 ("", "0"))[1]),
                        "note": "dram__bytes_read.sum + dram__bytes_write.sum of one launch on the bench workload "
                                "(100k M156 cells, P regime); compulsory bytes are 1.496e9; the *_frac are the same "
                                "capture's shared-memory pipe, issue and FP64 utilisation"}, f, indent=1)
