@@ -891,12 +891,14 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
     const int lu_dyn_max = kMaxDynSmem - static_cast<int>(fa.sharedSizeBytes);
     check_cuda(cudaFuncSetAttribute(bc::lu_fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_dyn_max),
                "cudaFuncSetAttribute(lu)");
-    // block-diagonal groups whose s x s block fits: factor it in shared memory
-    // (BC_LU_SMEM=0 keeps the scratch-resident path for A/B)
+    // BC_LU_SMEM=1: block-diagonal groups whose s x s block fits are factored in
+    // shared memory (one CTA per SM).  Measured slower than three scratch-resident
+    // CTAs per SM (B200, Block-cells(N) M156 P, 100k cells: 557 vs 384 ms):
+    // the kernel is bound by its serial chains, which more CTAs overlap.
     const size_t smem_blk = sizeof(int) * ((nmax + 1) & ~1) +
                             sizeof(double) * (nmax + std::max<int64_t>(pmax, static_cast<int64_t>(s) * s));
     const char* lue = std::getenv("BC_LU_SMEM");
-    const bool use_smem_block = blockdiag && smem_blk <= static_cast<size_t>(lu_dyn_max) && !(lue && *lue == '0');
+    const bool use_smem_block = blockdiag && smem_blk <= static_cast<size_t>(lu_dyn_max) && lue && *lue == '1';
     if (use_smem_block) smem = smem_blk;
     if (smem > static_cast<size_t>(lu_dyn_max)) fail(BC_ERR_INVALID_ARGUMENT, "LU fallback: group too large");
     for (size_t b0 = 0; b0 < ents.size(); b0 += batch) {

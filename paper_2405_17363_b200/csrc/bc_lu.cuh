@@ -104,13 +104,8 @@ constexpr int kLuTile = 64;  // A22 tile edge: 256 threads x (4 x 4) register mi
 __device__ bool lu_panel_warp(double* lu, const int n, int* perm, double* pbuf, const int k0, const int k1,
                               int* piv_out) {
     constexpr int LD = kLuPanel + 1;
-    const int lane = threadIdx.x;  // warp 0 only
+    const int lane = threadIdx.x;  // warp 0 only; the CTA loaded the panel into pbuf (lu_factor)
     const int K = k1 - k0, rows = n - k0;
-    for (int q = lane; q < rows * K; q += 32) {
-        const int r = q / K, c = q % K;
-        pbuf[r * LD + c] = lu[static_cast<int64_t>(k0 + r) * n + k0 + c];
-    }
-    __syncwarp();
     for (int kk = 0; kk < K; ++kk) {
         // dense_lu.cpp:32-41: largest magnitude in column k, ties to the lowest row
         const double a0 = fabs(pbuf[kk * LD + kk]);
@@ -161,11 +156,7 @@ __device__ bool lu_panel_warp(double* lu, const int n, int* perm, double* pbuf, 
         }
         __syncwarp();
     }
-    for (int q = lane; q < rows * K; q += 32) {
-        const int r = q / K, c = q % K;
-        lu[static_cast<int64_t>(k0 + r) * n + k0 + c] = pbuf[r * LD + c];
-    }
-    return true;
+    return true;  // the CTA writes pbuf back (lu_factor)
 }
 
 __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
@@ -184,12 +175,29 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
     for (int k0 = 0; k0 < n; k0 += kLuPanel) {
         const int k1 = min(n, k0 + kLuPanel);
         if (pbuf) {
+            // the panel (rows [k0, n) x columns [k0, k1)) into shared memory by the
+            // whole CTA -- warp 0 alone would expose one L2 round trip per row
+            {
+                const int K = k1 - k0, rows = n - k0;
+                for (int q = tid; q < rows * K; q += nt) {
+                    const int r = q / K, c = q % K;
+                    pbuf[r * (kLuPanel + 1) + c] = A(k0 + r, k0 + c);
+                }
+            }
+            __syncthreads();
             if (tid < 32) {
                 const bool ok = lu_panel_warp(lu, n, perm, pbuf, k0, k1, s_piv);
                 if (tid == 0 && !ok) s_singular = 1;
             }
             __syncthreads();
             if (s_singular) return false;
+            {
+                const int K = k1 - k0, rows = n - k0;
+                for (int q = tid; q < rows * K; q += nt) {
+                    const int r = q / K, c = q % K;
+                    A(k0 + r, k0 + c) = pbuf[r * (kLuPanel + 1) + c];
+                }
+            }
             // the panel's row swaps, in order, on the columns outside it
             for (int c = tid; c < n; c += nt) {
                 if (c >= k0 && c < k1) continue;
@@ -320,9 +328,37 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
 }
 
 // Forward substitution L y = P b (dense_lu.cpp:53-57) on y[] (shared, holding
-// P b): row i subtracts j = 0..i-1 in order, as a wavefront over j.
+// P b): row i subtracts j = 0..i-1 in order, as a wavefront over j.  Each
+// thread's row entries l_ij are read kLuFwdAhead steps ahead of use, so the
+// per-step cost is the barrier, not an L2 round trip.
+constexpr int kLuFwdAhead = 8;
 __device__ void lu_forward(const double* lu, const int n, double* y) {
     const int tid = threadIdx.x, nt = blockDim.x;
+    if (n <= nt) {  // one row per thread (every block-diagonal block and most groups)
+        const int i = tid;
+        const double* row = lu + static_cast<int64_t>(i < n ? i : 0) * n;
+        double win[kLuFwdAhead];
+#pragma unroll
+        for (int q = 0; q < kLuFwdAhead; ++q) win[q] = (i < n && q < i) ? row[q] : 0.0;
+        for (int j0 = 0; j0 < n; j0 += kLuFwdAhead) {
+            double nxt[kLuFwdAhead];
+#pragma unroll
+            for (int q = 0; q < kLuFwdAhead; ++q) {
+                const int j = j0 + kLuFwdAhead + q;
+                nxt[q] = (i < n && j < i) ? row[j] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < kLuFwdAhead; ++q) {
+                const int j = j0 + q;
+                __syncthreads();
+                if (j < n && i > j && i < n) y[i] = __dsub_rn(y[i], __dmul_rn(win[q], y[j]));
+            }
+#pragma unroll
+            for (int q = 0; q < kLuFwdAhead; ++q) win[q] = nxt[q];
+        }
+        __syncthreads();
+        return;
+    }
     for (int j = 0; j < n; ++j) {
         __syncthreads();
         const double xj = y[j];
@@ -341,22 +377,62 @@ __device__ bool lu_backward(const double* lu, const int n, double* x, double* sl
     __shared__ int s_negzero_sum;
     const int tid = threadIdx.x;
     if (tid < 32) {
+        // lane L owns columns j = L + 32q; the next row's entries (and its
+        // pivot, for lane 0) are loaded while lane 0 runs this row's chain
+        const int nq = (n + 31) / 32;  // columns per lane
         bool z = false;
-        for (int ii = n - 1; ii >= 0; --ii) {
+        double cur[8], nxt[8], dcur = 0.0, dnxt = 0.0;
+        auto load_row = [&](int ii, double (&dst)[8], double& dg) {
             const double* row = lu + static_cast<int64_t>(ii) * n;
-            for (int j = ii + 1 + tid; j < n; j += 32) slots[j] = __dmul_rn(row[j], x[j]);
-            __syncwarp();
-            if (tid == 0) {
-                double acc = x[ii];
-#pragma unroll 8
-                for (int j = ii + 1; j < n; ++j) acc = __dsub_rn(acc, slots[j]);
-                if (is_neg_zero(acc)) {
-                    z = true;
-                    if (later_neg) acc = 0.0;
-                }
-                x[ii] = __ddiv_rn(acc, row[ii]);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int j = tid + 32 * q;
+                dst[q] = (q < nq && j > ii && j < n) ? row[j] : 0.0;
             }
-            __syncwarp();
+            dg = tid == 0 ? row[ii] : 0.0;
+        };
+        if (nq <= 8) {
+            load_row(n - 1, cur, dcur);
+            for (int ii = n - 1; ii >= 0; --ii) {
+                if (ii > 0) load_row(ii - 1, nxt, dnxt);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int j = tid + 32 * q;
+                    if (q < nq && j > ii && j < n) slots[j] = __dmul_rn(cur[q], x[j]);
+                }
+                __syncwarp();
+                if (tid == 0) {
+                    double acc = x[ii];
+#pragma unroll 8
+                    for (int j = ii + 1; j < n; ++j) acc = __dsub_rn(acc, slots[j]);
+                    if (is_neg_zero(acc)) {
+                        z = true;
+                        if (later_neg) acc = 0.0;
+                    }
+                    x[ii] = __ddiv_rn(acc, dcur);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
+                dcur = dnxt;
+            }
+        } else {
+            for (int ii = n - 1; ii >= 0; --ii) {
+                const double* row = lu + static_cast<int64_t>(ii) * n;
+                for (int j = ii + 1 + tid; j < n; j += 32) slots[j] = __dmul_rn(row[j], x[j]);
+                __syncwarp();
+                if (tid == 0) {
+                    double acc = x[ii];
+#pragma unroll 8
+                    for (int j = ii + 1; j < n; ++j) acc = __dsub_rn(acc, slots[j]);
+                    if (is_neg_zero(acc)) {
+                        z = true;
+                        if (later_neg) acc = 0.0;
+                    }
+                    x[ii] = __ddiv_rn(acc, row[ii]);
+                }
+                __syncwarp();
+            }
         }
         if (tid == 0) s_negzero_sum = z;
     }

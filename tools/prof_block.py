@@ -17,7 +17,8 @@ v, b = m.newton_batch(0, cells, cells, reg.h)
 s = Solver(0)
 sysm = BatchedSystem(species, cells, m.row_ptr, m.col_idx, torch.from_numpy(v).cuda(), torch.from_numpy(b).cuda())
 for _ in range(int(os.environ.get("REPS", "1"))):
-    rep = s.solve_block_cells(sysm, int(os.environ.get("K", "1")), DeviceSpec(), reg.tol, reg.max_iter, algo=algo,
+    kk = os.environ.get("K", "1")
+    rep = s.solve_block_cells(sysm, None if kk == "N" else int(kk), DeviceSpec(), reg.tol, reg.max_iter, algo=algo,
                               timing=True)
     print(f"cells={cells} algo={algo.name} regime={reg.name} it_sum={rep.iterations_sum} "
           f"device_ms={rep.device_ms:.3f} -> {cells / rep.device_ms * 1e3:.0f} cell-solves/s", flush=True)
