@@ -60,13 +60,16 @@ struct MultiCtx {
     int P2;          // slots per value
 };
 
+// The gathered vector was written by other CTAs before the last grid.sync():
+// read it through L2 (ld.global.cg), never from a possibly stale L1 line --
+// under compute-sanitizer racecheck plain loads returned pre-sync values.
 __device__ __forceinline__ double mc_spmv_row(const MultiParams& p, int64_t i, const double* xin) {
     const int64_t c = i / p.species;
     const int r = static_cast<int>(i - c * p.species);
     const double* v = p.values + c * p.nnz;
     const double* xc = xin + c * p.species;
     double acc = 0.0;
-    for (int e = p.row_ptr[r]; e < p.row_ptr[r + 1]; ++e) acc = dadd(acc, dmul(v[e], xc[p.col_idx[e]]));
+    for (int e = p.row_ptr[r]; e < p.row_ptr[r + 1]; ++e) acc = dadd(acc, dmul(v[e], __ldcg(xc + p.col_idx[e])));
     return acc;
 }
 
@@ -76,7 +79,8 @@ __device__ __forceinline__ double mc_spmvt_row(const MultiParams& p, int64_t j, 
     const double* v = p.values + c * p.nnz;
     const double* xc = xin + c * p.species;
     double acc = 0.0;
-    for (int q = p.trow_ptr[lc]; q < p.trow_ptr[lc + 1]; ++q) acc = dadd(acc, dmul(v[p.tval[q]], xc[p.trow[q]]));
+    for (int q = p.trow_ptr[lc]; q < p.trow_ptr[lc + 1]; ++q)
+        acc = dadd(acc, dmul(v[p.tval[q]], __ldcg(xc + p.trow[q])));
     return acc;
 }
 

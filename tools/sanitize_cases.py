@@ -50,6 +50,12 @@ def run(name):
         np.array_equal(np.asarray(rep.per_block_iterations), res.iters)
     print(f"{name}: kernels={rep.kernels} fallbacks={rep.breakdown_fallbacks} bitwise={'yes' if ok else 'NO'}",
           flush=True)
+    if not ok and st == 0:
+        xg = np.asarray(rep.per_cell_x)
+        bad = (of.bits(xg) != of.bits(res.x))
+        print(f"  x mismatches {int(bad.sum())} of {bad.size}; iterations gpu {list(rep.per_block_iterations)[:4]} "
+              f"oracle {list(res.iters)[:4]}; max rel {float(np.abs(xg - res.x).max() / np.abs(res.x).max()):.3e}",
+              flush=True)
     s.close()
     return ok
 
