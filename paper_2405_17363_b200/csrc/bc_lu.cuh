@@ -167,7 +167,8 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
     __shared__ double s_ut[kLuPanel][kLuTile];      // U12 tile (panel x cols)
     static_assert(kLuTile == 64, "the A22 micro-tiling below assumes 256 threads on a 64 x 64 tile");
     const int tid = threadIdx.x, nt = blockDim.x;
-    auto A = [&](int i, int j) -> double& { return lu[static_cast<int64_t>(i) * n + j]; };
+    // n <= 2048 (kMaxGroupRows): 32-bit element offsets
+    auto A = [&](int i, int j) -> double& { return lu[i * n + j]; };
     if (tid == 0) s_singular = 0;
     __syncthreads();
 
@@ -272,12 +273,27 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
             }
         }
         if (k1 == n) break;
-        // U12: rows [k0, k1), columns [k1, n): a_ij -= l_ik u_kj for k = k0 .. i-1
-        for (int j = k1 + tid; j < n; j += nt)
-            for (int k = k0; k < k1; ++k) {
-                const double ukj = A(k, j);
-                for (int i = k + 1; i < k1; ++i) A(i, j) = __dsub_rn(A(i, j), __dmul_rn(A(i, k), ukj));
+        // U12: rows [k0, k1), columns [k1, n): a_ij -= l_ik u_kj for k = k0 .. i-1,
+        // one column per thread held in registers (L11 from the panel buffer)
+        {
+            const int K = k1 - k0;
+            for (int j = k1 + tid; j < n; j += nt) {
+                double u[kLuPanel];
+#pragma unroll
+                for (int i = 0; i < kLuPanel; ++i) u[i] = i < K ? A(k0 + i, j) : 0.0;
+#pragma unroll
+                for (int k = 0; k < kLuPanel; ++k)
+#pragma unroll
+                    for (int i = k + 1; i < kLuPanel; ++i)
+                        if (i < K) {
+                            const double l = pbuf ? pbuf[i * (kLuPanel + 1) + k] : A(k0 + i, k0 + k);
+                            u[i] = __dsub_rn(u[i], __dmul_rn(l, u[k]));
+                        }
+#pragma unroll
+                for (int i = 1; i < kLuPanel; ++i)
+                    if (i < K) A(k0 + i, j) = u[i];
             }
+        }
         __syncthreads();
         // A22: rows and columns [k1, n), the panel's updates in ascending k per element
         const int K = k1 - k0, m = n - k1, tiles = (m + kLuTile - 1) / kLuTile;
@@ -293,15 +309,23 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
             // thread (tr, tc) owns rows 4tr..4tr+3 and columns tc + 16q of the tile; per
             // element the panel's updates still run one k at a time in ascending order
             const int tr = tid / 16, tc = tid % 16;
+            const bool interior = i0 + kLuTile <= n && j0 + kLuTile <= n;
             if (tid < 256) {
                 double a[4][4];
+                if (interior) {
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                    for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int r = i0 + 4 * tr + i, cc = j0 + tc + 16 * q;
-                        a[i][q] = (r < n && cc < n) ? A(r, cc) : 0.0;
-                    }
+                        for (int q = 0; q < 4; ++q) a[i][q] = A(i0 + 4 * tr + i, j0 + tc + 16 * q);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int r = i0 + 4 * tr + i, cc = j0 + tc + 16 * q;
+                            a[i][q] = (r < n && cc < n) ? A(r, cc) : 0.0;
+                        }
+                }
                 for (int kk = 0; kk < K; ++kk) {
                     double l[4], u[4];
 #pragma unroll
@@ -313,13 +337,20 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
 #pragma unroll
                         for (int q = 0; q < 4; ++q) a[i][q] = __dsub_rn(a[i][q], __dmul_rn(l[i], u[q]));
                 }
+                if (interior) {
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                    for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int r = i0 + 4 * tr + i, cc = j0 + tc + 16 * q;
-                        if (r < n && cc < n) A(r, cc) = a[i][q];
-                    }
+                        for (int q = 0; q < 4; ++q) A(i0 + 4 * tr + i, j0 + tc + 16 * q) = a[i][q];
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int r = i0 + 4 * tr + i, cc = j0 + tc + 16 * q;
+                            if (r < n && cc < n) A(r, cc) = a[i][q];
+                        }
+                }
             }
             __syncthreads();
         }
