@@ -107,7 +107,8 @@ typedef struct {
 } bc_report;
 
 enum {
-    BC_KERNEL_TMEM = 1,   /* block_cells_tmem_kernel (Jacobi-BiCGSTAB, one warp per group, TMEM operands) */
+    BC_KERNEL_TMEM = 1,   /* block_cells_tmem_kernel (both algorithms; one warp or a 2/4-warp team per group,
+                             TMEM operands) */
     BC_KERNEL_BLOCK = 2,  /* block_cells_kernel (BiCG / wide groups, shared-memory operands) */
     BC_KERNEL_MULTI = 4,  /* multi_cells_kernel (cooperative, grid-wide reductions) */
     BC_KERNEL_THREAD = 8, /* thread_per_cell_kernel (+ interleave_kernel) */

@@ -9,16 +9,19 @@
  * /root/reference/proj/core) with identical floating-point operation order,
  * so that, compiled with -ffp-contract=off on x86-64 (SSE2 doubles, no FMA),
  * it is bit-identical to the reference.  That claim is pinned by
- * tests/test_oracle_vs_reference.py against oracle/_ref (the reference
- * compiled from its own sources) and by the committed golden fixtures in
- * tests/golden/.
+ * tests/test_oracle.py against oracle/_ref (the reference compiled from its
+ * own sources; for BICGSTAB_JACOBI, the same algorithm composed from the
+ * reference's primitives, oracle/ref_bicgstab.cpp) and by the committed
+ * golden fixtures in tests/golden/.
  *
  * BICGSTAB_JACOBI has no reference implementation: it is
  * defined here, using the reference's primitives (spmv, axpby-style updates,
  * the stride-halving tree reduction, RMS convergence with fresh-residual
- * confirmation, the 1e-300 breakdown floor).  Its primitives are pinned
- * through the BiCG parity above; the algorithm itself is cross-checked
- * against the reference's dense LU (lu_solve) on converging systems.
+ * confirmation, the 1e-300 breakdown floor).  It is pinned bitwise against
+ * the same algorithm composed from the reference's compiled spmv / axpby /
+ * plan_reduce_map / lu_solve and strategy drivers (oracle/ref_bicgstab.cpp),
+ * and cross-checked against the reference's dense LU (lu_solve) on
+ * converging systems.
  */
 #ifndef BC_ORACLE_H
 #define BC_ORACLE_H

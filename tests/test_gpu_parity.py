@@ -96,9 +96,11 @@ def test_m156_bicg_bitwise_vs_reference(solver, m156, m156_batches, regime, kind
                                     (Strategy.BlockCells, 4), (Strategy.MultiCells, None),
                                     (Strategy.ThreadPerCell, None)])
 def test_m156_bicgstab_bitwise_vs_oracle(solver, m156, m156_batches, regime, kind, k):
-    if kind == Strategy.MultiCells and regime == "P":
-        pytest.skip("a Multi-cells breakdown makes the CPU checker densify a 15600^2 system for its LU")
     reg, v, b = m156_batches[regime]
+    if kind == Strategy.MultiCells and regime == "P":
+        # a breakdown makes the checker densify the whole system for its LU: 10
+        # cells (1,560 rows, the device's dense-LU path) keep that to seconds
+        v, b = np.ascontiguousarray(v[:10]), np.ascontiguousarray(b[:10])
     sysm = system_of(m156.row_ptr, m156.col_idx, v, b)
     rep = run_gpu(solver, sysm, kind, k, Algo.BICGSTAB_JACOBI, reg.tol, reg.max_iter)
     kk = 0 if k is None else k
@@ -126,9 +128,9 @@ def test_m156_bicgstab_bitwise_vs_oracle(solver, m156, m156_batches, regime, kin
         # worst 1.05e-10 on this batch, CPU-measured with the same bits)
         x = np.asarray(rep.per_cell_x)
         k_eff = 1 if kind in (Strategy.OneCell, Strategy.ThreadPerCell) else int(rep.cells_per_block)
-        flags = np.repeat(np.asarray(rep.per_block_flags), k_eff)[:100]
+        flags = np.repeat(np.asarray(rep.per_block_flags), k_eff)[:len(v)]
         checked = 0
-        for c in range(100):
+        for c in range(len(v)):
             if not flags[c] & 1:
                 continue
             st, xl = of.lu_solve("ref" if of.have_ref() else "orc", m156.row_ptr, m156.col_idx, v[c], b[c])
