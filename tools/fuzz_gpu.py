@@ -2,9 +2,11 @@
     python tools/fuzz_gpu.py [seconds] [seed]
 Each case draws a mechanism (generated, or a random diagonally dominant
 pattern), a batch size, a strategy (Block-cells(k) / (N), One-cell, Multi-cells,
-thread-per-cell), an algorithm and solver settings, solves it through the
-public API and compares x, iterations, residuals and flags bit for bit with
-the C oracle (tests/oracle_ffi.py).  Prints one line per case and a summary;
+thread-per-cell), an algorithm and solver settings, a kernel policy (latency
+mode forced on / off / default) and a front end (one Solver, or a DeviceSet
+listing GPU 0 two or three times), solves it through the public API and
+compares x, iterations, residuals and flags bit for bit with the C oracle
+(tests/oracle_ffi.py).  Prints one line per case and a summary;
 exit status 1 on any mismatch."""
 import os
 import sys
@@ -17,8 +19,8 @@ import numpy as np  # noqa: E402
 
 import oracle_ffi as of  # noqa: E402
 from fixtures import random_batch  # noqa: E402
-from paper_2405_17363_b200 import (Algo, BatchedSystem, DeviceSpec, Mechanism, Solver, Strategy,  # noqa: E402
-                                   StrategyConfig)
+from paper_2405_17363_b200 import (Algo, BatchedSystem, DeviceSet, DeviceSpec, Mechanism, Solver,  # noqa: E402
+                                   Strategy, StrategyConfig)
 
 STRAT_ORC = {Strategy.OneCell: 0, Strategy.MultiCells: 1, Strategy.BlockCells: 2, Strategy.ThreadPerCell: 0}
 
@@ -67,16 +69,26 @@ def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 600.0
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
     solver = Solver(0)
+    sets = {2: DeviceSet([0, 0]), 3: DeviceSet([0, 0, 0])}
     t0, n, bad = time.time(), 0, 0
     while time.time() - t0 < budget:
         src, rp, ci, v, b, kind, k, algo, tol, max_iter = case(rng)
         species, cells = len(rp) - 1, v.shape[0]
-        label = f"{src} cells={cells} {kind.name}({k}) {algo.name} tol={tol:g} it={max_iter}"
+        lat = str(rng.choice(["default", "default", "1", "0"]))
+        front = int(rng.choice([1, 1, 2, 3]))
+        if lat == "default":
+            os.environ.pop("BC_LATENCY", None)
+        else:
+            os.environ["BC_LATENCY"] = lat
+        label = (f"{src} cells={cells} {kind.name}({k}) {algo.name} tol={tol:g} it={max_iter} latency={lat} "
+                 f"devices={front}")
         st, res = of.orc_solve_batch(STRAT_ORC[kind], int(algo), 0 if k is None else k, rp, ci, v, b, tol, max_iter,
                                      workers=16)
         try:
-            rep = solver.run_strategy(BatchedSystem(species, cells, rp, ci, v, b), StrategyConfig(kind, k),
-                                      DeviceSpec(), tol, max_iter, 1, algo)
+            api = solver if front == 1 else sets[front]
+            rep = api.run_strategy(BatchedSystem(species, cells, rp, ci, v, b), StrategyConfig(kind, k),
+                                   DeviceSpec(), tol, max_iter, 1, algo)
+            label += f" kernels={rep.kernels}"
             err = None
         except Exception as e:  # noqa: BLE001
             err = type(e).__name__
