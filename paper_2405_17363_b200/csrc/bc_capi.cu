@@ -883,8 +883,9 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
     // panels in shared memory while a panel of the largest factored matrix fits in 48 KB
     const int64_t prow = blockdiag ? s : nmax;
     const int panel_rows = prow * (bc::kLuPanel + 1) * 8 <= 48 * 1024 ? static_cast<int>(prow) : 0;
+    // [panel] perm | sum (n) | ycopy (n) | slots (max(padded n, n, 8 warps x species))
     size_t smem = sizeof(double) * panel_rows * (bc::kLuPanel + 1) + sizeof(int) * ((nmax + 1) & ~1) +
-                  sizeof(double) * (nmax + std::max(pmax, nmax));
+                  sizeof(double) * (2 * nmax + std::max<int64_t>(std::max(pmax, nmax), 8 * s));
     // opt in above 48 KB of static + dynamic shared memory (per device: set on every call)
     cudaFuncAttributes fa{};
     check_cuda(cudaFuncGetAttributes(&fa, bc::lu_fallback_kernel), "cudaFuncGetAttributes(lu)");
@@ -896,7 +897,7 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
     // CTAs per SM (B200, Block-cells(N) M156 P, 100k cells: 557 vs 384 ms):
     // the kernel is bound by its serial chains, which more CTAs overlap.
     const size_t smem_blk = sizeof(int) * ((nmax + 1) & ~1) +
-                            sizeof(double) * (nmax + std::max<int64_t>(pmax, static_cast<int64_t>(s) * s));
+                            sizeof(double) * (2 * nmax + std::max<int64_t>(pmax, static_cast<int64_t>(s) * s));
     const char* lue = std::getenv("BC_LU_SMEM");
     const bool use_smem_block = blockdiag && smem_blk <= static_cast<size_t>(lu_dyn_max) && lue && *lue == '1';
     if (use_smem_block) smem = smem_blk;

@@ -471,6 +471,52 @@ __device__ bool lu_backward(const double* lu, const int n, double* x, double* sl
     return s_negzero_sum != 0;
 }
 
+// lu_backward for one warp (any warp of the CTA) on one block, with the
+// block's own product slots: returns (warp-uniform) whether some row summed
+// to -0 -- the case where a later block's negative x would have flipped it
+// (block-diagonal mode runs every block's chain at once with later_neg
+// false, then redoes the rare blocks where that guess was wrong).
+__device__ bool lu_backward_warp(const double* lu, const int n, double* x, double* slots, const bool later_neg) {
+    const int lane = threadIdx.x % 32;
+    const int nq = (n + 31) / 32;
+    bool z = false;
+    double cur[8], nxt[8], dcur = 0.0, dnxt = 0.0;
+    auto load_row = [&](int ii, double (&dst)[8], double& dg) {
+        const double* row = lu + static_cast<int64_t>(ii) * n;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int j = lane + 32 * q;
+            dst[q] = (q < nq && j > ii && j < n) ? row[j] : 0.0;
+        }
+        dg = lane == 0 ? row[ii] : 0.0;
+    };
+    load_row(n - 1, cur, dcur);
+    for (int ii = n - 1; ii >= 0; --ii) {
+        if (ii > 0) load_row(ii - 1, nxt, dnxt);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int j = lane + 32 * q;
+            if (q < nq && j > ii && j < n) slots[j] = __dmul_rn(cur[q], x[j]);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            double acc = x[ii];
+#pragma unroll 8
+            for (int j = ii + 1; j < n; ++j) acc = __dsub_rn(acc, slots[j]);
+            if (is_neg_zero(acc)) {
+                z = true;
+                if (later_neg) acc = 0.0;
+            }
+            x[ii] = __ddiv_rn(acc, dcur);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
+        dcur = dnxt;
+    }
+    return __shfl_sync(0xffffffffu, z ? 1 : 0, 0) != 0;
+}
+
 // Scatter cells [c0, c0 + cells) of the group into the zeroed dense matrix
 // `lu` (row length ld): dense_lu.cpp:8-16 on the block-diagonal matrix.
 __device__ void lu_densify(double* lu, const int ld, const double* vals, const int32_t* row_ptr,
@@ -504,7 +550,8 @@ __global__ void __launch_bounds__(256, 3) lu_fallback_kernel(const LuParams p) {
     }
     int* perm = reinterpret_cast<int*>(base);
     double* sum = reinterpret_cast<double*>(base + sizeof(int) * ((n + 1) & ~1));
-    double* slots = sum + n;  // >= padded length (also used for products)
+    double* ycopy = sum + n;  // block-diagonal mode: the forward results, for the rare backward redo
+    double* slots = ycopy + n;  // >= max(padded length, 8 * species) (also used for products)
     double* sblk = p.smem_block ? slots : nullptr;
     const int tid = threadIdx.x, nt = blockDim.x;
     const double* vals = p.values + ent.cell0 * p.nnz;
@@ -555,14 +602,38 @@ __global__ void __launch_bounds__(256, 3) lu_fallback_kernel(const LuParams p) {
                 for (int q = tid; q < s * s; q += nt) gblk[q] = sblk[q];
             __syncthreads();
         }
-        bool later_neg = false;
-        for (int c = ent.kc - 1; c >= 0; --c) {
-            double* xc = sum + c * s;
-            lu_backward(lu + static_cast<int64_t>(c) * s * s, s, xc, slots, later_neg);
-            int neg = 0;
-            for (int i = tid; i < s; i += nt) neg |= signbit(xc[i]) ? 1 : 0;
-            later_neg = __syncthreads_or(neg) || later_neg;
+        // Backward substitutions of all blocks at once, one warp per block, each
+        // assuming no later block has a negative x (later_neg false); then, in
+        // the reference's order (last block first), the rare block that summed a
+        // row to -0 while a later x is negative is redone from its forward result.
+        __shared__ unsigned s_zmask[64];  // kc <= kMaxGroupRows / 1
+        for (int i = tid; i < 64; i += nt) s_zmask[i] = 0u;
+        for (int i = tid; i < n; i += nt) ycopy[i] = sum[i];
+        __syncthreads();
+        {
+            const int warp = tid / 32, nw = nt / 32;
+            for (int c = warp; c < ent.kc; c += nw) {
+                const bool z = lu_backward_warp(lu + static_cast<int64_t>(c) * s * s, s, sum + c * s,
+                                                slots + warp * s, false);
+                if (z && (tid % 32) == 0) atomicOr(&s_zmask[c / 32], 1u << (c % 32));
+            }
         }
+        __syncthreads();
+        if (tid < 32) {
+            bool later_neg = false;
+            for (int c = ent.kc - 1; c >= 0; --c) {
+                double* xc = sum + c * s;
+                if (later_neg && (s_zmask[c / 32] >> (c % 32) & 1u)) {
+                    for (int i = tid; i < s; i += 32) xc[i] = ycopy[c * s + i];
+                    __syncwarp();
+                    lu_backward_warp(lu + static_cast<int64_t>(c) * s * s, s, xc, slots, true);
+                }
+                int neg = 0;
+                for (int i = tid; i < s; i += 32) neg |= signbit(xc[i]) ? 1 : 0;
+                later_neg = __any_sync(0xffffffffu, neg) || later_neg;
+            }
+        }
+        __syncthreads();
         int nonfinite = 0;
         for (int i = tid; i < n; i += nt) nonfinite |= !isfinite(sum[i]);
         if (__syncthreads_or(nonfinite)) {
