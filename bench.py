@@ -563,8 +563,9 @@ def main_b200(args):
         if args.algo == "bicgstab":
             env["BLOCKCELLS_B200_ALGO"] = "bicgstab"
         try:
-            r = subprocess.run([exe, str(cells), str(max(1, min(args.steps, 5))), "1", str(n)], env=env,
-                               capture_output=True, text=True, timeout=900)
+            r = subprocess.run([exe, str(cells), str(max(1, min(args.steps, 5))), "1", str(n), repr(reg.h),
+                                repr(reg.tol), str(reg.max_iter)], env=env, capture_output=True, text=True,
+                               timeout=900)
             if r.returncode == 0:
                 dropin = json.loads(r.stdout.strip().splitlines()[-1])
                 dropin["h2d_bytes_per_step"] = dropin.pop("input_bytes_per_step")

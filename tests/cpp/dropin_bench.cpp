@@ -10,7 +10,7 @@
 // realistic conditions over the global cell index, P regime) from
 // libbc_workload.  Prints one JSON line.  Algorithm: BLOCKCELLS_B200_ALGO
 // (bicgstab | unset = BiCG); devices: BLOCKCELLS_B200_DEVICES (shim).
-//   dropin_bench <cells> <steps> <warmup> [species] [workers]
+//   dropin_bench <cells> <steps> <warmup> [species] [h] [tol] [max_iter] [workers]
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -26,14 +26,17 @@ int main(int argc, char** argv) {
     const int steps = argc > 2 ? atoi(argv[2]) : 5;
     const int warmup = argc > 3 ? atoi(argv[3]) : 2;
     const int species = argc > 4 ? atoi(argv[4]) : 156;
-    const std::size_t workers = argc > 5 ? static_cast<std::size_t>(atol(argv[5])) : 0;
+    const double h = argc > 5 ? atof(argv[5]) : 120.0;        // P regime by default (bench.hpp:20)
+    const double tol = argc > 6 ? atof(argv[6]) : 1e-30;
+    const std::size_t max_iter = argc > 7 ? static_cast<std::size_t>(atol(argv[7])) : 1000;
+    const std::size_t workers = argc > 8 ? static_cast<std::size_t>(atol(argv[8])) : 0;
     bcw_mechanism* m = nullptr;
     if (bcw_mechanism_create(species, 3 * species, 0, &m) != 0) return 2;
     const long nnz = bcw_nnz(m);
     std::vector<int32_t> rp(species + 1), ci(nnz);
     bcw_pattern(m, rp.data(), ci.data());
     std::vector<double> vals(static_cast<size_t>(cells) * nnz), rhs(static_cast<size_t>(cells) * species);
-    if (bcw_newton_batch(m, 0, cells, cells, 1, 120.0, nullptr, nullptr, vals.data(), rhs.data(), 0) != 0) return 3;
+    if (bcw_newton_batch(m, 0, cells, cells, 1, h, nullptr, nullptr, vals.data(), rhs.data(), 0) != 0) return 3;
     BatchedSystem sys;
     sys.species = species;
     sys.cells = cells;
@@ -58,7 +61,7 @@ int main(int argc, char** argv) {
     std::size_t it_sum = 0, fallbacks = 0;
     for (int i = 0; i < warmup + steps; ++i) {
         const auto t0 = std::chrono::steady_clock::now();
-        const SolveReport r = run_strategy(sys, cfg, DeviceSpec{}, 1e-30, 1000, workers);
+        const SolveReport r = run_strategy(sys, cfg, DeviceSpec{}, tol, max_iter, workers);
         const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (i >= warmup) {
             total += dt;
@@ -69,11 +72,11 @@ int main(int argc, char** argv) {
     }
     const char* algo = std::getenv("BLOCKCELLS_B200_ALGO");
     std::printf("{\"cells\": %ld, \"species\": %d, \"steps\": %d, \"warmup\": %d, \"algorithm\": \"%s\", "
-                "\"value\": %.3f, \"unit\": \"cell-solves/s\", \"ms_per_step\": %.3f, "
+                "\"h\": %g, \"tol\": %g, \"max_iter\": %zu, \"value\": %.3f, \"unit\": \"cell-solves/s\", \"ms_per_step\": %.3f, "
                 "\"report_wall_ms_per_step\": %.3f, \"iterations_sum\": %zu, \"breakdown_fallbacks\": %zu, "
                 "\"entry\": \"blockcells::run_strategy (strategies.hpp:80-82) over the drop-in shim\", "
                 "\"input_bytes_per_step\": %ld}\n",
-                cells, species, steps, warmup, algo ? algo : "bicg", cells * steps / total, 1e3 * total / steps,
+                cells, species, steps, warmup, algo ? algo : "bicg", h, tol, max_iter, cells * steps / total, 1e3 * total / steps,
                 1e3 * rep_total / steps, it_sum, fallbacks, static_cast<long>(cells) * (nnz + species) * 8);
     bcw_mechanism_destroy(m);
     return 0;
