@@ -1026,7 +1026,10 @@ MultiResult run_multi(bc_ctx* ctx, const bc::Pattern& pat, const int32_t* d_rp, 
     p.out_flags = reinterpret_cast<int32_t*>(ctx->m_out.as<char>() + 16);
     int P2 = 256;
     while (P2 < max_len) P2 <<= 1;
-    const size_t smem = sizeof(double) * 2 * P2;
+    // two staging areas for the cells an interval's rows gather from (bc_multi.cuh mc_stage)
+    const int64_t span = (max_len + 2 * static_cast<int64_t>(pat.species) - 2) / pat.species * pat.species;
+    p.stage_len = 2 * span * 8 + 2 * P2 * 8 <= 160 * 1024 ? static_cast<int>(span) : 0;
+    const size_t smem = sizeof(double) * (2 * P2 + 2 * static_cast<size_t>(p.stage_len));
     check_cuda(cudaFuncSetAttribute(bc::multi_cells_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)), "cudaFuncSetAttribute(multi)");
     int per_sm = 0;

@@ -49,6 +49,7 @@ struct MultiParams {
     int64_t* out_iters;
     double* out_rms;
     int32_t* out_flags;
+    int stage_len;            // doubles per staging area (2 areas after the slots), 0 = none
 };
 
 namespace cgm = cooperative_groups;
@@ -58,44 +59,79 @@ struct MultiCtx {
     double* slots;   // 2 * pow2(max_len) doubles (dynamic smem)
     double* red;     // small smem for broadcasts
     int P2;          // slots per value
+    double* stage;   // 2 * stage_len doubles after the slots: gathered vectors of an interval's cells
 };
 
-// The gathered vector was written by other CTAs before the last grid.sync():
-// read it through L2 (ld.global.cg), never from a possibly stale L1 line --
-// under compute-sanitizer racecheck plain loads returned pre-sync values.
-__device__ __forceinline__ double mc_spmv_row(const MultiParams& p, int64_t i, const double* xin) {
+// The gathered vectors were written by other CTAs before the last grid sync.
+// An interval's rows only gather from their own cells (the system is block
+// diagonal), so those cells' entries are staged into shared memory with
+// coherent L2 reads (ld.global.cg, coalesced) and gathered from there; a
+// plain L1-cached gather could return a line cached before the sync (under
+// compute-sanitizer racecheck it did).  Returns the vector index of
+// stage[0], or -1 when the cells do not fit (the row then reads through L2).
+__device__ int64_t mc_stage(const MultiCtx& m, int area, const double* xin, int64_t r0, int64_t r1) {
+    const MultiParams& p = *m.p;
+    const int64_t c0 = r0 / p.species, c1 = (r1 - 1) / p.species;
+    const int64_t base = c0 * p.species, cnt = (c1 - c0 + 1) * p.species;
+    if (cnt > p.stage_len) return -1;
+    double* st = m.stage + static_cast<int64_t>(area) * p.stage_len;
+    __syncthreads();  // the previous interval's gathers are done
+    for (int64_t q = threadIdx.x; q < cnt; q += blockDim.x) st[q] = __ldcg(xin + base + q);
+    __syncthreads();
+    return base;
+}
+
+// Row i of A x (csr.cpp:90-101) / of A^T x (csr.cpp:129-142): x from the
+// staged copy (off >= 0, see mc_stage) or through L2.
+__device__ __forceinline__ double mc_spmv_row(const MultiCtx& m, int area, int64_t off, int64_t i,
+                                              const double* xin) {
+    const MultiParams& p = *m.p;
     const int64_t c = i / p.species;
     const int r = static_cast<int>(i - c * p.species);
     const double* v = p.values + c * p.nnz;
-    const double* xc = xin + c * p.species;
     double acc = 0.0;
-    for (int e = p.row_ptr[r]; e < p.row_ptr[r + 1]; ++e) acc = dadd(acc, dmul(v[e], __ldcg(xc + p.col_idx[e])));
+    if (off >= 0) {
+        const double* xc = m.stage + static_cast<int64_t>(area) * p.stage_len + (c * p.species - off);
+        for (int e = p.row_ptr[r]; e < p.row_ptr[r + 1]; ++e) acc = dadd(acc, dmul(v[e], xc[p.col_idx[e]]));
+    } else {
+        const double* xc = xin + c * p.species;
+        for (int e = p.row_ptr[r]; e < p.row_ptr[r + 1]; ++e)
+            acc = dadd(acc, dmul(v[e], __ldcg(xc + p.col_idx[e])));
+    }
     return acc;
 }
 
-__device__ __forceinline__ double mc_spmvt_row(const MultiParams& p, int64_t j, const double* xin) {
+__device__ __forceinline__ double mc_spmvt_row(const MultiCtx& m, int area, int64_t off, int64_t j,
+                                               const double* xin) {
+    const MultiParams& p = *m.p;
     const int64_t c = j / p.species;
     const int lc = static_cast<int>(j - c * p.species);
     const double* v = p.values + c * p.nnz;
-    const double* xc = xin + c * p.species;
     double acc = 0.0;
-    for (int q = p.trow_ptr[lc]; q < p.trow_ptr[lc + 1]; ++q)
-        acc = dadd(acc, dmul(v[p.tval[q]], __ldcg(xc + p.trow[q])));
+    if (off >= 0) {
+        const double* xc = m.stage + static_cast<int64_t>(area) * p.stage_len + (c * p.species - off);
+        for (int q = p.trow_ptr[lc]; q < p.trow_ptr[lc + 1]; ++q) acc = dadd(acc, dmul(v[p.tval[q]], xc[p.trow[q]]));
+    } else {
+        const double* xc = xin + c * p.species;
+        for (int q = p.trow_ptr[lc]; q < p.trow_ptr[lc + 1]; ++q)
+            acc = dadd(acc, dmul(v[p.tval[q]], __ldcg(xc + p.trow[q])));
+    }
     return acc;
 }
 
 // Partials of NV per-row values over this CTA's intervals: slot value of row
 // i comes from f(i, v); tree in shared memory; partials[b*2+v].
 template <int NV, class F>
-__device__ void mc_block_partials(const MultiCtx& m, F&& f) {
+__device__ void mc_block_partials(const MultiCtx& m, F&& f, const double* xin = nullptr) {
     const MultiParams& p = *m.p;
     for (int64_t b = blockIdx.x; b < p.n_blocks; b += gridDim.x) {
         const int64_t b0 = p.ranges[2 * b], len = p.ranges[2 * b + 1] - b0;
+        const int64_t off = xin ? mc_stage(m, 0, xin, b0, b0 + len) : -1;  // f's SpMV gathers (fresh residual)
         int P = 1;
         while (P < len) P <<= 1;
         for (int q = threadIdx.x; q < P; q += blockDim.x)
 #pragma unroll
-            for (int v = 0; v < NV; ++v) m.slots[v * m.P2 + q] = q < len ? f(b0 + q, v) : 0.0;
+            for (int v = 0; v < NV; ++v) m.slots[v * m.P2 + q] = q < len ? f(b0 + q, v, off) : 0.0;
         for (int stride = P / 2; stride >= 1; stride /= 2) {
             __syncthreads();
             for (int q = threadIdx.x; q < stride; q += blockDim.x)
@@ -143,6 +179,14 @@ __device__ void mc_combine(const MultiCtx& m, double (&tot)[NV]) {
     __syncthreads();
 }
 
+// grid.sync() then a gpu-scope acquire fence: the next phase's plain loads of
+// vectors other CTAs wrote must not hit a stale L1 line (compute-sanitizer
+// racecheck's execution exposed exactly that without the fence).
+__device__ __forceinline__ void mc_sync(cgm::grid_group& grid) {
+    grid.sync();
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
 template <class F>
 __device__ __forceinline__ void mc_rows(const MultiParams& p, F&& f) {
     // rows of this CTA's intervals (so reductions never wait on other CTAs)
@@ -150,15 +194,27 @@ __device__ __forceinline__ void mc_rows(const MultiParams& p, F&& f) {
         for (int64_t i = p.ranges[2 * b] + threadIdx.x; i < p.ranges[2 * b + 1]; i += blockDim.x) f(i);
 }
 
+// The same, with the interval's cells of x0 (and x1) staged first: f(i, off0, off1).
+template <class F>
+__device__ __forceinline__ void mc_rows_x(const MultiCtx& m, const double* x0, const double* x1, F&& f) {
+    const MultiParams& p = *m.p;
+    for (int64_t b = blockIdx.x; b < p.n_blocks; b += gridDim.x) {
+        const int64_t r0 = p.ranges[2 * b], r1 = p.ranges[2 * b + 1];
+        const int64_t off0 = mc_stage(m, 0, x0, r0, r1);
+        const int64_t off1 = x1 ? mc_stage(m, 1, x1, r0, r1) : -1;
+        for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) f(i, off0, off1);
+    }
+}
+
 // fresh residual: sqrt(plan_reduce((b - A x)^2) / n)  (bicg.cpp:61-72)
 __device__ double mc_fresh_rms(const MultiCtx& m, cgm::grid_group& grid) {
     const MultiParams& p = *m.p;
-    grid.sync();  // x complete
-    mc_block_partials<1>(m, [&](int64_t i, int) {
-        const double ri = dsub(p.rhs[i], mc_spmv_row(p, i, p.x));
+    mc_sync(grid);  // x complete
+    mc_block_partials<1>(m, [&](int64_t i, int, int64_t off) {
+        const double ri = dsub(p.rhs[i], mc_spmv_row(m, 0, off, i, p.x));
         return dmul(ri, ri);
-    });
-    grid.sync();
+    }, p.x);
+    mc_sync(grid);
     double t[1];
     mc_combine<1>(m, t);
     return __dsqrt_rn(ddiv(t[0], static_cast<double>(p.n)));
@@ -175,6 +231,7 @@ __global__ void __launch_bounds__(256) multi_cells_kernel(const MultiParams p) {
     m.P2 = 1;
     while (m.P2 < p.max_len) m.P2 <<= 1;
     if (m.P2 < 256) m.P2 = 256;
+    m.stage = mc_smem + 2 * m.P2;
     const int64_t n = p.n;
     double* r = p.work;
     double* rh = r + n;   // BiCG: r~
@@ -192,9 +249,9 @@ __global__ void __launch_bounds__(256) multi_cells_kernel(const MultiParams p) {
     }
     // setup (bicg.cpp:74-91): x = x0, r = 1*b + (-1)*A x
     mc_rows(p, [&](int64_t i) { p.x[i] = p.x0 ? p.x0[i] : 0.0; });
-    grid.sync();
-    mc_rows(p, [&](int64_t i) {
-        const double ri = dadd(p.rhs[i], -mc_spmv_row(p, i, p.x));
+    mc_sync(grid);
+    mc_rows_x(m, p.x, nullptr, [&](int64_t i, int64_t off, int64_t) {
+        const double ri = dadd(p.rhs[i], -mc_spmv_row(m, 0, off, i, p.x));
         r[i] = ri;
         rh[i] = ri;
         if (p.algo == kBiCGStab) {
@@ -211,8 +268,8 @@ __global__ void __launch_bounds__(256) multi_cells_kernel(const MultiParams p) {
         }
     });
     // sigma = <r,r>, rho = <r~,r> from this CTA's rows only: no sync needed
-    mc_block_partials<2>(m, [&](int64_t i, int w) { return w == 0 ? dmul(r[i], r[i]) : dmul(rh[i], r[i]); });
-    grid.sync();
+    mc_block_partials<2>(m, [&](int64_t i, int w, int64_t) { return w == 0 ? dmul(r[i], r[i]) : dmul(rh[i], r[i]); });
+    mc_sync(grid);
     double tot[2];
     mc_combine<2>(m, tot);
     double sigma = tot[0], rho_next = tot[1];
@@ -234,10 +291,10 @@ __global__ void __launch_bounds__(256) multi_cells_kernel(const MultiParams p) {
                     pv[i] = dadd(r[i], dmul(beta, dsub(pv[i], dmul(omega, v[i]))));
                     y[i] = dmul(dinv[i], pv[i]);
                 });
-                grid.sync();
-                mc_rows(p, [&](int64_t i) { v[i] = mc_spmv_row(p, i, y); });
-                mc_block_partials<1>(m, [&](int64_t i, int) { return dmul(rh[i], v[i]); });
-                grid.sync();
+                mc_sync(grid);
+                mc_rows_x(m, y, nullptr, [&](int64_t i, int64_t off, int64_t) { v[i] = mc_spmv_row(m, 0, off, i, y); });
+                mc_block_partials<1>(m, [&](int64_t i, int, int64_t) { return dmul(rh[i], v[i]); });
+                mc_sync(grid);
                 double d1[1];
                 mc_combine<1>(m, d1);
                 if (scalar_breaks(d1[0])) { brk = true; break; }
@@ -247,10 +304,10 @@ __global__ void __launch_bounds__(256) multi_cells_kernel(const MultiParams p) {
                     p.x[i] = dadd(p.x[i], dmul(alpha, y[i]));
                     y[i] = dmul(dinv[i], r[i]);           // y <- z
                 });
-                grid.sync();
-                mc_rows(p, [&](int64_t i) { t[i] = mc_spmv_row(p, i, y); });
-                mc_block_partials<2>(m, [&](int64_t i, int w) { return w == 0 ? dmul(t[i], t[i]) : dmul(t[i], r[i]); });
-                grid.sync();
+                mc_sync(grid);
+                mc_rows_x(m, y, nullptr, [&](int64_t i, int64_t off, int64_t) { t[i] = mc_spmv_row(m, 0, off, i, y); });
+                mc_block_partials<2>(m, [&](int64_t i, int w, int64_t) { return w == 0 ? dmul(t[i], t[i]) : dmul(t[i], r[i]); });
+                mc_sync(grid);
                 double d2[2];
                 mc_combine<2>(m, d2);
                 const double tt = d2[0], ts = d2[1];
@@ -268,13 +325,13 @@ __global__ void __launch_bounds__(256) multi_cells_kernel(const MultiParams p) {
                         v[i] = dadd(rh[i], dmul(beta, v[i]));
                     });
                 }
-                grid.sync();
-                mc_rows(p, [&](int64_t i) {
-                    y[i] = mc_spmv_row(p, i, pv);
-                    t[i] = mc_spmvt_row(p, i, v);
+                mc_sync(grid);
+                mc_rows_x(m, pv, v, [&](int64_t i, int64_t off0, int64_t off1) {
+                    y[i] = mc_spmv_row(m, 0, off0, i, pv);
+                    t[i] = mc_spmvt_row(m, 1, off1, i, v);
                 });
-                mc_block_partials<1>(m, [&](int64_t i, int) { return dmul(v[i], y[i]); });
-                grid.sync();
+                mc_block_partials<1>(m, [&](int64_t i, int, int64_t) { return dmul(v[i], y[i]); });
+                mc_sync(grid);
                 double d1[1];
                 mc_combine<1>(m, d1);
                 if (scalar_breaks(d1[0])) { brk = true; break; }
@@ -288,8 +345,8 @@ __global__ void __launch_bounds__(256) multi_cells_kernel(const MultiParams p) {
             }
             rho_prev = rho;
             iters = it;
-            mc_block_partials<2>(m, [&](int64_t i, int w) { return w == 0 ? dmul(r[i], r[i]) : dmul(rh[i], r[i]); });
-            grid.sync();
+            mc_block_partials<2>(m, [&](int64_t i, int w, int64_t) { return w == 0 ? dmul(r[i], r[i]) : dmul(rh[i], r[i]); });
+            mc_sync(grid);
             mc_combine<2>(m, tot);
             sigma = tot[0];
             rho_next = tot[1];
