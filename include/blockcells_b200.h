@@ -164,6 +164,17 @@ int bc_tmem_schedule_export(int32_t species, const int32_t* row_ptr, const int32
                             int32_t pair, int32_t team, int32_t* info, uint16_t* words, int32_t* vidx,
                             int32_t* xpos, int32_t* yslot);
 
+/* Schedule of the latency-mode kernel (csrc/bc_latency.cuh; bc_plan.hpp
+ * LatencySchedule) for a group of k cells and a kernel instance of `threads`
+ * threads (no GPU needed; for tests).  info[0..7] = n, P, T (threads), lmax
+ * (longest row, A^T row too for bicg), L (padded steps: the [L][T] tables),
+ * xslots (doubles of one warp's gather region), modelled gather wavefronts
+ * of one SpMV, 1 if tables were produced (lmax <= 32).  Arrays (NULL to skip):
+ * rowof/steps [T], rvi/rxo (and for bicg tvi/txo) [L][T], didx [P]. */
+int bc_latency_schedule_export(int32_t species, const int32_t* row_ptr, const int32_t* col_idx, int32_t k,
+                               int32_t bicg, int32_t threads, int32_t* info, int32_t* rowof, int32_t* steps,
+                               int32_t* rvi, uint16_t* rxo, int32_t* tvi, uint16_t* txo, int32_t* didx);
+
 /*
  * Solve every cell's system A_c x_c = b_c (x0 = 0, as solve_group does).
  *   values: cells * nnz fp64, cell-major, each cell in the pattern's CSR order

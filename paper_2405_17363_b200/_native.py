@@ -100,6 +100,7 @@ def b200() -> C.CDLL:
         lib.bc_simulate.argtypes = [_c_p, C.POINTER(SimParams), C.POINTER(MechTables), _c_p, _c_p, _c_p,
                                     C.POINTER(_i64)]
         lib.bc_ctx_pattern_info.argtypes = [_c_p, _c_p]
+        lib.bc_latency_schedule_export.argtypes = [_i32, _c_p, _c_p, _i32, _i32, _i32] + [_c_p] * 8
         lib.bc_devset_create.argtypes = [C.c_int, _c_p, C.POINTER(_c_p)]
         lib.bc_devset_destroy.argtypes = [_c_p]
         lib.bc_devset_destroy.restype = None

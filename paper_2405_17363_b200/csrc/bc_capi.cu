@@ -1198,6 +1198,27 @@ int bc_tmem_schedule_export(int32_t species, const int32_t* row_ptr, const int32
     });
 }
 
+int bc_latency_schedule_export(int32_t species, const int32_t* row_ptr, const int32_t* col_idx, int32_t k,
+                               int32_t bicg, int32_t threads, int32_t* info, int32_t* rowof, int32_t* steps,
+                               int32_t* rvi, uint16_t* rxo, int32_t* tvi, uint16_t* txo, int32_t* didx) {
+    if (!info || k < 1) return BC_ERR_INVALID_ARGUMENT;
+    return guarded(nullptr, [&] {
+        const bc::Pattern pat = make_pattern(species, row_ptr, col_idx);
+        const bc::LatencySchedule ls = bc::build_latency_schedule(pat, k, bicg != 0, threads);
+        const int v[8] = {ls.n, ls.P, ls.T, ls.lmax, ls.L, ls.xslots, ls.model_wavefronts, ls.lmax <= 32 ? 1 : 0};
+        std::memcpy(info, v, sizeof v);
+        if (ls.lmax > 32) return BC_OK;  // no tables: the kernel has no instance for it
+        if (rowof) std::memcpy(rowof, ls.rowof.data(), sizeof(int32_t) * ls.rowof.size());
+        if (steps) std::memcpy(steps, ls.steps.data(), sizeof(int32_t) * ls.steps.size());
+        if (rvi) std::memcpy(rvi, ls.rvi.data(), sizeof(int32_t) * ls.rvi.size());
+        if (rxo) std::memcpy(rxo, ls.rxo.data(), sizeof(uint16_t) * ls.rxo.size());
+        if (bicg && tvi) std::memcpy(tvi, ls.tvi.data(), sizeof(int32_t) * ls.tvi.size());
+        if (bicg && txo) std::memcpy(txo, ls.txo.data(), sizeof(uint16_t) * ls.txo.size());
+        if (didx) std::memcpy(didx, ls.didx.data(), sizeof(int32_t) * ls.didx.size());
+        return BC_OK;
+    });
+}
+
 int bc_solve(bc_ctx* ctx, const bc_solve_params* prm, const double* values, const double* rhs,
              double* x_out, int32_t* group_iters, double* group_rms, uint8_t* group_flags,
              bc_report* report) {

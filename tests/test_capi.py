@@ -309,3 +309,94 @@ def test_tmem_schedule_reproduces_spmv_order(species, k, density, seed, pair, te
             np.testing.assert_array_equal(of.bits(y[n:]), of.bits(ref_spmv_t(rp, ci, vals, x[n:], k, species, nnz)))
     used = sc["vidx"][sc["vidx"] >= 0]
     assert sorted(used.tolist()) == sorted(list(range(k * nnz)) * (2 if pair else 1))
+
+
+# --- latency-mode schedule (bc_latency_plan.cpp) ------------------------------
+
+def export_latency_schedule(rp, ci, k, bicg, threads):
+    lib = _native.b200()
+    _p = of.ptr
+    rp = np.ascontiguousarray(rp, np.int32)
+    ci = np.ascontiguousarray(ci, np.int32)
+    species = len(rp) - 1
+    info = np.zeros(8, np.int32)
+    assert lib.bc_latency_schedule_export(species, _p(rp), _p(ci), k, bicg, threads, _p(info), *([None] * 7)) == 0
+    n, P, T, lmax, L, xslots, model, ok = (int(v) for v in info)
+    out = dict(n=n, P=P, T=T, lmax=lmax, L=L, xslots=xslots, model=model, ok=ok)
+    if not ok:
+        return out
+    rowof, steps, didx = np.zeros(T, np.int32), np.zeros(T, np.int32), np.zeros(P, np.int32)  # noqa: E501
+    rvi, tvi = np.zeros(L * T, np.int32), np.zeros(L * T, np.int32)
+    rxo, txo = np.zeros(L * T, np.uint16), np.zeros(L * T, np.uint16)
+    assert lib.bc_latency_schedule_export(species, _p(rp), _p(ci), k, bicg, threads, _p(info), _p(rowof), _p(steps),
+                                          _p(rvi), _p(rxo), _p(tvi), _p(txo), _p(didx)) == 0
+    out.update(rowof=rowof, steps=steps, didx=didx, rvi=rvi.reshape(L, T), rxo=rxo.reshape(L, T),
+               tvi=tvi.reshape(L, T), txo=txo.reshape(L, T))
+    return out
+
+
+def emulate_latency_spmv(sc, vals, x, xt=None):
+    """The latency kernel's SpMV as it runs: every thread its row in its
+    warp's private gather region (x at slot = row, 16 zero slots, p~ after
+    them), entries in table order from +0.0 up to its warp's step count;
+    the sums land in Y[row]."""
+    P, T = sc["P"], sc["T"]
+    X = np.zeros(sc["xslots"])
+    X[:len(x)] = x
+    if xt is not None:
+        X[P + 16:P + 16 + len(xt)] = xt
+    Y, YT = np.zeros(P), np.zeros(P)
+    for t in range(T):
+        row = sc["rowof"][t]
+        if row < 0:
+            continue
+        for tab_v, tab_o, out in ((sc["rvi"], sc["rxo"], Y), (sc["tvi"], sc["txo"], YT if xt is not None else None)):
+            if out is None:
+                continue
+            acc = 0.0
+            for e in range(sc["steps"][t]):
+                vi = tab_v[e, t]
+                a = vals[vi] if vi >= 0 else 0.0
+                with np.errstate(invalid="ignore"):
+                    acc = acc + a * X[tab_o[e, t] // 8]
+            out[row] = acc
+    return Y, YT
+
+
+@pytest.mark.parametrize("bicg", [0, 1])
+@pytest.mark.parametrize("species,k,density,seed", [(156, 1, 0.0, 0), (40, 3, 0.2, 1), (70, 2, 0.1, 2),
+                                                    (33, 1, 0.3, 3), (100, 2, 0.05, 4)])
+def test_latency_schedule_reproduces_spmv_order(species, k, density, seed, bicg):
+    """Every row (and, for BiCG, A^T row) in CSR / ascending-source-row order
+    from +0.0 with padding that only adds +0.0: bit-identical to csr.cpp's
+    spmv / spmv_transpose; each value used exactly once per pass; rows dealt
+    longest first with per-warp step counts covering every row."""
+    rng = np.random.default_rng(seed)
+    if density == 0.0:
+        m = Mechanism(156, 468, 0)
+        rp, ci = m.row_ptr, m.col_idx
+    else:
+        rp, ci, _, _ = random_batch(rng, 1, species, density)
+    nnz = int(rp[-1])
+    n = k * species
+    threads = 32 * ((n + 31) // 32)
+    sc = export_latency_schedule(rp, ci, k, bicg, threads)
+    assert sc["ok"] and sc["T"] == threads
+    assert sorted(int(r) for r in sc["rowof"] if r >= 0) == list(range(n))
+    lens = np.diff(rp)
+    for t in range(threads):
+        r = sc["rowof"][t]
+        if r >= 0:
+            assert sc["steps"][t] >= lens[r % species]
+    vals = rng.uniform(-1, 1, k * nnz) * 10.0 ** rng.integers(-8, 8, k * nnz)
+    x = rng.uniform(-1, 1, n)
+    xt = rng.uniform(-1, 1, n) if bicg else None
+    Y, YT = emulate_latency_spmv(sc, vals, x, xt)
+    np.testing.assert_array_equal(of.bits(Y[:n]), of.bits(ref_spmv(rp, ci, vals, x, k, species, nnz)))
+    if bicg:
+        np.testing.assert_array_equal(of.bits(YT[:n]), of.bits(ref_spmv_t(rp, ci, vals, xt, k, species, nnz)))
+    used = sc["rvi"][sc["rvi"] >= 0]
+    assert sorted(used.tolist()) == list(range(k * nnz))
+    # padding gathers one of the 16 zero slots
+    pad = sc["rxo"][sc["rvi"] < 0] // 8
+    assert ((pad >= sc["P"]) & (pad < sc["P"] + 16)).all()
