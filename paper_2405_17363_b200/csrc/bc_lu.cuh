@@ -96,26 +96,28 @@ constexpr int kLuTile = 64;  // A22 tile edge: 256 threads x (4 x 4) register mi
 // Factor the n x n row-major matrix `lu` in place (all threads of the CTA);
 // perm[] (shared) starts as the identity and records the row swaps.  Returns
 // false when the matrix is exactly singular (dense_lu.cpp:35).
-// Panel of columns [k0, k1) factored by warp 0 in shared memory (pbuf: rows
-// [k0, n) x kLuPanel + 1): the same pivot choice and per-element update order
-// as the CTA-wide loop below, with warp syncs instead of CTA barriers.  Row
-// swaps are applied to the panel here and to the other columns afterwards
-// (nothing else reads them in between).  Returns false if singular.
-__device__ bool lu_panel_warp(double* lu, const int n, int* perm, double* pbuf, const int k0, const int k1,
-                              int* piv_out) {
+// Panel of columns [k0, k1) factored by the whole CTA in shared memory (pbuf:
+// rows [k0, n) x kLuPanel + 1, one row per thread per pass): the same pivot
+// choice and per-element update order as the unblocked loop in lu_factor,
+// three barriers per column.  Every thread combines the eight warp winners
+// itself, so the pivot needs no broadcast.  Row swaps are applied to the
+// panel here and to the other columns afterwards (nothing else reads them in
+// between).  Returns false (uniformly) if singular.
+__device__ bool lu_panel_cta(const int n, int* perm, double* pbuf, const int k0, const int k1, int* piv_out,
+                             double* red_m, int* red_i) {
     constexpr int LD = kLuPanel + 1;
-    const int lane = threadIdx.x;  // warp 0 only; the CTA loaded the panel into pbuf (lu_factor)
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid % 32, warp = tid / 32, nw = nt / 32;
     const int K = k1 - k0, rows = n - k0;
     for (int kk = 0; kk < K; ++kk) {
         // dense_lu.cpp:32-41: largest magnitude in column k, ties to the lowest row
         const double a0 = fabs(pbuf[kk * LD + kk]);
         double bm = -1.0;
         int bi = n;
-        if (isnan(a0)) {
-            bm = a0;  // every later comparison with NaN fails: pivot stays k
+        if (isnan(a0)) {  // every later comparison with NaN fails: pivot stays k (uniform branch)
+            bm = a0;
             bi = kk;
         } else {
-            for (int r = kk + lane; r < rows; r += 32) {
+            for (int r = kk + tid; r < rows; r += nt) {
                 const double mag = fabs(pbuf[r * LD + kk]);
                 if (!isnan(mag)) lu_argmax_combine(bm, bi, mag, r);
             }
@@ -124,37 +126,39 @@ __device__ bool lu_panel_warp(double* lu, const int n, int* perm, double* pbuf, 
                 const int i2 = __shfl_xor_sync(0xffffffffu, bi, off);
                 lu_argmax_combine(bm, bi, m2, i2);
             }
+            if (lane == 0) {
+                red_m[warp] = bm;
+                red_i[warp] = bi;
+            }
+            __syncthreads();
+            bm = red_m[0];
+            bi = red_i[0];
+            for (int w = 1; w < nw; ++w) lu_argmax_combine(bm, bi, red_m[w], red_i[w]);
         }
-        if (bm == 0.0) return false;  // dense_lu.cpp:35
-        if (lane == 0) {
+        if (bm == 0.0) return false;  // dense_lu.cpp:35 (every thread sees the same bm)
+        if (tid == 0) {
             piv_out[kk] = k0 + bi;
             const int t = perm[k0 + kk];
             perm[k0 + kk] = perm[k0 + bi];
             perm[k0 + bi] = t;
         }
-        if (bi != kk && lane < K) {
-            const double t = pbuf[kk * LD + lane];
-            pbuf[kk * LD + lane] = pbuf[bi * LD + lane];
-            pbuf[bi * LD + lane] = t;
+        if (bi != kk && tid < K) {
+            const double t = pbuf[kk * LD + tid];
+            pbuf[kk * LD + tid] = pbuf[bi * LD + tid];
+            pbuf[bi * LD + tid] = t;
         }
-        __syncwarp();
-        // l_rk = a_rk / pivot, then row r's rest of the panel, in registers
+        __syncthreads();
+        // l_rk = a_rk / pivot, then row r's rest of the panel
         const double pv = pbuf[kk * LD + kk];
-        double u[kLuPanel];
-#pragma unroll
-        for (int c = 0; c < kLuPanel; ++c) u[c] = pbuf[kk * LD + c];
-        for (int r = kk + 1 + lane; r < rows; r += 32) {
+        for (int r = kk + 1 + tid; r < rows; r += nt) {
             double* row = pbuf + r * LD;
             const double l = __ddiv_rn(row[kk], pv);
-            double a[kLuPanel];
-#pragma unroll
-            for (int c = 0; c < kLuPanel; ++c) a[c] = row[c];
             row[kk] = l;
 #pragma unroll
             for (int c = 0; c < kLuPanel; ++c)
-                if (c > kk && c < K) row[c] = __dsub_rn(a[c], __dmul_rn(l, u[c]));
+                if (c > kk && c < K) row[c] = __dsub_rn(row[c], __dmul_rn(l, pbuf[kk * LD + c]));
         }
-        __syncwarp();
+        __syncthreads();
     }
     return true;  // the CTA writes pbuf back (lu_factor)
 }
@@ -186,12 +190,7 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
                 }
             }
             __syncthreads();
-            if (tid < 32) {
-                const bool ok = lu_panel_warp(lu, n, perm, pbuf, k0, k1, s_piv);
-                if (tid == 0 && !ok) s_singular = 1;
-            }
-            __syncthreads();
-            if (s_singular) return false;
+            if (!lu_panel_cta(n, perm, pbuf, k0, k1, s_piv, red_m, red_i)) return false;
             {
                 const int K = k1 - k0, rows = n - k0;
                 for (int q = tid; q < rows * K; q += nt) {
@@ -490,6 +489,25 @@ __device__ bool lu_backward_warp(const double* lu, const int n, double* x, doubl
         }
         dg = lane == 0 ? row[ii] : 0.0;
     };
+    if (nq > 8) {  // rows longer than 256: no prefetch window, the plain loop
+        for (int ii = n - 1; ii >= 0; --ii) {
+            const double* row = lu + static_cast<int64_t>(ii) * n;
+            for (int j = ii + 1 + lane; j < n; j += 32) slots[j] = __dmul_rn(row[j], x[j]);
+            __syncwarp();
+            if (lane == 0) {
+                double acc = x[ii];
+#pragma unroll 8
+                for (int j = ii + 1; j < n; ++j) acc = __dsub_rn(acc, slots[j]);
+                if (is_neg_zero(acc)) {
+                    z = true;
+                    if (later_neg) acc = 0.0;
+                }
+                x[ii] = __ddiv_rn(acc, row[ii]);
+            }
+            __syncwarp();
+        }
+        return __shfl_sync(0xffffffffu, z ? 1 : 0, 0) != 0;
+    }
     load_row(n - 1, cur, dcur);
     for (int ii = n - 1; ii >= 0; --ii) {
         if (ii > 0) load_row(ii - 1, nxt, dnxt);
