@@ -135,3 +135,22 @@ def test_multi_cells_large_breakdown_sign_chain(solver, seed):
     rep = solver.run_strategy(sysm, StrategyConfig(Strategy.MultiCells), DeviceSpec(), 1e-30, 40, 1, Algo.BICG)
     np.testing.assert_array_equal(of.bits(rep.per_cell_x), of.bits(want.x))
     assert of.bits(rep.max_residual_rms) == of.bits(want.report.max_residual_rms)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [None, 2])
+def test_coupled_breakdown_blocks_above_256_rows(solver, k):
+    """Coupled groups of 312-species cells (blocks above 256 rows: the back
+    substitution's long-row path) breaking down in the P regime -- the cases
+    the round-2 fuzzer caught (tools/fuzz_gpu.py seed 41)."""
+    from paper_2405_17363_b200 import Mechanism, REGIME_P
+    m = Mechanism(312, 936, 0)
+    v, b = m.newton_batch(0, 9, 100_000, REGIME_P.h)
+    rep = solver.run_strategy(BatchedSystem(312, 9, m.row_ptr, m.col_idx, v, b), StrategyConfig(Strategy.BlockCells, k),
+                              DeviceSpec(), 1e-30, 300, 1, Algo.BICGSTAB_JACOBI)
+    assert rep.breakdown_fallbacks >= 1
+    st, res = of.orc_solve_batch(2, 1, 0 if k is None else k, m.row_ptr, m.col_idx, v, b, 1e-30, 300, workers=8)
+    assert st == 0
+    np.testing.assert_array_equal(of.bits(np.asarray(rep.per_cell_x)), of.bits(res.x))
+    np.testing.assert_array_equal(of.bits(np.asarray(rep.per_block_residual_rms)), of.bits(res.rms))
+    np.testing.assert_array_equal(np.asarray(rep.per_block_iterations), res.iters)
