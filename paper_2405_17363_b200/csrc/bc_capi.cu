@@ -902,19 +902,6 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
     const bool use_smem_block = blockdiag && smem_blk <= static_cast<size_t>(lu_dyn_max) && lue && *lue == '1';
     if (use_smem_block) smem = smem_blk;
     if (smem > static_cast<size_t>(lu_dyn_max)) fail(BC_ERR_INVALID_ARGUMENT, "LU fallback: group too large");
-    // Coupled groups whose s x s block fits shared memory: the warp-specialised
-    // kernel (factor team + back-substitution warp, bc_lu.cuh); BC_LU_WS=0 keeps
-    // lu_fallback_kernel for A/B.
-    cudaFuncAttributes fw{};
-    check_cuda(cudaFuncGetAttributes(&fw, bc::lu_blockdiag_ws_kernel), "cudaFuncGetAttributes(lu ws)");
-    const int ws_dyn_max = kMaxDynSmem - static_cast<int>(fw.sharedSizeBytes);
-    const size_t smem_ws = sizeof(double) * (static_cast<size_t>(s) * s + nmax + s) + sizeof(int) * ((nmax + 1) & ~1);
-    const char* wse = std::getenv("BC_LU_WS");
-    const bool use_ws = blockdiag && !use_smem_block && kmax <= 64 && smem_ws <= static_cast<size_t>(ws_dyn_max) &&
-                        !(wse && *wse == '0');
-    if (use_ws)
-        check_cuda(cudaFuncSetAttribute(bc::lu_blockdiag_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        ws_dyn_max), "cudaFuncSetAttribute(lu ws)");
     for (size_t b0 = 0; b0 < ents.size(); b0 += batch) {
         const int cnt = static_cast<int>(std::min<int64_t>(batch, ents.size() - b0));
         bc::LuParams lp{};
@@ -938,10 +925,7 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
         lp.flip = flip;
         lp.later_neg = later_neg;
         lp.chain_flags = d_chain_flags ? d_chain_flags + b0 : nullptr;
-        if (use_ws)
-            bc::lu_blockdiag_ws_kernel<<<cnt, 288, smem_ws, st>>>(lp);
-        else
-            bc::lu_fallback_kernel<<<cnt, 256, smem, st>>>(lp);
+        bc::lu_fallback_kernel<<<cnt, 256, smem, st>>>(lp);
         check_cuda(cudaGetLastError(), "lu_fallback_kernel launch");
         ctx->launches++;
         ctx->kernels |= BC_KERNEL_LU;

@@ -56,7 +56,6 @@ struct LuParams {
     int block_width;         // 0 = single interval
     int mode;                // 0 block-diagonal when k > 1, 1 dense
     int panel_rows;          // > 0: panels are factored in shared memory (rows <= panel_rows)
-    int ws;                  // lu_blockdiag_ws_kernel: the block lives in shared memory (see there)
     int smem_block;          // block-diagonal mode: each s x s block is densified, factored and
                              // forward-substituted in shared memory, then parked in scratch
                              // for the backward pass (one CTA per SM; 156^2 doubles = 195 KB)
@@ -84,17 +83,6 @@ __device__ __forceinline__ void lu_argmax_combine(double& m, int& i, double m2, 
 
 __device__ __forceinline__ bool is_neg_zero(double v) { return v == 0.0 && signbit(v); }
 
-// Barrier policies: the whole CTA, or the 256-thread factor team (warps 0-7,
-// named barrier 1) of the warp-specialised kernel below.
-struct CtaSync {
-    static __device__ __forceinline__ void sync() { __syncthreads(); }
-    static __device__ __forceinline__ int threads() { return blockDim.x; }
-};
-struct TeamSync {
-    static __device__ __forceinline__ void sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-    static __device__ __forceinline__ int threads() { return 256; }
-};
-
 // Right-looking LU in panels of kLuPanel columns on physically swapped rows:
 // every element still receives its updates a_ij -= l_ik * u_kj one k at a
 // time in ascending k, each product and difference rounded separately, with
@@ -115,11 +103,10 @@ constexpr int kLuTile = 64;  // A22 tile edge: 256 threads x (4 x 4) register mi
 // itself, so the pivot needs no broadcast.  Row swaps are applied to the
 // panel here and to the other columns afterwards (nothing else reads them in
 // between).  Returns false (uniformly) if singular.
-template <class S>
 __device__ bool lu_panel_cta(const int n, int* perm, double* pbuf, const int k0, const int k1, int* piv_out,
                              double* red_m, int* red_i) {
     constexpr int LD = kLuPanel + 1;
-    const int tid = threadIdx.x, nt = S::threads(), lane = tid % 32, warp = tid / 32, nw = nt / 32;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid % 32, warp = tid / 32, nw = nt / 32;
     const int K = k1 - k0, rows = n - k0;
     for (int kk = 0; kk < K; ++kk) {
         // dense_lu.cpp:32-41: largest magnitude in column k, ties to the lowest row
@@ -143,7 +130,7 @@ __device__ bool lu_panel_cta(const int n, int* perm, double* pbuf, const int k0,
                 red_m[warp] = bm;
                 red_i[warp] = bi;
             }
-            S::sync();
+            __syncthreads();
             bm = red_m[0];
             bi = red_i[0];
             for (int w = 1; w < nw; ++w) lu_argmax_combine(bm, bi, red_m[w], red_i[w]);
@@ -160,7 +147,7 @@ __device__ bool lu_panel_cta(const int n, int* perm, double* pbuf, const int k0,
             pbuf[kk * LD + tid] = pbuf[bi * LD + tid];
             pbuf[bi * LD + tid] = t;
         }
-        S::sync();
+        __syncthreads();
         // l_rk = a_rk / pivot, then row r's rest of the panel
         const double pv = pbuf[kk * LD + kk];
         for (int r = kk + 1 + tid; r < rows; r += nt) {
@@ -171,12 +158,11 @@ __device__ bool lu_panel_cta(const int n, int* perm, double* pbuf, const int k0,
             for (int c = 0; c < kLuPanel; ++c)
                 if (c > kk && c < K) row[c] = __dsub_rn(row[c], __dmul_rn(l, pbuf[kk * LD + c]));
         }
-        S::sync();
+        __syncthreads();
     }
     return true;  // the CTA writes pbuf back (lu_factor)
 }
 
-template <class S>
 __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
     __shared__ double red_m[8];
     __shared__ int red_i[8];
@@ -184,11 +170,11 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
     __shared__ double s_lt[kLuTile][kLuPanel + 1];  // L21 tile (rows x panel)
     __shared__ double s_ut[kLuPanel][kLuTile];      // U12 tile (panel x cols)
     static_assert(kLuTile == 64, "the A22 micro-tiling below assumes 256 threads on a 64 x 64 tile");
-    const int tid = threadIdx.x, nt = S::threads();
+    const int tid = threadIdx.x, nt = blockDim.x;
     // n <= 2048 (kMaxGroupRows): 32-bit element offsets
     auto A = [&](int i, int j) -> double& { return lu[i * n + j]; };
     if (tid == 0) s_singular = 0;
-    S::sync();
+    __syncthreads();
 
     __shared__ int s_piv[kLuPanel];
     for (int k0 = 0; k0 < n; k0 += kLuPanel) {
@@ -203,8 +189,8 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
                     pbuf[r * (kLuPanel + 1) + c] = A(k0 + r, k0 + c);
                 }
             }
-            S::sync();
-            if (!lu_panel_cta<S>(n, perm, pbuf, k0, k1, s_piv, red_m, red_i)) return false;
+            __syncthreads();
+            if (!lu_panel_cta(n, perm, pbuf, k0, k1, s_piv, red_m, red_i)) return false;
             {
                 const int K = k1 - k0, rows = n - k0;
                 for (int q = tid; q < rows * K; q += nt) {
@@ -224,7 +210,7 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
                     }
                 }
             }
-            S::sync();
+            __syncthreads();
         }
         // panel factorization: columns [k0, k1), rows [k0, n)
         for (int k = k0; k < (pbuf ? k0 : k1); ++k) {
@@ -250,7 +236,7 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
                     red_i[tid >> 5] = bi;
                 }
             }
-            S::sync();
+            __syncthreads();
             if (tid == 0) {
                 if (!isnan(a0)) {
                     bm = red_m[0];
@@ -263,7 +249,7 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
                 perm[k] = perm[bi];
                 perm[bi] = t;
             }
-            S::sync();
+            __syncthreads();
             if (s_singular) return false;
             const int piv = s_pivot;
             if (piv != k)  // the whole row moves (its trailing part is as stale as row k's)
@@ -272,17 +258,17 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
                     A(k, c) = A(piv, c);
                     A(piv, c) = t;
                 }
-            S::sync();
+            __syncthreads();
             const double pv = A(k, k);
             for (int i = k + 1 + tid; i < n; i += nt) A(i, k) = __ddiv_rn(A(i, k), pv);
-            S::sync();
+            __syncthreads();
             const int w = k1 - k - 1;  // the rest of the panel
             if (w > 0) {
                 for (int64_t idx = tid; idx < static_cast<int64_t>(n - k - 1) * w; idx += nt) {
                     const int i = k + 1 + static_cast<int>(idx / w), j = k + 1 + static_cast<int>(idx % w);
                     A(i, j) = __dsub_rn(A(i, j), __dmul_rn(A(i, k), A(k, j)));
                 }
-                S::sync();
+                __syncthreads();
             }
         }
         if (k1 == n) break;
@@ -307,7 +293,7 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
                     if (i < K) A(k0 + i, j) = u[i];
             }
         }
-        S::sync();
+        __syncthreads();
         // A22: rows and columns [k1, n), the panel's updates in ascending k per element
         const int K = k1 - k0, m = n - k1, tiles = (m + kLuTile - 1) / kLuTile;
         for (int t = 0; t < tiles * tiles; ++t) {
@@ -318,7 +304,7 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
                 const int kr = q / kLuTile, c = q % kLuTile;
                 s_ut[kr][c] = (j0 + c < n && kr < K) ? A(k0 + kr, j0 + c) : 0.0;
             }
-            S::sync();
+            __syncthreads();
             // thread (tr, tc) owns rows 4tr..4tr+3 and columns tc + 16q of the tile; per
             // element the panel's updates still run one k at a time in ascending order
             const int tr = tid / 16, tc = tid % 16;
@@ -365,7 +351,7 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
                         }
                 }
             }
-            S::sync();
+            __syncthreads();
         }
     }
     return true;
@@ -376,9 +362,8 @@ __device__ bool lu_factor(double* lu, const int n, int* perm, double* pbuf) {
 // thread's row entries l_ij are read kLuFwdAhead steps ahead of use, so the
 // per-step cost is the barrier, not an L2 round trip.
 constexpr int kLuFwdAhead = 8;
-template <class S>
 __device__ void lu_forward(const double* lu, const int n, double* y) {
-    const int tid = threadIdx.x, nt = S::threads();
+    const int tid = threadIdx.x, nt = blockDim.x;
     if (n <= nt) {  // one row per thread (every block-diagonal block and most groups)
         const int i = tid;
         const double* row = lu + static_cast<int64_t>(i < n ? i : 0) * n;
@@ -395,22 +380,22 @@ __device__ void lu_forward(const double* lu, const int n, double* y) {
 #pragma unroll
             for (int q = 0; q < kLuFwdAhead; ++q) {
                 const int j = j0 + q;
-                S::sync();
+                __syncthreads();
                 if (j < n && i > j && i < n) y[i] = __dsub_rn(y[i], __dmul_rn(win[q], y[j]));
             }
 #pragma unroll
             for (int q = 0; q < kLuFwdAhead; ++q) win[q] = nxt[q];
         }
-        S::sync();
+        __syncthreads();
         return;
     }
     for (int j = 0; j < n; ++j) {
-        S::sync();
+        __syncthreads();
         const double xj = y[j];
         for (int i = j + 1 + tid; i < n; i += nt)
             y[i] = __dsub_rn(y[i], __dmul_rn(lu[static_cast<int64_t>(i) * n + j], xj));
     }
-    S::sync();
+    __syncthreads();
 }
 
 // Backward substitution U x = y (dense_lu.cpp:58-62) in place on x[]: row ii
@@ -552,19 +537,18 @@ __device__ bool lu_backward_warp(const double* lu, const int n, double* x, doubl
 
 // Scatter cells [c0, c0 + cells) of the group into the zeroed dense matrix
 // `lu` (row length ld): dense_lu.cpp:8-16 on the block-diagonal matrix.
-template <class S>
 __device__ void lu_densify(double* lu, const int ld, const double* vals, const int32_t* row_ptr,
                            const int32_t* col_idx, const int s, const int nnz, const int cells) {
-    const int tid = threadIdx.x, nt = S::threads();
+    const int tid = threadIdx.x, nt = blockDim.x;
     const int n = cells * s;
     for (int64_t idx = tid; idx < static_cast<int64_t>(n) * ld; idx += nt) lu[idx] = 0.0;
-    S::sync();
+    __syncthreads();
     for (int i = tid; i < n; i += nt) {
         const int c = i / s, r = i % s;
         for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e)
             lu[static_cast<int64_t>(i) * ld + (ld == s ? 0 : c * s) + col_idx[e]] = vals[c * nnz + e];
     }
-    S::sync();
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(256, 3) lu_fallback_kernel(const LuParams p) {
@@ -605,12 +589,12 @@ __global__ void __launch_bounds__(256, 3) lu_fallback_kernel(const LuParams p) {
         for (int c = 0; c < ent.kc; ++c) {
             double* gblk = lu + static_cast<int64_t>(c) * s * s;
             double* blk = sblk ? sblk : gblk;
-            lu_densify<CtaSync>(blk, s, vals + static_cast<int64_t>(c) * p.nnz, p.row_ptr, p.col_idx, s, p.nnz, 1);
+            lu_densify(blk, s, vals + static_cast<int64_t>(c) * p.nnz, p.row_ptr, p.col_idx, s, p.nnz, 1);
             if (neg_pivot)
                 for (int q = tid; q < s * s; q += nt)
                     if (is_neg_zero(blk[q])) blk[q] = 0.0;
             __syncthreads();
-            if (!lu_factor<CtaSync>(blk, s, perm + c * s, pbuf)) {
+            if (!lu_factor(blk, s, perm + c * s, pbuf)) {
                 if (tid == 0) p.status[blockIdx.x] = 1;
                 return;
             }
@@ -628,7 +612,7 @@ __global__ void __launch_bounds__(256, 3) lu_fallback_kernel(const LuParams p) {
                 if (fwd_flip && is_neg_zero(v)) v = 0.0;
                 y[i] = v;
             }
-            lu_forward<CtaSync>(blk, s, y);
+            lu_forward(blk, s, y);
             int flip = 0;
             for (int i = tid; i < s; i += nt) flip |= (signbit(blk[i * s + i]) != signbit(y[i])) ? 1 : 0;
             fwd_flip = __syncthreads_or(flip) || fwd_flip;
@@ -675,14 +659,14 @@ __global__ void __launch_bounds__(256, 3) lu_fallback_kernel(const LuParams p) {
             return;
         }
     } else {
-        lu_densify<CtaSync>(lu, n, vals, p.row_ptr, p.col_idx, s, p.nnz, ent.kc);
+        lu_densify(lu, n, vals, p.row_ptr, p.col_idx, s, p.nnz, ent.kc);
         int nzv = 0;
         for (int64_t q = tid; q < static_cast<int64_t>(ent.kc) * p.nnz; q += nt) nzv |= is_neg_zero(vals[q]);
         if (p.conv)
             for (int64_t q = tid; q < static_cast<int64_t>(n) * n; q += nt)
                 if (is_neg_zero(lu[q])) lu[q] = 0.0;
         __syncthreads();
-        if (!lu_factor<CtaSync>(lu, n, perm, pbuf)) {
+        if (!lu_factor(lu, n, perm, pbuf)) {
             if (tid == 0) p.status[blockIdx.x] = 1;
             return;
         }
@@ -693,7 +677,7 @@ __global__ void __launch_bounds__(256, 3) lu_fallback_kernel(const LuParams p) {
             if (p.flip && is_neg_zero(v)) v = 0.0;
             sum[i] = v;
         }
-        lu_forward<CtaSync>(lu, n, sum);
+        lu_forward(lu, n, sum);
         int neg = 0, fwd = 0;
         for (int i = tid; i < n; i += nt) {
             const double u = lu[static_cast<int64_t>(i) * n + i];
@@ -728,191 +712,6 @@ __global__ void __launch_bounds__(256, 3) lu_fallback_kernel(const LuParams p) {
                 double acc = 0.0;
                 for (int e = p.row_ptr[r]; e < p.row_ptr[r + 1]; ++e)
                     acc = __dadd_rn(acc, __dmul_rn(vals[c * p.nnz + e], sum[c * s + p.col_idx[e]]));
-                const double ri = __dsub_rn(b[i], acc);
-                v = __dmul_rn(ri, ri);
-            }
-            slots[q] = v;
-        }
-        for (int stride = P / 2; stride >= 1; stride /= 2) {
-            __syncthreads();
-            for (int q = tid; q < stride; q += nt) slots[q] = __dadd_rn(slots[q], slots[q + stride]);
-        }
-        __syncthreads();
-        total = blk == 0 ? slots[0] : __dadd_rn(total, slots[0]);
-    }
-    if (tid == 0) {
-        p.g_rms[ent.gout] = __dsqrt_rn(__ddiv_rn(total, static_cast<double>(n)));
-        p.status[blockIdx.x] = 0;
-    }
-}
-
-// Forward substitution L y = P b by one warp, L read from global memory (the
-// rare redo of lu_blockdiag_ws_kernel): row i subtracts j = 0..i-1 in order.
-__device__ void lu_forward_warp(const double* lu, const int n, double* y) {
-    const int lane = threadIdx.x % 32;
-    for (int j = 0; j < n; ++j) {
-        __syncwarp();
-        const double xj = y[j];
-        for (int i = j + 1 + lane; i < n; i += 32)
-            y[i] = __dsub_rn(y[i], __dmul_rn(lu[static_cast<int64_t>(i) * n + j], xj));
-    }
-    __syncwarp();
-}
-
-// Block-diagonal LU fallback, warp-specialised (coupled groups whose s x s
-// block fits shared memory, M156: 195 KB): 288 threads, one CTA per SM.
-//  * warps 0-7 (the factor team, named barrier 1) densify block c in shared
-//    memory, factor it (lu_factor's panels, A22 register tiles), run its
-//    forward substitution there, copy the factors to scratch and flag the
-//    block ready, then move to block c + 1;
-//  * warp 8 runs the back substitution of each ready block from scratch --
-//    a 12k-step dependent chain per 156-row block (dense_lu.cpp:58-62 order)
-//    that now overlaps the next block's factorisation instead of following
-//    the whole group -- assuming no later block has a negative x
-//    (later_neg false), and at the end redoes, last block first, the rare
-//    block that summed a row to -0 while a later x is negative.
-// The sign-of-zero replay and every operation order are lu_fallback_kernel's
-// (see the top of this file); results are bit-identical.
-__global__ void __launch_bounds__(288, 1) lu_blockdiag_ws_kernel(const LuParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int s_ready[64];        // per block: 0 pending, 1 factored, 2 abort
-    __shared__ int s_flag[4];          // team ORs: neg, nonfinite, flip
-    __shared__ uint8_t s_fwdflip[64];  // fwd_flip before block c (for the redo)
-    __shared__ unsigned s_zmask[2];
-    const LuEntry ent = p.entries[blockIdx.x];
-    const int s = p.species, kc = ent.kc, n = kc * s;
-    const int tid = threadIdx.x, nt = blockDim.x;
-    double* lu = p.scratch + static_cast<size_t>(blockIdx.x) * p.stride;
-    // dynamic shared memory: A (s*s) | perm (n ints) | yx (n) | wslots (s)
-    double* A = reinterpret_cast<double*>(smem_raw);
-    int* perm = reinterpret_cast<int*>(A + static_cast<size_t>(s) * s);
-    double* yx = reinterpret_cast<double*>(perm + ((n + 1) & ~1));
-    double* wslots = yx + n;
-    const double* vals = p.values + ent.cell0 * p.nnz;
-    const double* b = p.rhs + ent.cell0 * s;
-
-    for (int i = tid; i < n; i += nt) perm[i] = i % s;
-    for (int i = tid; i < 64; i += nt) s_ready[i] = 0;
-    if (tid < 2) s_zmask[tid] = 0u;
-    int bad = 0;  // finite inputs only (else the host reruns the group densely)
-    for (int64_t q = tid; q < static_cast<int64_t>(kc) * p.nnz; q += nt) bad |= !isfinite(vals[q]);
-    for (int q = tid; q < n; q += nt) bad |= !isfinite(b[q]);
-    if (__syncthreads_or(bad)) {
-        if (tid == 0) p.status[blockIdx.x] = 2;
-        return;
-    }
-    int status = 0;  // factor team: 1 singular, 2 non-finite
-    if (tid < 256) {
-        bool neg_pivot = false, fwd_flip = false;
-        for (int c = 0; c < kc; ++c) {
-            lu_densify<TeamSync>(A, s, vals + static_cast<int64_t>(c) * p.nnz, p.row_ptr, p.col_idx, s, p.nnz, 1);
-            if (neg_pivot)
-                for (int q = tid; q < s * s; q += 256)
-                    if (is_neg_zero(A[q])) A[q] = 0.0;
-            if (tid < 4) s_flag[tid] = 0;
-            TeamSync::sync();
-            if (!lu_factor<TeamSync>(A, s, perm + c * s, nullptr)) {
-                status = 1;
-            } else {
-                int neg = 0, nonfinite = 0;
-                for (int q = tid; q < s * s; q += 256) nonfinite |= !isfinite(A[q]);
-                for (int i = tid; i < s; i += 256) neg |= signbit(A[i * s + i]) ? 1 : 0;
-                if (neg) atomicOr(&s_flag[0], 1);
-                if (nonfinite) atomicOr(&s_flag[1], 1);
-                TeamSync::sync();
-                if (s_flag[1]) status = 2;
-                neg_pivot = neg_pivot || s_flag[0];
-            }
-            if (status) {  // abort: release warp 8
-                if (tid == 0)
-                    for (int q = c; q < kc; ++q) *reinterpret_cast<volatile int*>(&s_ready[q]) = 2;
-                break;
-            }
-            double* y = yx + c * s;
-            if (tid == 0) s_fwdflip[c] = fwd_flip;
-            for (int i = tid; i < s; i += 256) {
-                double v = b[c * s + perm[c * s + i]];
-                if (fwd_flip && is_neg_zero(v)) v = 0.0;
-                y[i] = v;
-            }
-            lu_forward<TeamSync>(A, s, y);
-            int flip = 0;
-            for (int i = tid; i < s; i += 256) flip |= (signbit(A[i * s + i]) != signbit(y[i])) ? 1 : 0;
-            if (flip) atomicOr(&s_flag[2], 1);
-            double* gblk = lu + static_cast<int64_t>(c) * s * s;
-            for (int q = tid; q < s * s; q += 256) gblk[q] = A[q];  // the factors, for warp 8
-            __threadfence_block();
-            TeamSync::sync();
-            fwd_flip = fwd_flip || s_flag[2];
-            if (tid == 0) *reinterpret_cast<volatile int*>(&s_ready[c]) = 1;
-        }
-    } else if (tid < 288) {
-        // warp 8: back substitutions as blocks become ready
-        bool aborted = false;
-        for (int c = 0; c < kc; ++c) {
-            int r;
-            while ((r = *reinterpret_cast<volatile int*>(&s_ready[c])) == 0) __nanosleep(100);
-            if (r == 2) {
-                aborted = true;
-                break;
-            }
-            __threadfence_block();
-            const bool z = lu_backward_warp(lu + static_cast<int64_t>(c) * s * s, s, yx + c * s, wslots, false);
-            if (z && tid == 256) s_zmask[c / 32] |= 1u << (c % 32);
-        }
-        __syncwarp();
-        if (!aborted) {  // the reference's order: last block first, later_neg from final x
-            bool later_neg = false;
-            for (int c = kc - 1; c >= 0; --c) {
-                double* xc = yx + c * s;
-                if (later_neg && (s_zmask[c / 32] >> (c % 32) & 1u)) {
-                    const double* gblk = lu + static_cast<int64_t>(c) * s * s;
-                    for (int i = tid - 256; i < s; i += 32) {
-                        double v = b[c * s + perm[c * s + i]];
-                        if (s_fwdflip[c] && is_neg_zero(v)) v = 0.0;
-                        xc[i] = v;
-                    }
-                    lu_forward_warp(gblk, s, xc);
-                    lu_backward_warp(gblk, s, xc, wslots, true);
-                }
-                int neg = 0;
-                for (int i = tid - 256; i < s; i += 32) neg |= signbit(xc[i]) ? 1 : 0;
-                later_neg = __any_sync(0xffffffffu, neg) || later_neg;
-            }
-        }
-    }
-    // everyone: the team's status, then the checks and the residual as lu_fallback_kernel
-    __shared__ int s_status;
-    if (tid == 0) s_status = status;
-    __syncthreads();
-    if (s_status) {
-        if (tid == 0) p.status[blockIdx.x] = s_status;
-        return;
-    }
-    int nonfinite = 0;
-    for (int i = tid; i < n; i += nt) nonfinite |= !isfinite(yx[i]);
-    if (__syncthreads_or(nonfinite)) {
-        if (tid == 0) p.status[blockIdx.x] = 2;
-        return;
-    }
-    double* xo = p.x_out + ent.cell0 * s;
-    for (int i = tid; i < n; i += nt) xo[i] = yx[i];
-    // residual through the group's plan (strategies.cpp:48-58); A's space holds the tree
-    double* slots = A;
-    const int width = p.block_width > 0 ? p.block_width : n;
-    double total = 0.0;
-    for (int b0 = 0, blk = 0; b0 < n; b0 += width, ++blk) {
-        const int len = min(width, n - b0);
-        int P = 1;
-        while (P < len) P <<= 1;
-        __syncthreads();
-        for (int q = tid; q < P; q += nt) {
-            double v = 0.0;
-            if (q < len) {
-                const int i = b0 + q, c = i / s, r = i % s;
-                double acc = 0.0;
-                for (int e = p.row_ptr[r]; e < p.row_ptr[r + 1]; ++e)
-                    acc = __dadd_rn(acc, __dmul_rn(vals[c * p.nnz + e], yx[c * s + p.col_idx[e]]));
                 const double ri = __dsub_rn(b[i], acc);
                 v = __dmul_rn(ri, ri);
             }
