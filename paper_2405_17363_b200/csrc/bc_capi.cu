@@ -701,9 +701,9 @@ bool launch_latency(bc_ctx* ctx, const bc::Pattern& pat, const bc::GroupPlan& gp
     p.tol = tol;
     p.max_iter = static_cast<int>(std::min<int64_t>(max_iter, 0x7FFFFFFE));
     p.gate = gate;
-    // Y [2][2][P] + one gather region per warp
+    // Y [2][P] + the gather region
     const int threads = lp.T;
-    const size_t smem = sizeof(double) * (4 * static_cast<size_t>(lp.P) + static_cast<size_t>(threads / 32) * lp.xslots);
+    const size_t smem = sizeof(double) * (2 * static_cast<size_t>(lp.P) + static_cast<size_t>(lp.xslots));
     if (smem > static_cast<size_t>(kMaxDynSmem - 1024)) return false;
     if (!ctx->smem_set[reinterpret_cast<BlockFn>(cfg->fn)]) {
         check_cuda(cudaFuncSetAttribute(cfg->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem - 1024),

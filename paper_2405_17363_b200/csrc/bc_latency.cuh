@@ -6,27 +6,27 @@
 // steps per SpMV) and overlaps 16 cells per SM to fill the shared-memory
 // pipe; alone on an SM one cell takes ~4.5 ms for 1000 iterations (~8,900
 // cycles per iteration, a dependent-latency chain).  When there are fewer
-// groups than SMs can overlap, latency is the metric.  Here every warp of
-// the CTA holds the WHOLE group's Krylov vectors in the throughput kernel's
-// owner layout (lane l, slot j: row 32j + l -- so every dot product is
+// groups than SMs can overlap, latency is the metric.  Here warp 0 (the
+// leader) holds the group's Krylov vectors in the throughput kernel's owner
+// layout (lane l, slot j: row 32j + l -- so every dot product is
 // tmem_reduce's lane tree + xor butterfly, the reference's stride-halving
-// tree, computed in registers with no cross-warp step), and the SpMV is split
-// over the warps, one row per thread (the reference's own Block-cells
-// geometry, exec_model.cpp:115-122, 134-158):
+// tree, in registers with no cross-warp step) and runs the scalar
+// recurrences; the SpMV is split over all warps, one row per thread (the
+// reference's own Block-cells geometry, exec_model.cpp:115-122, 134-158):
 //
-//   * each warp publishes the vector into its private copy of the gather
-//     vector (lane-major, conflict-free) -- __syncwarp, no block barrier;
+//   * the leader publishes the vector into the one shared gather region
+//     (lane-major, conflict-free), posts the order (SpMV, SpMV pair, exit)
+//     and arrives at barrier A;
 //   * thread t computes the row the schedule gave it (rows dealt longest
 //     first, so later warps run fewer steps; bc_latency_plan.cpp): its
 //     values and gather offsets live in registers, entries in CSR order,
 //     padding entries are (0.0, a zero slot) which add exact +0.0 to a sum
 //     that started at +0.0 (csr.cpp:90-101 bit for bit);
-//   * the row sums meet in a double-buffered Y (one block barrier per SpMV)
-//     and every warp reads the whole product back into its owner slots.
-// Per Jacobi-BiCGSTAB iteration that is 2 block barriers (the throughput
-// kernel's team variant needs 7); reductions and scalar recurrences run
-// redundantly, bit-identically, in every warp.  BiCG's A^T row runs beside
-// the A row as a second chain over the p~ copy.  Rows >= n carry exact +0.0
+//   * the row sums meet in Y at barrier B and the leader reads the product
+//     back into its owner slots; the helper warps wait at the next A.
+// Per Jacobi-BiCGSTAB iteration that is 4 block barriers; nothing but the
+// row chains runs outside warp 0.  BiCG's A^T row runs beside the A row as a
+// second chain over p~ (published at P + 16).  Rows >= n carry exact +0.0
 // (dinv 0, values 0), as in bc_tmem.cuh.
 #pragma once
 
@@ -116,29 +116,39 @@ __device__ __forceinline__ double lat_row(const LatRow<LMAX>& rw, uint32_t xbase
 // Per-thread state of the split SpMV.
 template <int RV, int LMAX>
 struct LatWarp {
-    double* X;        // this warp's gather region (generic)
+    double* X;        // the gather region (generic): x | 16 zero slots | [p~]
     uint32_t xaddr;   // its shared address
-    double* Y;        // [2][2][P]: buffer, (A, A^T), slot
-    int P, lane;
+    double* Y;        // [2][P]: (A, A^T) row sums
+    int P, lane, T;
     int srow;         // the row this thread computes, -1 none
     int nsteps;
-    int ybuf;
+    volatile int* ctrl;  // the leader's order to the helper warps: kLatSpmv / kLatPair / kLatExit
     LatRow<LMAX> ra;
 };
 
-// y = A v: publish v (owner slots) into the warp's copy, this thread's row, Y exchange.
+constexpr int kLatSpmv = 1, kLatPair = 2, kLatExit = 3;
+
+// The two block barriers of an SpMV: A (operands published, order posted)
+// and B (row sums in Y).  Named, so that the leader and the helpers can reach
+// them from different code.
+__device__ __forceinline__ void lat_bar_a(int T) { asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory"); }
+__device__ __forceinline__ void lat_bar_b(int T) { asm volatile("bar.sync 2, %0;" ::"r"(T) : "memory"); }
+
+// y = A v, called by the leader (warp 0, which holds the Krylov vectors):
+// publish v (owner slots, lane-major, conflict-free), post the order, every
+// warp computes its rows (helpers in lat_helper), the leader reads the
+// products back after the second barrier.
 template <int RV, int LMAX>
 __device__ __forceinline__ void lat_spmv(LatWarp<RV, LMAX>& lw, const double (&v)[RV], double (&y)[RV]) {
 #pragma unroll
     for (int j = 0; j < RV; ++j) lw.X[j * 32 + lw.lane] = v[j];
-    __syncwarp();
+    if (lw.lane == 0) *lw.ctrl = kLatSpmv;
+    lat_bar_a(lw.T);
     const double s = lat_row<LMAX>(lw.ra, lw.xaddr, lw.nsteps);
-    double* Yb = lw.Y + lw.ybuf * 2 * lw.P;
-    if (lw.srow >= 0) Yb[lw.srow] = s;
-    __syncthreads();
+    if (lw.srow >= 0) lw.Y[lw.srow] = s;
+    lat_bar_b(lw.T);
 #pragma unroll
-    for (int j = 0; j < RV; ++j) y[j] = Yb[j * 32 + lw.lane];
-    lw.ybuf ^= 1;
+    for (int j = 0; j < RV; ++j) y[j] = lw.Y[j * 32 + lw.lane];
 }
 
 // BiCG: A p and A^T p~ in one exchange (p~ published at offset P + 16).
@@ -150,21 +160,39 @@ __device__ __forceinline__ void lat_spmv_pair(LatWarp<RV, LMAX>& lw, const LatRo
         lw.X[j * 32 + lw.lane] = pv[j];
         lw.X[lw.P + 16 + j * 32 + lw.lane] = ps[j];
     }
-    __syncwarp();
+    if (lw.lane == 0) *lw.ctrl = kLatPair;
+    lat_bar_a(lw.T);
     const double s0 = lat_row<LMAX>(lw.ra, lw.xaddr, lw.nsteps);
     const double s1 = lat_row<LMAX>(rt, lw.xaddr, lw.nsteps);
-    double* Yb = lw.Y + lw.ybuf * 2 * lw.P;
     if (lw.srow >= 0) {
-        Yb[lw.srow] = s0;
-        Yb[lw.P + lw.srow] = s1;
+        lw.Y[lw.srow] = s0;
+        lw.Y[lw.P + lw.srow] = s1;
     }
-    __syncthreads();
+    lat_bar_b(lw.T);
 #pragma unroll
     for (int j = 0; j < RV; ++j) {
-        ap[j] = Yb[j * 32 + lw.lane];
-        atps[j] = Yb[lw.P + j * 32 + lw.lane];
+        ap[j] = lw.Y[j * 32 + lw.lane];
+        atps[j] = lw.Y[lw.P + j * 32 + lw.lane];
     }
-    lw.ybuf ^= 1;
+}
+
+// Warps 1..: compute their rows of every SpMV the leader posts until it posts kLatExit.
+template <int RV, int LMAX, int ALGO>
+__device__ __forceinline__ void lat_helper(LatWarp<RV, LMAX>& lw, const LatRow<(ALGO == kBiCG ? LMAX : 1)>& rt) {
+    for (;;) {
+        lat_bar_a(lw.T);
+        const int op = *lw.ctrl;
+        if (op == kLatExit) return;
+        const double s0 = lat_row<LMAX>(lw.ra, lw.xaddr, lw.nsteps);
+        if constexpr (ALGO == kBiCG) {
+            if (op == kLatPair) {
+                const double s1 = lat_row<LMAX>(rt, lw.xaddr, lw.nsteps);
+                if (lw.srow >= 0) lw.Y[lw.P + lw.srow] = s1;
+            }
+        }
+        if (lw.srow >= 0) lw.Y[lw.srow] = s0;
+        lat_bar_b(lw.T);
+    }
 }
 
 template <int R, int RV, int LMAX>
@@ -187,18 +215,20 @@ template <int R, int RV, int LMAX, int ALGO>
 __global__ void __launch_bounds__(RV * 32, 1) block_cells_latency_kernel(const LatencyParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int t = threadIdx.x, T = blockDim.x, lane = t % 32, w = t / 32;
-    double* Y = reinterpret_cast<double*>(smem);  // [2][2][P]
+    __shared__ int s_ctrl;
+    double* Y = reinterpret_cast<double*>(smem);  // [2][P]
     LatWarp<RV, LMAX> lw;
     lw.P = p.P;
+    lw.T = T;
     lw.lane = lane;
     lw.Y = Y;
-    lw.X = Y + 4 * p.P + static_cast<size_t>(w) * p.xs;
+    lw.X = Y + 2 * p.P;
     lw.xaddr = static_cast<uint32_t>(__cvta_generic_to_shared(lw.X));
     lw.srow = p.rowof[t];
     lw.nsteps = p.steps[t];
-    lw.ybuf = 0;
-    // Y slots >= n, the zero slots and rows >= n of the copies: +0.0 for good
-    for (int i = t; i < 4 * p.P + T / 32 * p.xs; i += T) Y[i] = 0.0;
+    lw.ctrl = &s_ctrl;
+    // Y slots >= n, the zero slots and rows >= n of the gather region: +0.0 for good
+    for (int i = t; i < 2 * p.P + p.xs; i += T) Y[i] = 0.0;
 #pragma unroll
     for (int e = 0; e < LMAX; ++e) lw.ra.o[e] = p.rxo[e * T + t];
     LatRow<(ALGO == kBiCG ? LMAX : 1)> rt;
@@ -225,6 +255,10 @@ __global__ void __launch_bounds__(RV * 32, 1) block_cells_latency_kernel(const L
                 const int vi = p.tvi[e * T + t];
                 rt.a[e] = vi >= 0 ? __ldg(src + vi) : 0.0;
             }
+        }
+        if (w != 0) {  // helper warps: their rows of every SpMV of this group
+            lat_helper<RV, LMAX, ALGO>(lw, rt);
+            continue;
         }
         double b[RV], x[RV];
 #pragma unroll
@@ -460,7 +494,9 @@ __global__ void __launch_bounds__(RV * 32, 1) block_cells_latency_kernel(const L
                 }
             }
         }
-        if (w == 0) {
+        if (lane == 0) s_ctrl = kLatExit;  // release the helpers
+        lat_bar_a(T);
+        {
             double* xdst = p.x_out + cell0 * p.species;
 #pragma unroll
             for (int j = 0; j < RV; ++j)

@@ -11,11 +11,11 @@
 //
 // The cost is shared-memory wavefronts of the gathers (an LDS.64 per step per
 // warp; per half-warp the largest number of distinct 8-byte slots in one of
-// the 16 bank pairs).  Each warp gathers from its own copy of the vector;
-// padding steps read one of 16 zero slots (one per bank pair), picked per
+// the 16 bank pairs).  All warps gather from the one copy the leader warp
+// publishes; padding steps read one of 16 zero slots (one per bank pair), picked per
 // half-warp step as the least-loaded bank.
 //
-// A warp's gather region (doubles): [0, P) the vector (slot = row), [P, P + 16)
+// The gather region (doubles): [0, P) the vector (slot = row), [P, P + 16)
 // zero slots, and for BiCG p~ at [P + 16, 2P + 16).
 #include <algorithm>
 #include <numeric>
