@@ -18,6 +18,7 @@
 
 #include "bc_block.cuh"
 #include "bc_lu.cuh"
+#include "bc_lu_sm.cuh"
 #include "bc_multi.cuh"
 #include "bc_newton.cuh"
 #include "bc_thread.cuh"
@@ -902,6 +903,25 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
     const bool use_smem_block = blockdiag && smem_blk <= static_cast<size_t>(lu_dyn_max) && lue && *lue == '1';
     if (use_smem_block) smem = smem_blk;
     if (smem > static_cast<size_t>(lu_dyn_max)) fail(BC_ERR_INVALID_ARGUMENT, "LU fallback: group too large");
+    // Blocks that fit in shared memory (bc_lu_sm.cuh): factor kernel + solve
+    // kernel.  Not for the explicit dense reruns and the Multi-cells chain links.
+    const char* lsm = std::getenv("BC_LU_SM");
+    const bool use_sm = !use_smem_block && mode == 0 && !d_chain_flags && !conv && !flip && !later_neg &&
+                        s <= bc::kLuSmMaxRows && kmax <= 32 * 32 &&
+                        bc::lu_sm_factor_smem(s) + 1024 <= static_cast<size_t>(kMaxDynSmem) && !(lsm && *lsm == '0');
+    const int sm_warps = static_cast<int>(std::min<int64_t>(kmax, 32));
+    const size_t sm_solve_smem = bc::lu_sm_solve_smem(nmax, pmax, sm_warps, s);
+    if (use_sm) {
+        static_assert(sizeof(bc::LuEntry) == 24, "LuEntry layout");
+        check_cuda(cudaFuncSetAttribute(bc::lu_sm_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(bc::lu_sm_factor_smem(s))),
+                   "cudaFuncSetAttribute(lu_sm_factor)");
+        check_cuda(cudaFuncSetAttribute(bc::lu_sm_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kMaxDynSmem - 1024),
+                   "cudaFuncSetAttribute(lu_sm_solve)");
+        if (sm_solve_smem > static_cast<size_t>(kMaxDynSmem - 1024))
+            fail(BC_ERR_INVALID_ARGUMENT, "LU fallback: group too large");
+    }
     for (size_t b0 = 0; b0 < ents.size(); b0 += batch) {
         const int cnt = static_cast<int>(std::min<int64_t>(batch, ents.size() - b0));
         bc::LuParams lp{};
@@ -925,9 +945,17 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
         lp.flip = flip;
         lp.later_neg = later_neg;
         lp.chain_flags = d_chain_flags ? d_chain_flags + b0 : nullptr;
-        bc::lu_fallback_kernel<<<cnt, 256, smem, st>>>(lp);
-        check_cuda(cudaGetLastError(), "lu_fallback_kernel launch");
-        ctx->launches++;
+        if (use_sm) {
+            bc::lu_sm_factor_kernel<<<cnt, bc::kLuSmThreads, bc::lu_sm_factor_smem(s), st>>>(lp);
+            check_cuda(cudaGetLastError(), "lu_sm_factor_kernel launch");
+            bc::lu_sm_solve_kernel<<<cnt, 32 * sm_warps, sm_solve_smem, st>>>(lp);
+            check_cuda(cudaGetLastError(), "lu_sm_solve_kernel launch");
+            ctx->launches += 2;
+        } else {
+            bc::lu_fallback_kernel<<<cnt, 256, smem, st>>>(lp);
+            check_cuda(cudaGetLastError(), "lu_fallback_kernel launch");
+            ctx->launches++;
+        }
         ctx->kernels |= BC_KERNEL_LU;
     }
     std::vector<int32_t> status(ents.size());

@@ -551,6 +551,44 @@ __device__ void lu_densify(double* lu, const int ld, const double* vals, const i
     __syncthreads();
 }
 
+// The residual of a group's fallback solution x (shared) through the group's
+// reduction plan (strategies.cpp:48-58; spmv csr.cpp:90-101; plan_reduce_map
+// reduction.hpp:60-79) into g_rms, and status 0.  All threads of the CTA.
+__device__ void lu_group_residual(const LuParams& p, const LuEntry& ent, const int n, const double* vals,
+                                  const double* b, const double* x, double* slots) {
+    const int tid = threadIdx.x, nt = blockDim.x, s = p.species;
+    const int width = p.block_width > 0 ? p.block_width : n;
+    double total = 0.0;
+    for (int b0 = 0, blk = 0; b0 < n; b0 += width, ++blk) {
+        const int len = min(width, n - b0);
+        int P = 1;
+        while (P < len) P <<= 1;
+        __syncthreads();
+        for (int q = tid; q < P; q += nt) {
+            double v = 0.0;
+            if (q < len) {
+                const int i = b0 + q, c = i / s, r = i % s;
+                double acc = 0.0;
+                for (int e = p.row_ptr[r]; e < p.row_ptr[r + 1]; ++e)
+                    acc = __dadd_rn(acc, __dmul_rn(vals[c * p.nnz + e], x[c * s + p.col_idx[e]]));
+                const double ri = __dsub_rn(b[i], acc);
+                v = __dmul_rn(ri, ri);
+            }
+            slots[q] = v;
+        }
+        for (int stride = P / 2; stride >= 1; stride /= 2) {
+            __syncthreads();
+            for (int q = tid; q < stride; q += nt) slots[q] = __dadd_rn(slots[q], slots[q + stride]);
+        }
+        __syncthreads();
+        total = blk == 0 ? slots[0] : __dadd_rn(total, slots[0]);
+    }
+    if (tid == 0) {
+        p.g_rms[ent.gout] = __dsqrt_rn(__ddiv_rn(total, static_cast<double>(n)));
+        p.status[blockIdx.x] = 0;
+    }
+}
+
 __global__ void __launch_bounds__(256, 3) lu_fallback_kernel(const LuParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const LuEntry ent = p.entries[blockIdx.x];
@@ -696,38 +734,7 @@ __global__ void __launch_bounds__(256, 3) lu_fallback_kernel(const LuParams p) {
     double* xo = p.x_out + ent.cell0 * s;
     for (int i = tid; i < n; i += nt) xo[i] = sum[i];
 
-    // residual of the fallback solution through the same plan
-    // (strategies.cpp:48-58; spmv csr.cpp:90-101; plan_reduce_map reduction.hpp:60-79)
-    const int width = p.block_width > 0 ? p.block_width : n;
-    double total = 0.0;
-    for (int b0 = 0, blk = 0; b0 < n; b0 += width, ++blk) {
-        const int len = min(width, n - b0);
-        int P = 1;
-        while (P < len) P <<= 1;
-        __syncthreads();
-        for (int q = tid; q < P; q += nt) {
-            double v = 0.0;
-            if (q < len) {
-                const int i = b0 + q, c = i / s, r = i % s;
-                double acc = 0.0;
-                for (int e = p.row_ptr[r]; e < p.row_ptr[r + 1]; ++e)
-                    acc = __dadd_rn(acc, __dmul_rn(vals[c * p.nnz + e], sum[c * s + p.col_idx[e]]));
-                const double ri = __dsub_rn(b[i], acc);
-                v = __dmul_rn(ri, ri);
-            }
-            slots[q] = v;
-        }
-        for (int stride = P / 2; stride >= 1; stride /= 2) {
-            __syncthreads();
-            for (int q = tid; q < stride; q += nt) slots[q] = __dadd_rn(slots[q], slots[q + stride]);
-        }
-        __syncthreads();
-        total = blk == 0 ? slots[0] : __dadd_rn(total, slots[0]);
-    }
-    if (tid == 0) {
-        p.g_rms[ent.gout] = __dsqrt_rn(__ddiv_rn(total, static_cast<double>(n)));
-        p.status[blockIdx.x] = 0;
-    }
+    lu_group_residual(p, ent, n, vals, b, sum, slots);
 }
 
 }  // namespace bc
