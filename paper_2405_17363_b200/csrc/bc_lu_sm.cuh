@@ -35,7 +35,7 @@ namespace bc {
 
 #ifdef BC_LU_PROFILE
 // phase cycles of CTA 0 (thread 0's clock), tools/luprof.cu
-__device__ unsigned long long bc_lu_prof[16];
+__device__ unsigned long long bc_lu_prof[64];
 #define LU_MARK(i)                                         \
     do {                                                   \
         if (blockIdx.x == 0 && threadIdx.x == 0) {         \
@@ -45,14 +45,33 @@ __device__ unsigned long long bc_lu_prof[16];
         }                                                  \
     } while (0)
 #define LU_PROF_START long long lu_t0_ = clock64()
+#define LU_TICKS_DECL long long lu_tk_[4] = {0, 0, 0, 0}, lu_tq_ = clock64()
+#define LU_TICK(i)                           \
+    do {                                     \
+        const long long now_ = clock64();    \
+        lu_tk_[i] += now_ - lu_tq_;          \
+        lu_tq_ = now_;                       \
+    } while (0)
+#define LU_TICKS_FLUSH                                                              \
+    do {                                                                            \
+        if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)                             \
+            for (int q_ = 0; q_ < 4; ++q_) bc_lu_prof[16 + 4 * (threadIdx.x >> 5) + q_] += lu_tk_[q_]; \
+    } while (0)
 #else
+#define LU_TICKS_DECL
+#define LU_TICK(i) \
+    do {           \
+    } while (0)
+#define LU_TICKS_FLUSH \
+    do {               \
+    } while (0)
 #define LU_MARK(i) \
     do {           \
     } while (0)
 #define LU_PROF_START
 #endif
 
-constexpr int kLuSmThreads = 512;
+constexpr int kLuSmThreads = 256;
 constexpr int kLuSmPanel = 16;
 constexpr int kLuSmMaxRows = 160;                     // blocks up to 160 x 160 (196 KB at 156)
 constexpr int kLuSmColsPerLane = kLuSmMaxRows / 32;  // A22: a lane's 32-strided columns
@@ -60,6 +79,56 @@ constexpr int kLuSmColsPerLane = kLuSmMaxRows / 32;  // A22: a lane's 32-strided
 // leading dimension of a block in shared memory: odd, so a column walk (one
 // row per thread) touches distinct banks
 __host__ __device__ constexpr int lu_sm_ld(int s) { return s | 1; }
+
+// A22 -= L21 U12 over the panel [k0, k1): row bands of 4, one warp per band,
+// lane L holding columns k1 + L + 32q (q < NQ); per element the panel's
+// updates one k at a time in ascending order.  Rows past the edge read the
+// zero padding rows and are never stored.
+template <int NQ>
+__device__ __forceinline__ void lu_sm_a22(double* a, const int n, const int ld, const int k0, const int k1) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int m = n - k1, bands = (m + 3) >> 2, j0 = k1 + lane;
+    bool cok[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) cok[q] = j0 + 32 * q < n;
+    for (int band = warp; band < bands; band += nw) {
+        const int i0 = k1 + 4 * band;
+        double acc[4][NQ];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) acc[r][q] = cok[q] ? a[(i0 + r) * ld + j0 + 32 * q] : 0.0;
+#pragma unroll 4
+        for (int kk = k0; kk < k1; ++kk) {
+            double l[4], u[NQ];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) l[r] = a[(i0 + r) * ld + kk];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) u[q] = cok[q] ? a[kk * ld + j0 + 32 * q] : 0.0;
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) acc[r][q] = __dsub_rn(acc[r][q], __dmul_rn(l[r], u[q]));
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+                if (i0 + r < n && cok[q]) a[(i0 + r) * ld + j0 + 32 * q] = acc[r][q];
+    }
+}
+
+// a / b as __ddiv_rn for b != 0, with a zero dividend answered directly:
+// __ddiv_rn sends a zero quotient down its slow path (~1,000 cycles), and most
+// entries below a sparse block's diagonal are zero.  0 / b (b finite or
+// infinite, nonzero) is a zero with the sign sign(a) ^ sign(b); 0 / NaN is
+// left to __ddiv_rn.
+__device__ __forceinline__ double lu_div(const double a, const double b) {
+    if (a == 0.0 && !isnan(b))
+        return __longlong_as_double((__double_as_longlong(a) ^ __double_as_longlong(b)) &
+                                    static_cast<long long>(0x8000000000000000ull));
+    return __ddiv_rn(a, b);
+}
 
 // Named barrier over the first `count` threads (the row owners).
 __device__ __forceinline__ void lu_sm_bar(int count) { asm volatile("bar.sync 1, %0;" ::"r"(count) : "memory"); }
@@ -79,101 +148,118 @@ __device__ __forceinline__ void lu_sm_bar(int count) { asm volatile("bar.sync 1,
 //     warp per band, each lane a 4 x ceil(m/32) micro-tile of 32-strided
 //     columns (conflict-free loads of the pivot rows, broadcast L loads).
 __device__ bool lu_sm_factor(double* a, const int n, const int ld, int* perm, int* s_piv, int* s_flag,
-                             unsigned* red_u) {
+                             int* posof, double* magk, double* prow_s) {
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-    const int owners = (n + 31) & ~31;  // threads [0, owners): one row each
+    // every warp owns a contiguous run of rows (lanes [0, per)): the panel's
+    // work spreads evenly over the four SM sub-partitions
+    const int nwarps = nt >> 5, per = (n + nwarps - 1) / nwarps;
     LU_PROF_START;
     for (int k0 = 0; k0 < n; k0 += kLuSmPanel) {
         const int k1 = min(n, k0 + kLuSmPanel), K = k1 - k0;
-        // ---- panel: columns [k0, k1), rows [k0, n), by the row owners.  Rows stay
-        // where they are during the panel; each owner tracks its row's position
-        // (the reference's swapped order), which breaks magnitude ties.
-        if (tid < owners) {
-            const int i = tid;  // physical row
-            int pos = i;        // its position
+        // ---- panel: columns [k0, k1), rows [k0, n).  Every thread owns at most one
+        // row and keeps the row's panel part in registers for the whole panel;
+        // rows stay where they are (each owner tracks its row's position, the
+        // reference's swapped order, which breaks magnitude ties).  Per column:
+        // barrier A; every warp scans the published (magnitude, position) pairs
+        // the same way (uniform pivot); the pivot row's owner publishes its
+        // panel part; barrier B; the owners below form l = a_ik / pivot, update
+        // their registers and publish their next candidate.
+        {
+            const bool owner = lane < per && warp * per + lane < n;
+            const int i = owner ? warp * per + lane : n;  // physical row (n: none)
+            int pos = i;                                  // its position
             bool singular = false;
-            // this column's pivot candidate among positions >= k, per warp:
-            // max magnitude (hi word + 1, lo word; 0 = none, NaN skipped), lowest
-            // position; plus whether the row at position k holds a NaN there
-            auto candidate = [&](int k) {
-                unsigned hi = 0u, lo = 0u;
+            double v[kLuSmPanel];
+#pragma unroll
+            for (int jj = 0; jj < kLuSmPanel; ++jj) v[jj] = (owner && jj < K) ? a[i * ld + k0 + jj] : 0.0;
+            if (owner) {
+                posof[i] = pos;
+                magk[i] = fabs(v[0]);
+            }
+            LU_TICKS_DECL;
+#pragma unroll
+            for (int kk = 0; kk < kLuSmPanel; ++kk) {
+                if (kk >= K) break;  // uniform
+                const int k = k0 + kk, cur = kk & 1;
+                __syncthreads();  // A: the candidates of column k are published
+                LU_TICK(0);
+                // the scan: largest magnitude, ties to the lowest position, NaN
+                // skipped; the row at position k and whether it holds a NaN there
+                int pr_[kLuSmMaxRows / 32];
+                double mg_[kLuSmMaxRows / 32];
+#pragma unroll
+                for (int q = 0; q < kLuSmMaxRows / 32; ++q) {
+                    pr_[q] = posof[cur * kLuSmMaxRows + lane + 32 * q];
+                    mg_[q] = magk[cur * kLuSmMaxRows + lane + 32 * q];
+                }
+                double bm = -1.0;
+                unsigned bp = 0x7fffffffu;
+                int brow = 0, krow = -1;
                 bool nan_k = false;
-                if (i < n && pos >= k) {
-                    const double mag = fabs(a[i * ld + k]);
-                    if (isnan(mag)) {
-                        nan_k = pos == k;
-                    } else {
-                        hi = static_cast<unsigned>(__double2hiint(mag)) + 1u;
-                        lo = static_cast<unsigned>(__double2loint(mag));
-                    }
+#pragma unroll
+                for (int q = 0; q < kLuSmMaxRows / 32; ++q) {
+                    const int r = lane + 32 * q;
+                    const bool live = r < n;
+                    const bool isk = live && pr_[q] == k;
+                    krow = isk ? r : krow;
+                    nan_k = nan_k || (isk && isnan(mg_[q]));
+                    const bool better = live && pr_[q] >= k &&
+                                        (mg_[q] > bm || (mg_[q] == bm && static_cast<unsigned>(pr_[q]) < bp));
+                    bm = better ? mg_[q] : bm;
+                    bp = better ? static_cast<unsigned>(pr_[q]) : bp;
+                    brow = better ? r : brow;
                 }
-                const unsigned H = __reduce_max_sync(0xffffffffu, hi);
-                const unsigned L = __reduce_max_sync(0xffffffffu, hi == H ? lo : 0u);
-                const unsigned P = __reduce_min_sync(0xffffffffu, (hi == H && lo == L && H != 0u) ? pos : 0x7fffffff);
-                const unsigned R = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(pos) == P ? i : 0x7fffffff);
-                const unsigned Nk = __ballot_sync(0xffffffffu, nan_k);
-                const unsigned Rk = __reduce_min_sync(0xffffffffu, pos == k ? i : 0x7fffffff);
-                if (lane == 0) {
-                    red_u[warp * 6 + 0] = H;
-                    red_u[warp * 6 + 1] = L;
-                    red_u[warp * 6 + 2] = P;
-                    red_u[warp * 6 + 3] = R;
-                    red_u[warp * 6 + 4] = Nk != 0u;
-                    red_u[warp * 6 + 5] = Rk;
-                }
-            };
-            candidate(k0);
-            for (int k = k0; k < k1; ++k) {
-                lu_sm_bar(owners);
-                // combine the warps' candidates (every warp the same way, uniform)
-                const bool in = lane < owners / 32;
-                const unsigned h = in ? red_u[lane * 6 + 0] : 0u, l = in ? red_u[lane * 6 + 1] : 0u;
-                const unsigned H = __reduce_max_sync(0xffffffffu, h);
-                const unsigned L = __reduce_max_sync(0xffffffffu, h == H ? l : 0u);
-                const unsigned P = __reduce_min_sync(0xffffffffu, (in && h == H && l == L && H != 0u) ? red_u[lane * 6 + 2] : 0x7fffffff);
-                const unsigned R = __reduce_min_sync(0xffffffffu, (in && h == H && l == L && H != 0u) ? red_u[lane * 6 + 3] : 0x7fffffff);
-                const bool nan_k = __any_sync(0xffffffffu, in && red_u[lane * 6 + 4] != 0u);
-                const int rk = static_cast<int>(__reduce_min_sync(0xffffffffu, in ? red_u[lane * 6 + 5] : 0x7fffffff));
+                // (hi, lo) word order = magnitude order for non-negative doubles;
+                // hi | 1 << 31 keeps 0 for "none"
+                const unsigned bh = bm >= 0.0 ? (static_cast<unsigned>(__double2hiint(bm)) | 0x80000000u) : 0u;
+                const unsigned bl = bm >= 0.0 ? static_cast<unsigned>(__double2loint(bm)) : 0u;
+                const unsigned H = __reduce_max_sync(0xffffffffu, bh);
+                const unsigned L = __reduce_max_sync(0xffffffffu, bh == H ? bl : 0u);
+                const unsigned P = __reduce_min_sync(0xffffffffu, (bh == H && bl == L) ? bp : 0x7fffffffu);
+                const unsigned wb = __ballot_sync(0xffffffffu, bh == H && bl == L && bp == P);
+                const unsigned kb = __ballot_sync(0xffffffffu, krow >= 0);
+                const bool nan_any = __any_sync(0xffffffffu, nan_k);
                 // dense_lu.cpp:32-41: largest magnitude in column k, ties to the
                 // lowest position; a NaN at (k, k) fails every comparison: pivot k
-                int pp = k, pr = rk;
-                if (!nan_k) {
-                    if (H == 1u && L == 0u) {  // the largest magnitude is 0: dense_lu.cpp:35
+                int pp = k, pr = __shfl_sync(0xffffffffu, krow, __ffs(kb) - 1);
+                if (!nan_any) {
+                    if (H == 0x80000000u && L == 0u) {  // the largest magnitude is 0: dense_lu.cpp:35
                         singular = true;
                         break;
                     }
                     pp = static_cast<int>(P);
-                    pr = static_cast<int>(R);
+                    pr = __shfl_sync(0xffffffffu, brow, __ffs(wb) - 1);
                 }
-                if (i == 0) {
-                    s_piv[k - k0] = pp;
-                    if (pp != k) {
-                        const int t = perm[k];
-                        perm[k] = perm[pp];
-                        perm[pp] = t;
-                    }
+                LU_TICK(1);
+                if (i == 0) s_piv[kk] = pp;
+                if (i == pr) {  // the pivot row's panel part, for everyone
+#pragma unroll
+                    for (int jj = kk; jj < kLuSmPanel; ++jj) prow_s[cur * kLuSmPanel + jj] = v[jj];
                 }
                 if (pos == pp) pos = k;
                 else if (pos == k) pos = pp;
+                __syncthreads();  // B: the pivot row is published
                 if (i < n && pos > k) {  // rows not yet pivoted: l = a_ik / pivot, the panel's rest
-                    double* row = a + i * ld + k0;
-                    const double* prow = a + pr * ld + k0;
-                    double u[kLuSmPanel], v[kLuSmPanel];
+                    double u[kLuSmPanel];
 #pragma unroll
-                    for (int jj = 0; jj < kLuSmPanel; ++jj) {
-                        u[jj] = prow[jj];
-                        v[jj] = row[jj];
-                    }
-                    const double lk = __ddiv_rn(row[k - k0], prow[k - k0]);
-                    row[k - k0] = lk;
+                    for (int jj = kk; jj < kLuSmPanel; ++jj) u[jj] = prow_s[cur * kLuSmPanel + jj];
+                    const double lk = lu_div(v[kk], u[kk]);
+                    v[kk] = lk;
 #pragma unroll
-                    for (int jj = 0; jj < kLuSmPanel; ++jj)
-                        if (k0 + jj > k && jj < K) row[jj] = __dsub_rn(v[jj], __dmul_rn(lk, u[jj]));
+                    for (int jj = kk + 1; jj < kLuSmPanel; ++jj)
+                        if (jj < K) v[jj] = __dsub_rn(v[jj], __dmul_rn(lk, u[jj]));
                 }
-                if (k + 1 < k1) {
-                    __syncwarp();
-                    candidate(k + 1);  // reads only the owner's own row
+                if (kk + 1 < K && i < n) {  // the next column's candidate (buffer cur ^ 1)
+                    posof[(cur ^ 1) * kLuSmMaxRows + i] = pos;
+                    magk[(cur ^ 1) * kLuSmMaxRows + i] = fabs(v[kk + 1 < kLuSmPanel ? kk + 1 : kk]);
                 }
+                LU_TICK(2);
+            }
+            LU_TICKS_FLUSH;
+            if (owner) {
+#pragma unroll
+                for (int jj = 0; jj < kLuSmPanel; ++jj)
+                    if (jj < K) a[i * ld + k0 + jj] = v[jj];
             }
             if (i == 0) *s_flag = singular ? 1 : 0;
         }
@@ -181,7 +267,14 @@ __device__ bool lu_sm_factor(double* a, const int n, const int ld, int* perm, in
         LU_MARK(0);
         if (*s_flag) return false;
         // ---- the panel's row swaps, in order, on every column (the panel's too:
-        // its rows stayed in place)
+        // its rows stayed in place), and on perm
+        if (tid == nt - 1)
+            for (int kk = 0; kk < K; ++kk) {
+                const int pr = s_piv[kk];
+                const int t = perm[k0 + kk];
+                perm[k0 + kk] = perm[pr];
+                perm[pr] = t;
+            }
         for (int c = tid; c < n; c += nt) {
             for (int kk = 0; kk < K; ++kk) {
                 const int pr = s_piv[kk];
@@ -212,39 +305,13 @@ __device__ bool lu_sm_factor(double* a, const int n, const int ld, int* perm, in
         __syncthreads();
         LU_MARK(2);
         // ---- A22: rows and columns [k1, n); row bands of 4, one warp per band,
-        // lane L holding columns k1 + L + 32q (q < kLuSmColsPerLane); rows past
-        // the edge read the zero padding rows and are never stored
-        {
-            const int m = n - k1, bands = (m + 3) >> 2;
-            for (int band = warp; band < bands; band += nt >> 5) {
-                const int i0 = k1 + 4 * band, j0 = k1 + lane;
-                bool cok[kLuSmColsPerLane];
-#pragma unroll
-                for (int q = 0; q < kLuSmColsPerLane; ++q) cok[q] = j0 + 32 * q < n;
-                double acc[4][kLuSmColsPerLane];
-#pragma unroll
-                for (int r = 0; r < 4; ++r)
-#pragma unroll
-                    for (int q = 0; q < kLuSmColsPerLane; ++q) acc[r][q] = cok[q] ? a[(i0 + r) * ld + j0 + 32 * q] : 0.0;
-#pragma unroll 4
-                for (int kk = k0; kk < k1; ++kk) {
-                    double l[4], u[kLuSmColsPerLane];
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) l[r] = a[(i0 + r) * ld + kk];
-#pragma unroll
-                    for (int q = 0; q < kLuSmColsPerLane; ++q) u[q] = cok[q] ? a[kk * ld + j0 + 32 * q] : 0.0;
-#pragma unroll
-                    for (int r = 0; r < 4; ++r)
-#pragma unroll
-                        for (int q = 0; q < kLuSmColsPerLane; ++q)
-                            acc[r][q] = __dsub_rn(acc[r][q], __dmul_rn(l[r], u[q]));
-                }
-#pragma unroll
-                for (int r = 0; r < 4; ++r)
-#pragma unroll
-                    for (int q = 0; q < kLuSmColsPerLane; ++q)
-                        if (i0 + r < n && cok[q]) a[(i0 + r) * ld + j0 + 32 * q] = acc[r][q];
-            }
+        // lane L holding columns k1 + L + 32q (q < ceil(m / 32))
+        switch ((n - k1 + 31) >> 5) {
+            case 1: lu_sm_a22<1>(a, n, ld, k0, k1); break;
+            case 2: lu_sm_a22<2>(a, n, ld, k0, k1); break;
+            case 3: lu_sm_a22<3>(a, n, ld, k0, k1); break;
+            case 4: lu_sm_a22<4>(a, n, ld, k0, k1); break;
+            default: lu_sm_a22<kLuSmColsPerLane>(a, n, ld, k0, k1); break;
         }
         __syncthreads();
         LU_MARK(3);
@@ -275,7 +342,9 @@ __host__ __device__ constexpr size_t lu_sm_factor_smem(int s) {
 __global__ void __launch_bounds__(kLuSmThreads, 1) lu_sm_factor_kernel(const LuParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int s_piv[kLuSmPanel], s_flag;
-    __shared__ unsigned red_u[6 * kLuSmMaxRows / 32];
+    __shared__ int posof[2 * kLuSmMaxRows];
+    __shared__ double prow_s[2 * kLuSmPanel];
+    __shared__ double magk[2 * kLuSmMaxRows];
     const LuEntry ent = p.entries[blockIdx.x];
     const int s = p.species, ld = lu_sm_ld(s), tid = threadIdx.x, nt = blockDim.x;
     double* a = reinterpret_cast<double*>(smem_raw);
@@ -309,7 +378,7 @@ __global__ void __launch_bounds__(kLuSmThreads, 1) lu_sm_factor_kernel(const LuP
             }
         __syncthreads();
         LU_MARK(4);
-        if (!lu_sm_factor(a, s, ld, perm, s_piv, &s_flag, red_u)) {
+        if (!lu_sm_factor(a, s, ld, perm, s_piv, &s_flag, posof, magk, prow_s)) {
             if (tid == 0) p.status[blockIdx.x] = 1;
             return;
         }

@@ -43,10 +43,10 @@ int main(int argc, char** argv) {
     const size_t smem = bc::lu_sm_factor_smem(species);
     cudaFuncSetAttribute(bc::lu_sm_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const char* names[14] = {"panel", "row swaps", "U12", "A22", "densify", "factor total", "checks",
-                             "forward", "park factors", " panel: bar 1", " panel: bar 2", " panel: l + update",
-                             " panel: candidate", " panel: pivot+swap"};
+                             "forward", "park factors", " panel: bar", " panel: scan+pivot", " panel: update+publish",
+                             " panel: scan (loads+local)", " -"};
     for (int rep = 0; rep < 2; ++rep) {
-        unsigned long long z[16] = {0};
+        unsigned long long z[64] = {0};
         cudaMemcpyToSymbol(bc::bc_lu_prof, z, sizeof z);
         cudaEvent_t a, b;
         cudaEventCreate(&a);
@@ -57,13 +57,18 @@ int main(int argc, char** argv) {
         cudaEventSynchronize(b);
         float ms;
         cudaEventElapsedTime(&ms, a, b);
-        unsigned long long h[16];
+        unsigned long long h[64];
         cudaMemcpyFromSymbol(h, bc::bc_lu_prof, sizeof h);
         int st = 0;
         cudaMemcpy(&st, p.status, 4, cudaMemcpyDeviceToHost);
         printf("rep %d: %d CTAs x %d blocks, %.3f ms, status %d (%s)\n", rep, ctas, k, ms, st,
                cudaGetErrorString(cudaGetLastError()));
-        for (int i = 0; i < 14; ++i) printf("  %-16s %10.0f cycles/block\n", names[i], double(h[i]) / k);
+        for (int i = 0; i < 9; ++i) printf("  %-16s %10.0f cycles/block\n", names[i], double(h[i]) / k);
+        for (int w = 0; w < 12; ++w)
+            if (h[16 + 4 * w] + h[17 + 4 * w] + h[18 + 4 * w] + h[19 + 4 * w])
+                printf("  warp %2d panel: bar-return %8.0f  pivot %8.0f  update %8.0f  scan %8.0f\n", w,
+                       double(h[16 + 4 * w]) / k, double(h[17 + 4 * w]) / k, double(h[18 + 4 * w]) / k,
+                       double(h[19 + 4 * w]) / k);
     }
     return 0;
 }
