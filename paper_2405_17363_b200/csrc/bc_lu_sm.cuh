@@ -168,7 +168,6 @@ __device__ bool lu_sm_factor(double* a, const int n, const int ld, int* perm, in
             const bool owner = lane < per && warp * per + lane < n;
             const int i = owner ? warp * per + lane : n;  // physical row (n: none)
             int pos = i;                                  // its position
-            bool singular = false;
             double v[kLuSmPanel];
 #pragma unroll
             for (int jj = 0; jj < kLuSmPanel; ++jj) v[jj] = (owner && jj < K) ? a[i * ld + k0 + jj] : 0.0;
@@ -176,6 +175,7 @@ __device__ bool lu_sm_factor(double* a, const int n, const int ld, int* perm, in
                 posof[i] = pos;
                 magk[i] = fabs(v[0]);
             }
+            if (tid == 0) *s_flag = 0;  // read after barrier B at the earliest
             LU_TICKS_DECL;
 #pragma unroll
             for (int kk = 0; kk < kLuSmPanel; ++kk) {
@@ -183,6 +183,14 @@ __device__ bool lu_sm_factor(double* a, const int n, const int ld, int* perm, in
                 const int k = k0 + kk, cur = kk & 1;
                 __syncthreads();  // A: the candidates of column k are published
                 LU_TICK(0);
+                // a warp whose rows are all pivoted has nothing left in this panel
+                // but the barriers (uniform per warp)
+                if (!__any_sync(0xffffffffu, i < n && pos >= k)) {
+                    __syncthreads();  // B
+                    if (*s_flag) break;  // singular (uniform)
+                    if (kk + 1 < K && i < n) posof[(cur ^ 1) * kLuSmMaxRows + i] = pos;  // (< k: never a candidate)
+                    continue;
+                }
                 // the scan: largest magnitude, ties to the lowest position, NaN
                 // skipped; the row at position k and whether it holds a NaN there
                 int pr_[kLuSmMaxRows / 32];
@@ -224,15 +232,16 @@ __device__ bool lu_sm_factor(double* a, const int n, const int ld, int* perm, in
                 int pp = k, pr = __shfl_sync(0xffffffffu, krow, __ffs(kb) - 1);
                 if (!nan_any) {
                     if (H == 0x80000000u && L == 0u) {  // the largest magnitude is 0: dense_lu.cpp:35
-                        singular = true;
+                        if (lane == 0) *s_flag = 1;
+                        __syncthreads();  // B: every thread then leaves (below)
                         break;
                     }
                     pp = static_cast<int>(P);
                     pr = __shfl_sync(0xffffffffu, brow, __ffs(wb) - 1);
                 }
                 LU_TICK(1);
-                if (i == 0) s_piv[kk] = pp;
                 if (i == pr) {  // the pivot row's panel part, for everyone
+                    s_piv[kk] = pp;
 #pragma unroll
                     for (int jj = kk; jj < kLuSmPanel; ++jj) prow_s[cur * kLuSmPanel + jj] = v[jj];
                 }
@@ -261,7 +270,6 @@ __device__ bool lu_sm_factor(double* a, const int n, const int ld, int* perm, in
                 for (int jj = 0; jj < kLuSmPanel; ++jj)
                     if (jj < K) a[i * ld + k0 + jj] = v[jj];
             }
-            if (i == 0) *s_flag = singular ? 1 : 0;
         }
         __syncthreads();
         LU_MARK(0);
