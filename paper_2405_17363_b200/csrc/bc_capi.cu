@@ -968,7 +968,9 @@ void run_lu(bc_ctx* ctx, const std::vector<bc::LuEntry>& ents, const double* d_v
         if (status[i] == 2) dense.push_back(ents[i]);
     }
     if (!dense.empty()) {
-        if (!blockdiag) fail(BC_ERR_CUDA, "lu_fallback_kernel: unexpected status");
+        // one-cell groups reach status 2 only from the shared-memory kernels
+        // (use_sm); the scratch kernel runs them densely already
+        if (!blockdiag && !use_sm) fail(BC_ERR_CUDA, "lu_fallback_kernel: unexpected status");
         run_lu(ctx, dense, d_values, d_rhs, d_x, g_rms, s, nnz, block_width, st, 1);
     }
 }

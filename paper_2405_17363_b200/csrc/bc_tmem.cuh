@@ -314,11 +314,47 @@ __device__ __forceinline__ void tmem_reduce(const double (&vals)[NV][RV], double
         for (int v = 0; v < NV; ++v) out[v] = dadd(out[v], __shfl_xor_sync(0xffffffffu, out[v], mask));
 }
 
+// Two values through the xor butterfly with 6 instead of 10 64-bit shuffles:
+// at mask 16 each lane sends the value its partner keeps -- lanes < 16 keep
+// value 0, lanes >= 16 value 1 -- so masks 8..1 run one value per lane, and a
+// last xor-16 shuffle hands every lane the other half's result.  Every dadd
+// has the operands of tmem_reduce's butterfly (own value first, partner
+// second; the xor butterfly leaves the same bits in every lane), so the
+// results are bit-identical.  Measured neutral on the bench (586.3k both
+// ways, B200): the kernel is not bound by its shuffles.  The chain is one
+// shuffle longer, so the latency kernel keeps tmem_reduce.
+template <int R, int RV>
+__device__ __forceinline__ void tmem_reduce2(const double (&vals)[2][RV], double (&out)[2]) {
+    static_assert(R >= 1 && RV <= R, "row slots beyond the tree");
+    double o[2];
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+        double t[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) t[j] = j < RV ? vals[v][j < RV ? j : 0] : 0.0;
+#pragma unroll
+        for (int stride = R / 2; stride >= 1; stride /= 2)
+#pragma unroll
+            for (int j = 0; j < stride; ++j) t[j] = dadd(t[j], t[j + stride]);
+        o[v] = t[0];
+    }
+    const bool upper = (threadIdx.x & 16u) != 0;
+    double keep = upper ? o[1] : o[0];
+    keep = dadd(keep, __shfl_xor_sync(0xffffffffu, upper ? o[0] : o[1], 16));
+#pragma unroll
+    for (int mask = 8; mask >= 1; mask >>= 1) keep = dadd(keep, __shfl_xor_sync(0xffffffffu, keep, mask));
+    const double other = __shfl_xor_sync(0xffffffffu, keep, 16);
+    out[0] = upper ? other : keep;
+    out[1] = upper ? keep : other;
+}
+
 // W > 1: team_reduce (per-lane tree, one cross-warp step through shared
 // memory, xor butterfly -- the same tree order for any team width).
 template <int NV, int W, int R, int RV>
 __device__ __forceinline__ void tmem_reduce(Ctx<W, R, RV>& c, const double (&vals)[NV][RV], double (&out)[NV]) {
-    if constexpr (W == 1)
+    if constexpr (W == 1 && NV == 2)
+        tmem_reduce2<R, RV>(vals, out);
+    else if constexpr (W == 1)
         tmem_reduce<NV, R, RV>(vals, out);
     else
         team_reduce<NV>(c, vals, out);
