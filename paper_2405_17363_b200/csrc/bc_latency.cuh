@@ -309,13 +309,14 @@ __global__ void __launch_bounds__(RV * 32, 1) block_cells_latency_kernel(const L
             }
             if (!conv) {
                 double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
+                double aw = ddiv(alpha, omega);  // alpha/omega of beta, computed as soon as omega is known
 #ifdef BC_LAT_PROFILE
                 long long prof_t = clock64(), prof_acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
                 for (int it = 1; it <= p.max_iter; ++it) {
                     const double rho = rho_next;
                     if (scalar_breaks(rho)) { brk = true; break; }
-                    const double beta = dmul(ddiv(rho, rho_prev), ddiv(alpha, omega));
+                    const double beta = dmul(ddiv(rho, rho_prev), aw);
                     double y[RV];
 #pragma unroll
                     for (int j = 0; j < RV; ++j) {
@@ -362,6 +363,7 @@ __global__ void __launch_bounds__(RV * 32, 1) block_cells_latency_kernel(const L
                     LAT_MARK(5);
                     if (tt != 0.0 && scalar_breaks(tt)) { brk = true; break; }
                     omega = tt == 0.0 ? 0.0 : ddiv(ts, tt);
+                    aw = ddiv(alpha, omega);  // next beta's factor, off the critical path
 #pragma unroll
                     for (int j = 0; j < RV; ++j) {
                         x[j] = dadd(x[j], dmul(omega, z[j]));

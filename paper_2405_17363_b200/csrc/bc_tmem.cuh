@@ -542,10 +542,11 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
             }
             if (!conv) {
                 double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
+                double aw = ddiv(alpha, omega);  // alpha/omega of beta, computed as soon as omega is known
                 for (int it = 1; it <= p.max_iter; ++it) {
                     const double rho = rho_next;
                     if (scalar_breaks(rho)) { brk = true; break; }
-                    const double beta = dmul(ddiv(rho, rho_prev), ddiv(alpha, omega));
+                    const double beta = dmul(ddiv(rho, rho_prev), aw);
                     double y[RV], dinv[RV];
                     tm_load_vec(tw.dcol, dinv);
     #pragma unroll
@@ -588,6 +589,7 @@ __global__ void __launch_bounds__(NT, 1) block_cells_tmem_kernel(const TmemParam
                     }
                     if (tt != 0.0 && scalar_breaks(tt)) { brk = true; break; }
                     omega = tt == 0.0 ? 0.0 : ddiv(ts, tt);
+                    aw = ddiv(alpha, omega);  // next beta's factor, off the critical path
                     double dinv3[RV];
                     tm_load_vec(tw.dcol, dinv3);
     #pragma unroll
