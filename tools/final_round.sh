@@ -14,6 +14,12 @@ bash tools/round_configs.sh $TAG
 bash tools/profile_round.sh $TAG
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29561 \
     bench.py --gpus 2 --cells 20000 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_n2_$TAG.json 2> gpurun_out/bench_n2_$TAG.err
+# small batches (latency kernel phase profile + sweep) and the Block-cells(N)
+# launch list (LU fallback share of the step)
+./tools/latprof.bin > gpurun_out/latprof_$TAG.txt 2>&1
+CELLS=1,10,100,148,1000,10000 timeout 600 python tools/latency_sweep.py > gpurun_out/latsweep_$TAG.jsonl 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bcN_$TAG.csv \
+    python bench.py --strategy block-cells-N --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-parity --no-companion --no-dropin > /dev/null 2>&1
 bash tools/sanitize.sh > /dev/null 2>&1
 timeout 900 python tools/fuzz_gpu.py 600 43 > gpurun_out/fuzz_$TAG.txt 2>&1; tail -1 gpurun_out/fuzz_$TAG.txt
 ls gpurun_out | wc -l
