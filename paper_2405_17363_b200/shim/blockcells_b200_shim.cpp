@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -249,32 +250,110 @@ SolveReport run_gpu(const BatchedSystem& system, int strategy, std::optional<std
     double* values = st_values.get(sizeof(double) * cells * nnz);
     double* rhs = st_rhs.get(sizeof(double) * cells * s);
     double* x = st_x.get(sizeof(double) * cells * s);
-    parallel_for(cells, threads, [&](std::size_t c0, std::size_t c1) {
-        for (std::size_t c = c0; c < c1; ++c) {
-            std::memcpy(values + c * nnz, system.per_cell_matrices[c].values.data(), sizeof(double) * nnz);
-            std::memcpy(rhs + c * s, system.per_cell_rhs[c].data(), sizeof(double) * s);
-        }
-    });
     std::vector<int32_t> iters(n_groups);
-    bc_report rep{};
-    {
-        const int st = set ? bc_devset_solve(set, &prm, values, rhs, x, iters.data(), nullptr, nullptr, &rep)
-                           : bc_solve(ctx, &prm, values, rhs, x, iters.data(), nullptr, nullptr, &rep);
-        if (st != BC_OK) raise_status(st, set ? bc_devset_last_error(set) : bc_last_error(ctx));
-    }
-
     SolveReport report;  // merge_groups, strategies.cpp:71-87
     report.strategy = kind;
+    report.per_cell_x.resize(cells);
+    auto pack = [&](std::size_t a, std::size_t b) {
+        parallel_for(b - a, threads, [&](std::size_t c0, std::size_t c1) {
+            for (std::size_t c = a + c0; c < a + c1; ++c) {
+                std::memcpy(values + c * nnz, system.per_cell_matrices[c].values.data(), sizeof(double) * nnz);
+                std::memcpy(rhs + c * s, system.per_cell_rhs[c].data(), sizeof(double) * s);
+            }
+        });
+    };
+    auto unpack = [&](std::size_t a, std::size_t b) {
+        parallel_for(b - a, threads, [&](std::size_t c0, std::size_t c1) {
+            for (std::size_t c = a + c0; c < a + c1; ++c) report.per_cell_x[c].assign(x + c * s, x + (c + 1) * s);
+        });
+    };
+    // Independent groups (One-cell, Block-cells(k), thread-per-cell) on one
+    // device: the batch in kPieces group-aligned pieces, each solved on the GPU
+    // (a solver thread) while the host packs the next and unpacks the previous,
+    // so packing and unpacking leave the critical path.  Each piece is its own
+    // bc_solve over disjoint groups, folded below as merge_groups folds groups:
+    // outputs bit-identical to one call.  BLOCKCELLS_B200_OVERLAP=0: one call.
+    constexpr int kPieces = 4;
+    constexpr std::size_t kOverlapMinCells = 16384;
+    const char* ov = std::getenv("BLOCKCELLS_B200_OVERLAP");
+    const bool independent = strategy == BC_STRATEGY_BLOCK_CELLS || strategy == BC_STRATEGY_ONE_CELL ||
+                             strategy == BC_STRATEGY_THREAD_PER_CELL;
+    const std::size_t kg = strategy == BC_STRATEGY_BLOCK_CELLS ? static_cast<std::size_t>(cpb) : 1;
+    const int pieces = (!set && independent && kg >= 1 && cells >= kOverlapMinCells && !(ov && *ov == '0'))
+                           ? kPieces : 1;
+    std::vector<std::size_t> cut(pieces + 1, cells);
+    for (int b = 0; b < pieces; ++b) cut[b] = (cells * b / pieces) / kg * kg;
+    std::vector<bc_report> reps(pieces);
+    if (pieces == 1) {
+        pack(0, cells);
+        const int st = set ? bc_devset_solve(set, &prm, values, rhs, x, iters.data(), nullptr, nullptr, &reps[0])
+                           : bc_solve(ctx, &prm, values, rhs, x, iters.data(), nullptr, nullptr, &reps[0]);
+        if (st != BC_OK) raise_status(st, set ? bc_devset_last_error(set) : bc_last_error(ctx));
+        unpack(0, cells);
+    } else {
+        std::mutex mu;
+        std::condition_variable cv;
+        int packed = 0, solved = 0, status = BC_OK;
+        std::string err;
+        std::thread solver([&] {
+            for (int b = 0; b < pieces; ++b) {
+                {
+                    std::unique_lock<std::mutex> lk(mu);
+                    cv.wait(lk, [&] { return packed > b; });
+                }
+                int st = BC_OK;
+                if (cut[b + 1] > cut[b]) {
+                    bc_solve_params sub = prm;
+                    sub.cells = static_cast<int64_t>(cut[b + 1] - cut[b]);
+                    st = bc_solve(ctx, &sub, values + cut[b] * nnz, rhs + cut[b] * s, x + cut[b] * s,
+                                  iters.data() + cut[b] / kg, nullptr, nullptr, &reps[b]);
+                }
+                std::lock_guard<std::mutex> lk(mu);
+                if (st != BC_OK) {
+                    status = st;
+                    err = bc_last_error(ctx);
+                    solved = pieces;  // the main thread stops waiting
+                } else {
+                    solved = b + 1;
+                }
+                cv.notify_all();
+                if (st != BC_OK) return;
+            }
+        });
+        for (int b = 0; b < pieces; ++b) {
+            pack(cut[b], cut[b + 1]);
+            std::lock_guard<std::mutex> lk(mu);
+            packed = b + 1;
+            cv.notify_all();
+        }
+        for (int b = 0; b < pieces; ++b) {
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return solved > b; });
+                if (status != BC_OK) break;
+            }
+            unpack(cut[b], cut[b + 1]);
+        }
+        solver.join();
+        if (status != BC_OK) raise_status(status, err.c_str());
+    }
+    bc_report rep{};  // the pieces folded in group order (bc_devset_solve's merge)
+    rep.cells_per_block = cpb;
+    for (int b = 0; b < pieces; ++b) {
+        if (cut[b + 1] == cut[b] && pieces > 1) continue;
+        const bc_report& q = reps[b];
+        rep.iterations_sum += q.iterations_sum;
+        rep.iterations_effective = std::max(rep.iterations_effective, q.iterations_effective);
+        rep.max_residual_rms = std::max(rep.max_residual_rms, q.max_residual_rms);
+        rep.breakdown_fallbacks += q.breakdown_fallbacks;
+        if (pieces == 1) rep.cells_per_block = q.cells_per_block;
+    }
     report.cells_per_block = rep.cells_per_block;
     report.per_block_iterations.assign(iters.begin(), iters.end());
     report.iterations_sum = static_cast<std::size_t>(rep.iterations_sum);
     report.iterations_effective = static_cast<std::size_t>(rep.iterations_effective);
     report.max_residual_rms = rep.max_residual_rms;
     report.breakdown_fallbacks = static_cast<std::size_t>(rep.breakdown_fallbacks);
-    report.per_cell_x.resize(cells);
-    parallel_for(cells, threads, [&](std::size_t c0, std::size_t c1) {
-        for (std::size_t c = c0; c < c1; ++c) report.per_cell_x[c].assign(x + c * s, x + (c + 1) * s);
-    });
     report.wall_time_ns = elapsed_ns(start);
     return report;
 }

@@ -12,6 +12,7 @@
 // (bicgstab | unset = BiCG); devices: BLOCKCELLS_B200_DEVICES (shim).
 //   dropin_bench <cells> <steps> <warmup> [species] [h] [tol] [max_iter] [workers]
 #include <chrono>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -59,6 +60,7 @@ int main(int argc, char** argv) {
     cfg.cells_per_block = 1;
     double total = 0.0, rep_total = 0.0;
     std::size_t it_sum = 0, fallbacks = 0;
+    uint64_t digest = 0;
     for (int i = 0; i < warmup + steps; ++i) {
         const auto t0 = std::chrono::steady_clock::now();
         const SolveReport r = run_strategy(sys, cfg, DeviceSpec{}, tol, max_iter, workers);
@@ -68,6 +70,19 @@ int main(int argc, char** argv) {
             rep_total += r.wall_time_ns * 1e-9;
             it_sum = r.iterations_sum;
             fallbacks = r.breakdown_fallbacks;
+            // FNV-1a over every output bit: x of every cell, per-group
+            // iterations, the report's max rms and effective iterations
+            uint64_t h = 1469598103934665603ull;
+            auto mix = [&](const void* p, std::size_t n) {
+                const unsigned char* b = static_cast<const unsigned char*>(p);
+                for (std::size_t q = 0; q < n; ++q) h = (h ^ b[q]) * 1099511628211ull;
+            };
+            for (const auto& xc : r.per_cell_x) mix(xc.data(), sizeof(double) * xc.size());
+            for (std::size_t g : r.per_block_iterations) mix(&g, sizeof g);
+            mix(&r.max_residual_rms, sizeof r.max_residual_rms);
+            mix(&r.iterations_effective, sizeof r.iterations_effective);
+            mix(&r.iterations_sum, sizeof r.iterations_sum);
+            digest = h;
         }
     }
     const char* algo = std::getenv("BLOCKCELLS_B200_ALGO");
@@ -75,9 +90,10 @@ int main(int argc, char** argv) {
                 "\"h\": %g, \"tol\": %g, \"max_iter\": %zu, \"value\": %.3f, \"unit\": \"cell-solves/s\", \"ms_per_step\": %.3f, "
                 "\"report_wall_ms_per_step\": %.3f, \"iterations_sum\": %zu, \"breakdown_fallbacks\": %zu, "
                 "\"entry\": \"blockcells::run_strategy (strategies.hpp:80-82) over the drop-in shim\", "
-                "\"input_bytes_per_step\": %ld}\n",
+                "\"input_bytes_per_step\": %ld, \"output_digest\": \"%016llx\"}\n",
                 cells, species, steps, warmup, algo ? algo : "bicg", h, tol, max_iter, cells * steps / total, 1e3 * total / steps,
-                1e3 * rep_total / steps, it_sum, fallbacks, static_cast<long>(cells) * (nnz + species) * 8);
+                1e3 * rep_total / steps, it_sum, fallbacks, static_cast<long>(cells) * (nnz + species) * 8,
+                static_cast<unsigned long long>(digest));
     bcw_mechanism_destroy(m);
     return 0;
 }
