@@ -20,6 +20,6 @@ timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --mast
 CELLS=1,10,100,148,1000,10000 timeout 600 python tools/latency_sweep.py > gpurun_out/latsweep_$TAG.jsonl 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bcN_$TAG.csv \
     python bench.py --strategy block-cells-N --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-parity --no-companion --no-dropin > /dev/null 2>&1
-bash tools/sanitize.sh > /dev/null 2>&1
+# (compute-sanitizer runs are closed on this GPU pool since round 2e: profiles/round2_sanitize_*.txt are the last)
 timeout 900 python tools/fuzz_gpu.py 600 43 > gpurun_out/fuzz_$TAG.txt 2>&1; tail -1 gpurun_out/fuzz_$TAG.txt
 ls gpurun_out | wc -l
