@@ -294,12 +294,14 @@ SolveReport run_gpu(const BatchedSystem& system, int strategy, std::optional<std
         std::mutex mu;
         std::condition_variable cv;
         int packed = 0, solved = 0, status = BC_OK;
+        bool cancel = false;  // the host side threw: the solver thread stops
         std::string err;
         std::thread solver([&] {
             for (int b = 0; b < pieces; ++b) {
                 {
                     std::unique_lock<std::mutex> lk(mu);
-                    cv.wait(lk, [&] { return packed > b; });
+                    cv.wait(lk, [&] { return packed > b || cancel; });
+                    if (cancel) return;
                 }
                 int st = BC_OK;
                 if (cut[b + 1] > cut[b]) {
@@ -320,19 +322,29 @@ SolveReport run_gpu(const BatchedSystem& system, int strategy, std::optional<std
                 if (st != BC_OK) return;
             }
         });
-        for (int b = 0; b < pieces; ++b) {
-            pack(cut[b], cut[b + 1]);
-            std::lock_guard<std::mutex> lk(mu);
-            packed = b + 1;
-            cv.notify_all();
-        }
-        for (int b = 0; b < pieces; ++b) {
-            {
-                std::unique_lock<std::mutex> lk(mu);
-                cv.wait(lk, [&] { return solved > b; });
-                if (status != BC_OK) break;
+        try {
+            for (int b = 0; b < pieces; ++b) {
+                pack(cut[b], cut[b + 1]);
+                std::lock_guard<std::mutex> lk(mu);
+                packed = b + 1;
+                cv.notify_all();
             }
-            unpack(cut[b], cut[b + 1]);
+            for (int b = 0; b < pieces; ++b) {
+                {
+                    std::unique_lock<std::mutex> lk(mu);
+                    cv.wait(lk, [&] { return solved > b; });
+                    if (status != BC_OK) break;
+                }
+                unpack(cut[b], cut[b + 1]);
+            }
+        } catch (...) {
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                cancel = true;
+                cv.notify_all();
+            }
+            solver.join();
+            throw;
         }
         solver.join();
         if (status != BC_OK) raise_status(status, err.c_str());
