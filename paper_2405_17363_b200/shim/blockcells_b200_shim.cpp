@@ -210,11 +210,39 @@ void check_system(const BatchedSystem& system, std::size_t threads) {
         if (bad_b[t] != none) throw std::invalid_argument("batched system: rhs dimension");
 }
 
+// Everything BatchedSystem::check tests except the per-cell pattern
+// comparison (the 1.7k-index compare per cell that dominates it): true when
+// it all holds.  Then the only error check() can still throw is the pattern
+// mismatch of the lowest such cell, which run_gpu tests piece by piece
+// (pack_checked) before each piece is handed to the GPU.
+bool light_check(const BatchedSystem& system, std::size_t threads) {
+    if (system.cells == 0 || system.species == 0 || system.per_cell_matrices.size() != system.cells ||
+        system.per_cell_rhs.size() != system.cells)
+        return false;
+    const std::size_t n = system.cells;
+    std::vector<char> ok(std::max<std::size_t>(1, std::min(threads, n / 256 + 1)), 1);
+    const std::size_t nt = ok.size();
+    std::vector<std::thread> pool;
+    for (std::size_t t = 0; t < nt; ++t)
+        pool.emplace_back([&, t] {
+            for (std::size_t c = n * t / nt; c < n * (t + 1) / nt && ok[t]; ++c) {
+                const CsrMatrix& m = system.per_cell_matrices[c];
+                ok[t] = m.n_rows == system.species && m.n_cols == system.species &&
+                        system.per_cell_rhs[c].size() == system.species;
+            }
+        });
+    for (std::thread& th : pool) th.join();
+    return std::all_of(ok.begin(), ok.end(), [](char v) { return v != 0; });
+}
+
 SolveReport run_gpu(const BatchedSystem& system, int strategy, std::optional<std::size_t> k,
                     const DeviceSpec& device, double tol, std::size_t max_iter, Strategy kind,
                     std::size_t worker_count = 1) {
     const std::size_t threads = host_threads(worker_count);
-    check_system(system, threads);  // strategies.cpp:91-107
+    // strategies.cpp:91-107: anything but a pattern mismatch is found here and
+    // thrown exactly as check() does; pattern mismatches below, before the
+    // cells concerned are solved, lowest cell first
+    if (!light_check(system, threads)) check_system(system, threads);
     const auto start = Clock::now();
     bc_devset* set = device_set();
     bc_ctx* ctx = set ? nullptr : context();
@@ -254,13 +282,25 @@ SolveReport run_gpu(const BatchedSystem& system, int strategy, std::optional<std
     SolveReport report;  // merge_groups, strategies.cpp:71-87
     report.strategy = kind;
     report.per_cell_x.resize(cells);
+    // pattern check (check()'s remaining test) and pack, one pass per cell;
+    // throws check()'s error for the lowest mismatching cell of [a, b)
     auto pack = [&](std::size_t a, std::size_t b) {
+        const std::size_t none = b;
+        std::mutex bad_mu;
+        std::size_t bad = none;
         parallel_for(b - a, threads, [&](std::size_t c0, std::size_t c1) {
             for (std::size_t c = a + c0; c < a + c1; ++c) {
-                std::memcpy(values + c * nnz, system.per_cell_matrices[c].values.data(), sizeof(double) * nnz);
+                const CsrMatrix& m = system.per_cell_matrices[c];
+                if (c > 0 && (m.row_ptr != first.row_ptr || m.col_idx != first.col_idx)) {
+                    std::lock_guard<std::mutex> lk(bad_mu);
+                    bad = std::min(bad, c);
+                    return;
+                }
+                std::memcpy(values + c * nnz, m.values.data(), sizeof(double) * nnz);
                 std::memcpy(rhs + c * s, system.per_cell_rhs[c].data(), sizeof(double) * s);
             }
         });
+        if (bad != none) throw std::invalid_argument("batched system: cells do not share one sparsity pattern");
     };
     auto unpack = [&](std::size_t a, std::size_t b) {
         parallel_for(b - a, threads, [&](std::size_t c0, std::size_t c1) {

@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <utility>
 #include <vector>
 
 #include "blockcells/strategies.hpp"
@@ -55,6 +56,26 @@ int main(int argc, char** argv) {
     }
     vals.clear();
     vals.shrink_to_fit();
+    // error-path checks (tests/test_dropin_overlap.py): a cell whose pattern
+    // differs and/or a cell whose rhs has the wrong size; run_strategy must
+    // throw what BatchedSystem::check (strategies.cpp:91-107) throws
+    const char* bad_pat = std::getenv("DROPIN_BAD_PATTERN_CELL");
+    const char* bad_rhs = std::getenv("DROPIN_BAD_RHS_CELL");
+    if (bad_pat || bad_rhs) {
+        if (bad_pat) std::swap(sys.per_cell_matrices[atol(bad_pat)].col_idx[0], sys.per_cell_matrices[atol(bad_pat)].col_idx[1]);
+        if (bad_rhs) sys.per_cell_rhs[atol(bad_rhs)].resize(species - 1);
+        StrategyConfig c1;
+        c1.kind = Strategy::BlockCells;
+        c1.cells_per_block = 1;
+        try {
+            run_strategy(sys, c1, DeviceSpec{}, tol, max_iter, workers);
+            std::printf("{\"error\": null}\n");
+        } catch (const std::invalid_argument& e) {
+            std::printf("{\"error\": \"%s\"}\n", e.what());
+        }
+        bcw_mechanism_destroy(m);
+        return 0;
+    }
     StrategyConfig cfg;
     cfg.kind = Strategy::BlockCells;
     cfg.cells_per_block = 1;

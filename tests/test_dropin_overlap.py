@@ -33,3 +33,23 @@ def test_overlapped_pieces_equal_one_call(algo, cells, regime):
     assert one["output_digest"] == pieces["output_digest"]
     assert one["iterations_sum"] == pieces["iterations_sum"]
     assert one["breakdown_fallbacks"] == pieces["breakdown_fallbacks"]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(BIN), reason="tests/cpp binaries not built (needs /root/reference at build time)")
+@pytest.mark.parametrize("overlap", ["0", "1"])
+@pytest.mark.parametrize("bad,want", [
+    ({"DROPIN_BAD_PATTERN_CELL": "19000"}, "batched system: cells do not share one sparsity pattern"),
+    ({"DROPIN_BAD_RHS_CELL": "5"}, "batched system: rhs dimension"),
+    # check() tests every matrix before any rhs: the later pattern error wins
+    ({"DROPIN_BAD_PATTERN_CELL": "19000", "DROPIN_BAD_RHS_CELL": "5"},
+     "batched system: cells do not share one sparsity pattern"),
+])
+def test_overlapped_pieces_raise_check_errors(overlap, bad, want):
+    """The piecewise pattern check throws BatchedSystem::check's exception
+    (strategies.cpp:91-107) for the lowest bad cell, with check()'s precedence."""
+    env = dict(os.environ, BLOCKCELLS_B200_OVERLAP=overlap, BLOCKCELLS_B200_ALGO="bicgstab", **bad)
+    r = subprocess.run([BIN, "20000", "1", "0", "156", "1.0", "1e-10", "50"], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert json.loads(r.stdout.strip().splitlines()[-1])["error"] == want
