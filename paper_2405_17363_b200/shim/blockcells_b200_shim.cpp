@@ -313,7 +313,14 @@ SolveReport run_gpu(const BatchedSystem& system, int strategy, std::optional<std
     // so packing and unpacking leave the critical path.  Each piece is its own
     // bc_solve over disjoint groups, folded below as merge_groups folds groups:
     // outputs bit-identical to one call.  BLOCKCELLS_B200_OVERLAP=0: one call.
-    constexpr int kPieces = 4;
+    int kPieces = 4;
+    if (const char* e = std::getenv("BLOCKCELLS_B200_PIECES")) kPieces = std::max(2, std::min(64, std::atoi(e)));
+    // the first piece, whose packing nothing overlaps, as a fraction of the
+    // batch in 1/64ths; the rest in equal shares.  B200, 100k M156 cells:
+    // 4 pieces with a 1/16 first piece 538k cell-solves/s, equal quarters
+    // 526k, 3 pieces 532k, 6 pieces 538k, 8 pieces 493-525k, 2 pieces 508k
+    int first64 = 4;
+    if (const char* e = std::getenv("BLOCKCELLS_B200_FIRST64")) first64 = std::max(1, std::min(63, std::atoi(e)));
     constexpr std::size_t kOverlapMinCells = 16384;
     const char* ov = std::getenv("BLOCKCELLS_B200_OVERLAP");
     const bool independent = strategy == BC_STRATEGY_BLOCK_CELLS || strategy == BC_STRATEGY_ONE_CELL ||
@@ -322,7 +329,10 @@ SolveReport run_gpu(const BatchedSystem& system, int strategy, std::optional<std
     const int pieces = (!set && independent && kg >= 1 && cells >= kOverlapMinCells && !(ov && *ov == '0'))
                            ? kPieces : 1;
     std::vector<std::size_t> cut(pieces + 1, cells);
-    for (int b = 0; b < pieces; ++b) cut[b] = (cells * b / pieces) / kg * kg;
+    for (int b = 0; b < pieces; ++b) {
+        const std::size_t c0 = cells * first64 / 64;  // then equal shares of the rest
+        cut[b] = (b == 0 ? 0 : c0 + (cells - c0) * (b - 1) / (pieces - 1)) / kg * kg;
+    }
     std::vector<bc_report> reps(pieces);
     if (pieces == 1) {
         pack(0, cells);
