@@ -31,6 +31,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -690,10 +691,25 @@ SolveOutcome bicg_solve(const CsrMatrix& a, const DenseVector& b, const DenseVec
     return single_system(b200::Algorithm::BiCG, a, b, x0, tol, max_iter, reduction);
 }
 
+// Every exit of the reference's bicg_solve ends with residual_rms(out.x)
+// (bicg.cpp:61-72, 126-141), so its ws.per_block_error holds the per-block
+// partials of the fresh residual (b - A x)^2 of the returned x.  x is bit-
+// identical here, so the same two reference functions over it (spmv,
+// csr.cpp:90-101; plan_reduce_map, reduction.hpp:60-79) give the same bits.
 SolveOutcome bicg_solve(const CsrMatrix& a, const DenseVector& b, const DenseVector& x0, double tol,
                         std::size_t max_iter, const ReductionPlan& reduction, BicgWorkspace& ws) {
-    ws.resize(a.n_rows, reduction.n_blocks());
-    return single_system(b200::Algorithm::BiCG, a, b, x0, tol, max_iter, reduction);
+    SolveOutcome out = single_system(b200::Algorithm::BiCG, a, b, x0, tol, max_iter, reduction);
+    const std::size_t n = a.n_rows;
+    ws.resize(n, reduction.n_blocks());
+    spmv(a, out.x, ws.ap);
+    plan_reduce_map(
+        n,
+        [&](std::size_t i) {
+            const double ri = b[i] - ws.ap[i];
+            return ri * ri;
+        },
+        reduction, ws.tree_scratch, std::span<double>(ws.per_block_error));
+    return out;
 }
 
 }  // namespace blockcells

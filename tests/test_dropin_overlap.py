@@ -53,3 +53,23 @@ def test_overlapped_pieces_raise_check_errors(overlap, bad, want):
                        text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert json.loads(r.stdout.strip().splitlines()[-1])["error"] == want
+
+
+WS_B200 = os.path.join(os.path.dirname(BIN), "ws_dump_b200")
+WS_REF = os.path.join(os.path.dirname(BIN), "ws_dump_reference")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not (os.path.exists(WS_B200) and os.path.exists(WS_REF)),
+                    reason="tests/cpp binaries not built (needs /root/reference at build time)")
+def test_bicg_workspace_outputs_equal_reference():
+    """bicg_solve(..., BicgWorkspace& ws) (bicg.hpp:42-48): x, iterations,
+    flags, final rms and ws.per_block_error (the per-block partials of the
+    final fresh residual, bicg.cpp:61-72) bit for bit, drop-in vs the
+    reference's own bicg.o, on one- and multi-block reduction plans, converged
+    and iteration-capped solves (tests/cpp/ws_dump.cpp)."""
+    ref = subprocess.run([WS_REF], capture_output=True, text=True, timeout=600)
+    got = subprocess.run([WS_B200], capture_output=True, text=True, timeout=600)
+    assert ref.returncode == 0 and got.returncode == 0, got.stderr[-2000:] + ref.stderr[-2000:]
+    assert ref.stdout.count("per_block_error") == 10
+    assert got.stdout == ref.stdout
