@@ -310,6 +310,9 @@ __global__ void __launch_bounds__(RV * 32, 1) block_cells_latency_kernel(const L
             if (!conv) {
                 double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
                 double aw = ddiv(alpha, omega);  // alpha/omega of beta, computed as soon as omega is known
+                double pt[RV];  // p - omega v of the next p update, formed as soon as omega is known
+#pragma unroll
+                for (int j = 0; j < RV; ++j) pt[j] = dsub(pv[j], dmul(omega, v[j]));
 #ifdef BC_LAT_PROFILE
                 long long prof_t = clock64(), prof_acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
@@ -320,7 +323,7 @@ __global__ void __launch_bounds__(RV * 32, 1) block_cells_latency_kernel(const L
                     double y[RV];
 #pragma unroll
                     for (int j = 0; j < RV; ++j) {
-                        pv[j] = dadd(r[j], dmul(beta, dsub(pv[j], dmul(omega, v[j]))));
+                        pv[j] = dadd(r[j], dmul(beta, pt[j]));
                         y[j] = dmul(dinv[j], pv[j]);
                     }
                     LAT_MARK(0);
@@ -368,6 +371,7 @@ __global__ void __launch_bounds__(RV * 32, 1) block_cells_latency_kernel(const L
                     for (int j = 0; j < RV; ++j) {
                         x[j] = dadd(x[j], dmul(omega, z[j]));
                         r[j] = dsub(r[j], dmul(omega, tv[j]));
+                        pt[j] = dsub(pv[j], dmul(omega, v[j]));  // the next p update's inner term
                     }
                     rho_prev = rho;
                     iters = it;
