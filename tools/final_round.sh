@@ -16,6 +16,10 @@ timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --mast
     bench.py --gpus 2 --cells 20000 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_n2_$TAG.json 2> gpurun_out/bench_n2_$TAG.err
 # small batches (latency kernel phase profile + sweep) and the Block-cells(N)
 # launch list (LU fallback share of the step)
+[ -x tools/latprof.bin ] || nvcc -gencode arch=compute_100a,code=sm_100a -O3 --fmad=false -std=c++17 --extended-lambda \
+    -DBC_LAT_PROFILE -I paper_2405_17363_b200/csrc -I include -o tools/latprof.bin tools/latprof.cu \
+    paper_2405_17363_b200/csrc/bc_latency_plan.cpp paper_2405_17363_b200/csrc/bc_plan.cpp -L paper_2405_17363_b200 \
+    -lbc_workload -Xlinker -rpath -Xlinker '$ORIGIN/../paper_2405_17363_b200'
 ./tools/latprof.bin > gpurun_out/latprof_$TAG.txt 2>&1
 CELLS=1,10,100,148,1000,10000 timeout 600 python tools/latency_sweep.py > gpurun_out/latsweep_$TAG.jsonl 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bcN_$TAG.csv \
