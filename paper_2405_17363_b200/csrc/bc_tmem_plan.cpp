@@ -19,6 +19,7 @@
 // ascending source row) and rows their values, so this changes speed only.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <numeric>
 #include <string>
@@ -651,6 +652,9 @@ TmemSchedule build_uncached(const Pattern& pat, int k, bool pair, int team, bool
         }
     ts.conflict_cost = cost;
     ts.model_total = o.total();
+    if (std::getenv("BC_PLAN_VERBOSE"))  // the model's unweighted terms
+        std::fprintf(stderr, "tmem plan n=%d k=%d pair=%d team=%d S=%d: gathers %d publishes %d yreads %d ystores %d "
+                     "total(weighted) %d\n", n, k, pair ? 1 : 0, team, o.S, o.gsum, o.pub, o.yrd, o.yst, o.total());
     if (ts.xslots * 8 > 0x7FFF) throw std::invalid_argument("TMEM schedule: gather vector too large");
     return ts;
 }
