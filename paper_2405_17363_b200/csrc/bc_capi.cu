@@ -327,7 +327,8 @@ const TmemCfg kTmemConfigs[] = {
     BC_TMEM_CFG(2, 4, 3, 16, 2, 2, kB),
     // four-warp teams for coupled Block-cells(k) groups of up to 1024 rows
     // (Block-cells(N) at M156: 936 rows, 2 groups per SM)
-    BC_TMEM_CFG(4, 8, 5, 8, 1, 2, kS), BC_TMEM_CFG(4, 8, 8, 8, 1, 2, kS), BC_TMEM_CFG(4, 8, 5, 4, 2, 2, kB),
+    BC_TMEM_CFG(4, 8, 5, 8, 1, 2, kS), BC_TMEM_CFG(4, 8, 8, 8, 1, 2, kS), BC_TMEM_CFG(4, 8, 8, 8, 2, 2, kS),
+    BC_TMEM_CFG(4, 8, 5, 4, 2, 2, kB),
     BC_TMEM_CFG(4, 8, 8, 4, 2, 2, kB),
 };
 #undef BC_TMEM_CFG

@@ -250,9 +250,12 @@ TmemSchedule build_uncached(const Pattern& pat, int k, bool pair, int team, bool
     // on steps 1, 3 (one stream) or 2, 3 (two streams) of a 4-step chunk
     constexpr int d = 2;
     // two interleaved accumulator chains per lane (BC_TMEM_STREAMS); four-warp
-    // teams use one, as their rows are already short (the longest row would
-    // set the step count)
-    int streams = team >= 4 ? 1 : 2;
+    // teams on groups of <= 512 rows use one, as their rows are already short
+    // (the longest row would set the step count).  Coupled groups above 512
+    // rows (Block-cells(N): 936) take two: B200, 100k M156 cells, BiCGSTAB P,
+    // 412k vs 394k cell-solves/s
+    const int n_rows = k * pat.species;
+    int streams = team >= 4 && n_rows <= 512 ? 1 : 2;
     if (const char* e = std::getenv("BC_TMEM_STREAMS")) streams = std::atoi(e) == 1 ? 1 : 2;
     if (pair) streams = 2;  // A on stream 0, A^T on stream 1
     const int s = pat.species, nnz = pat.nnz, n = k * s;

@@ -311,6 +311,27 @@ def test_tmem_schedule_reproduces_spmv_order(species, k, density, seed, pair, te
     assert sorted(used.tolist()) == sorted(list(range(k * nnz)) * (2 if pair else 1))
 
 
+@pytest.mark.parametrize("species,k", [(156, 6), (100, 8), (60, 17)])
+def test_tmem_schedule_coupled_team4_two_streams(species, k):
+    """Four-warp teams on coupled groups above 512 rows (Block-cells(N): 936 at
+    M156) run two row streams per lane: the walk still reproduces spmv's
+    per-row order (csr.cpp:90-101) bit for bit."""
+    rng = np.random.default_rng(species + k)
+    if species == 156:
+        m = Mechanism(156, 468, 0)
+        rp, ci = m.row_ptr, m.col_idx
+    else:
+        rp, ci, _, _ = random_batch(rng, 1, species, 0.1)
+    nnz = int(rp[-1])
+    sc = export_tmem_schedule(rp, ci, k, 0, 4)
+    assert sc["streams"] == 2 and sc["S"] % 4 == 0
+    vals = rng.uniform(-1, 1, k * nnz) * 10.0 ** rng.integers(-8, 8, k * nnz)
+    n = k * species
+    x = rng.uniform(-1, 1, n)
+    y = emulate_tmem_spmv(sc, vals, x)
+    np.testing.assert_array_equal(of.bits(y[:n]), of.bits(ref_spmv(rp, ci, vals, x, k, species, nnz)))
+
+
 # --- latency-mode schedule (bc_latency_plan.cpp) ------------------------------
 
 def export_latency_schedule(rp, ci, k, bicg, threads):
